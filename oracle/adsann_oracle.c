@@ -1,0 +1,695 @@
+/* oracle/adsann_oracle.c — TEST INFRASTRUCTURE ONLY.  See adsann_oracle.h.
+ *
+ * Each function cites the reference file:line it restates (paths relative
+ * to /root/reference/proj).  Written from the reference's documented
+ * behaviour; compiled with -ffp-contract=off so every multiply and add
+ * rounds separately, exactly as the reference's -O3 x86-64 build does.
+ */
+#include "adsann_oracle.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+static _Thread_local char g_err[256];
+
+static int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+const char *orc_last_error(void) { return g_err; }
+
+/* ------------------------------------------------------------------ rng
+ * rng.hpp:36-97.  Output i depends only on (seed, i). */
+static uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return z;
+}
+
+orc_rng orc_rng_make(uint64_t seed) {
+    orc_rng r = {seed, 0, 0.0, 0};
+    return r;
+}
+
+orc_rng orc_rng_for_stream(uint64_t seed, uint64_t tag) { return orc_rng_make(mix64(seed ^ tag)); }
+
+uint64_t orc_rng_next_u64(orc_rng *r) {
+    r->counter += 1;
+    return mix64(r->seed + r->counter * 0x9E3779B97F4A7C15ULL);
+}
+
+double orc_rng_uniform(orc_rng *r) { return (double)(orc_rng_next_u64(r) >> 11) * 0x1.0p-53; }
+
+double orc_rng_uniform_open0(orc_rng *r) {
+    return (double)((orc_rng_next_u64(r) >> 11) + 1) * 0x1.0p-53;
+}
+
+uint64_t orc_rng_below(orc_rng *r, uint64_t n) { return orc_rng_next_u64(r) % n; }
+
+/* rng.hpp:76-88: Box-Muller, cos variate returned first, sin variate cached. */
+double orc_rng_normal(orc_rng *r) {
+    if (r->has_cached) {
+        r->has_cached = 0;
+        return r->cached;
+    }
+    const double u1 = orc_rng_uniform_open0(r);
+    const double u2 = orc_rng_uniform(r);
+    const double mag = sqrt(-2.0 * log(u1));
+    const double ang = 6.283185307179586476925286766559 * u2;
+    r->cached = mag * sin(ang);
+    r->has_cached = 1;
+    return mag * cos(ang);
+}
+
+int orc_rng_draw(uint64_t seed, uint64_t tag, int use_stream, int kind, uint64_t arg,
+                 int64_t count, void *out) {
+    orc_rng r = use_stream ? orc_rng_for_stream(seed, tag) : orc_rng_make(seed);
+    for (int64_t i = 0; i < count; ++i) {
+        switch (kind) {
+            case 0: ((uint64_t *)out)[i] = orc_rng_next_u64(&r); break;
+            case 1: ((double *)out)[i] = orc_rng_uniform(&r); break;
+            case 2: ((double *)out)[i] = orc_rng_normal(&r); break;
+            default:
+                if (arg == 0) return fail(1, "below: n must be > 0");
+                ((uint64_t *)out)[i] = orc_rng_below(&r, arg);
+                break;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------ transform */
+#define TAG_TRANSFORM 0x9d5c41cf0f5e6a31ULL /* rng.hpp:27 */
+#define TAG_KMEANS 0x6b1febc8d1a07445ULL    /* rng.hpp:29 */
+
+static double dotd(const double *a, const double *b, int32_t n) {
+    double s = 0.0;
+    for (int32_t i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+
+/* transform.cpp:35-44: subtract projections on the already-orthonormal rows. */
+static void project_out(double *m, int32_t dim, int32_t i) {
+    double *v = m + (size_t)i * dim;
+    for (int32_t j = 0; j < i; ++j) {
+        const double *qj = m + (size_t)j * dim;
+        const double proj = dotd(v, qj, dim);
+        for (int32_t c = 0; c < dim; ++c) v[c] -= proj * qj[c];
+    }
+}
+
+/* transform.cpp:47-97 */
+int orc_generate_orthogonal(int32_t dim, uint64_t seed, double *out) {
+    if (dim < 1) return fail(1, "generate_orthogonal: dim must be >= 1");
+    orc_rng rng = orc_rng_for_stream(seed, TAG_TRANSFORM);
+    const size_t nn = (size_t)dim * dim;
+    for (size_t e = 0; e < nn; ++e) out[e] = orc_rng_normal(&rng);
+    for (int32_t i = 0; i < dim; ++i) {
+        double *v = out + (size_t)i * dim;
+        for (int attempt = 0;; ++attempt) {
+            project_out(out, dim, i);
+            project_out(out, dim, i);
+            const double norm = sqrt(dotd(v, v, dim));
+            if (norm > 1e-8) {
+                for (int32_t c = 0; c < dim; ++c) v[c] /= norm;
+                break;
+            }
+            if (attempt > 8) return fail(2, "generate_orthogonal: could not orthonormalize");
+            for (int32_t c = 0; c < dim; ++c) v[c] = orc_rng_normal(&rng);
+        }
+    }
+    double worst = 0.0;
+    for (int32_t i = 0; i < dim; ++i)
+        for (int32_t j = i; j < dim; ++j) {
+            const double g = dotd(out + (size_t)i * dim, out + (size_t)j * dim, dim);
+            const double dev = fabs(g - (i == j ? 1.0 : 0.0));
+            if (dev > worst) worst = dev;
+        }
+    if (worst > 1e-10) return fail(2, "generate_orthogonal: deviation %g exceeds 1e-10", worst);
+    return 0;
+}
+
+/* transform.cpp:103-117: y_i = sum_j P[i][j] * x_j, fp64, stored fp32. */
+int orc_apply_prefix(const double *P, int32_t dim, const float *x, int32_t d, float *y) {
+    if (d < 0 || d > dim) return fail(1, "apply_prefix: d out of range");
+    for (int32_t i = 0; i < d; ++i) {
+        const double *row = P + (size_t)i * dim;
+        double s = 0.0;
+        for (int32_t j = 0; j < dim; ++j) s += row[j] * (double)x[j];
+        y[i] = (float)s;
+    }
+    return 0;
+}
+
+/* transform.cpp:131-149 */
+int orc_apply_dataset(const double *P, int32_t dim, const float *X, int32_t n, float *Y) {
+    for (int64_t i = 0; i < n; ++i) orc_apply_prefix(P, dim, X + i * dim, dim, Y + i * dim);
+    return 0;
+}
+
+/* transform.cpp:119-129: acc[j] += P[i][j] * x_i, rows outer. */
+int orc_apply_transpose(const double *P, int32_t dim, const float *x, float *y) {
+    double *acc = calloc((size_t)dim, sizeof(double));
+    if (!acc) return fail(2, "oom");
+    for (int32_t i = 0; i < dim; ++i) {
+        const double *row = P + (size_t)i * dim;
+        const double xi = x[i];
+        for (int32_t j = 0; j < dim; ++j) acc[j] += row[j] * xi;
+    }
+    for (int32_t j = 0; j < dim; ++j) y[j] = (float)acc[j];
+    free(acc);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ dco */
+
+/* dco.cpp:63-68 */
+int orc_threshold_multiplier(int32_t d, double eps0, double *out) {
+    if (d < 1) return fail(1, "threshold_multiplier: d must be >= 1");
+    if (!(eps0 > 0.0)) return fail(1, "threshold_multiplier: epsilon0 must be > 0");
+    *out = 1.0 + eps0 / sqrt((double)d);
+    return 0;
+}
+
+/* dco.cpp:32-37 + 54-61: factor[k] = (1 + eps0/sqrt(k))^2 * k / D, factor[0] = 0. */
+int orc_ad_context(double eps0, int32_t delta_d, int32_t dim, double *factor) {
+    if (!(eps0 > 0.0)) return fail(1, "dco: epsilon0 must be > 0");
+    if (delta_d < 1 || delta_d > dim) return fail(1, "dco: delta_d must be in [1, D]");
+    factor[0] = 0.0;
+    for (int32_t k = 1; k < dim; ++k) {
+        const double mult = 1.0 + eps0 / sqrt((double)k);
+        factor[k] = mult * mult * (double)k / (double)dim;
+    }
+    return 0;
+}
+
+/* dco.hpp:86-93 */
+double orc_l2_sq(const float *a, const float *b, int32_t d) {
+    double s = 0.0;
+    for (int32_t i = 0; i < d; ++i) {
+        const double diff = (double)a[i] - (double)b[i];
+        s += diff * diff;
+    }
+    return s;
+}
+
+typedef struct {
+    int positive;
+    double dist_sq, observed;
+    int32_t dims;
+} scan_out;
+
+/* dco.hpp:122-148 (factor != NULL) and dco.hpp:152-177 (factor == NULL:
+ * the exact partial scan, i.e. the test against r^2 itself). */
+static scan_out scan(const float *data, const float *query, int32_t dim, int32_t d_start,
+                     double s_start, double r, const double *factor, int32_t delta_d,
+                     int test_at_start) {
+    const double r_sq = r * r;
+    double s = s_start;
+    int32_t d = d_start;
+    scan_out o;
+    if (test_at_start && d > 0 && d < dim && s > (factor ? factor[d] * r_sq : r_sq)) {
+        o.positive = 0;
+        o.dist_sq = 0.0;
+        o.observed = factor ? sqrt(s * dim / d) : sqrt(s);
+        o.dims = d;
+        return o;
+    }
+    while (d < dim) {
+        const int32_t stop = d + delta_d < dim ? d + delta_d : dim;
+        const float *a = data + (d - d_start);
+        const float *b = query + (d - d_start);
+        for (int32_t i = 0; i < stop - d; ++i) {
+            const double diff = (double)a[i] - (double)b[i];
+            s += diff * diff;
+        }
+        d = stop;
+        if (d < dim && s > (factor ? factor[d] * r_sq : r_sq)) {
+            o.positive = 0;
+            o.dist_sq = 0.0;
+            o.observed = factor ? sqrt(s * dim / d) : sqrt(s);
+            o.dims = d;
+            return o;
+        }
+    }
+    o.positive = s <= r_sq;
+    o.dist_sq = s;
+    o.observed = sqrt(s);
+    o.dims = dim;
+    return o;
+}
+
+int orc_scan_kernel(int kind, const float *data, const float *query, int32_t dim,
+                    int32_t d_start, double s_start, double r, double eps0, int32_t delta_d,
+                    int test_at_start, int *positive, double *dist_sq, double *observed,
+                    int *dims) {
+    double *factor = NULL;
+    if (kind == 0) {
+        factor = malloc(sizeof(double) * (size_t)(dim > 0 ? dim : 1));
+        const int rc = orc_ad_context(eps0, delta_d, dim, factor);
+        if (rc) {
+            free(factor);
+            return rc;
+        }
+    }
+    const scan_out o = scan(data, query, dim, d_start, s_start, r, factor, delta_d, test_at_start);
+    free(factor);
+    *positive = o.positive;
+    *dist_sq = o.dist_sq;
+    *observed = o.observed;
+    *dims = o.dims;
+    return 0;
+}
+
+/* dco.cpp:70-110 with validate_query dco.cpp:23-30 */
+int orc_dco(int kind, const float *o, int32_t n_o, const float *q, int32_t n_q, double r,
+            double eps0, int32_t delta_d, int *positive, double *distance, double *observed,
+            int *dims) {
+    if (n_o != n_q) return fail(1, "dco: vector lengths differ");
+    if (n_o == 0) return fail(1, "dco: empty vectors");
+    if (!(r >= 0.0) || !isfinite(r)) return fail(1, "dco: threshold must be finite and >= 0");
+    const int32_t dim = n_o;
+    if (kind == 0) { /* fd_scan */
+        const double s = orc_l2_sq(o, q, dim);
+        const double dist = sqrt(s);
+        *positive = dist <= r;
+        *observed = dist;
+        *dims = dim;
+        *distance = *positive ? dist : NAN;
+        return 0;
+    }
+    scan_out res;
+    if (kind == 1) { /* pd_scan */
+        if (delta_d < 1 || delta_d > dim) return fail(1, "pd_scan: delta_d must be in [1, D]");
+        res = scan(o, q, dim, 0, 0.0, r, NULL, delta_d, 0);
+    } else { /* ad_sampling */
+        double *factor = malloc(sizeof(double) * (size_t)dim);
+        const int rc = orc_ad_context(eps0, delta_d, dim, factor);
+        if (rc) {
+            free(factor);
+            return rc;
+        }
+        res = scan(o, q, dim, 0, 0.0, r, factor, delta_d, 0);
+        free(factor);
+    }
+    *positive = res.positive;
+    *observed = res.observed;
+    *dims = res.dims;
+    *distance = res.positive ? res.observed : NAN;
+    return 0;
+}
+
+int orc_ad_scan_pairs(const float *X, const float *Q, int32_t dim, int64_t npairs,
+                      const int64_t *rows, const int32_t *qidx, const double *r, double eps0,
+                      int32_t delta_d, int pd_mode, uint8_t *positive, int32_t *dims,
+                      double *dist_sq, double *observed) {
+    double *factor = NULL;
+    if (!pd_mode) {
+        factor = malloc(sizeof(double) * (size_t)dim);
+        const int rc = orc_ad_context(eps0, delta_d, dim, factor);
+        if (rc) {
+            free(factor);
+            return rc;
+        }
+    }
+    for (int64_t i = 0; i < npairs; ++i) {
+        const scan_out o = scan(X + rows[i] * dim, Q + (int64_t)qidx[i] * dim, dim, 0, 0.0, r[i],
+                                factor, delta_d, 0);
+        positive[i] = (uint8_t)o.positive;
+        dims[i] = o.dims;
+        dist_sq[i] = o.positive ? o.dist_sq : NAN;
+        observed[i] = o.observed;
+    }
+    free(factor);
+    return 0;
+}
+
+/* --------------------------------------------------------------- kmeans */
+
+/* ivf.cpp:36-60: nearest centroid, ties to the lowest index; objective is
+ * the sequential fp64 sum of the per-point minima. */
+static double assign_points(const float *X, int32_t n, int32_t d, const float *C, int32_t k,
+                            int32_t *assignment, double *best_d2) {
+    for (int64_t i = 0; i < n; ++i) {
+        const float *x = X + i * d;
+        double best = INFINITY;
+        int32_t arg = 0;
+        for (int32_t c = 0; c < k; ++c) {
+            const double d2 = orc_l2_sq(x, C + (int64_t)c * d, d);
+            if (d2 < best) {
+                best = d2;
+                arg = c;
+            }
+        }
+        assignment[i] = arg;
+        best_d2[i] = best;
+    }
+    double obj = 0.0;
+    for (int64_t i = 0; i < n; ++i) obj += best_d2[i];
+    return obj;
+}
+
+/* ivf.cpp:62-117: k-means++ seeding with a sequential fp64 CDF walk. */
+static void kmeanspp(const float *X, int32_t n, int32_t d, int32_t k, orc_rng *rng, float *C) {
+    double *min_d2 = malloc(sizeof(double) * (size_t)n);
+    char *chosen = calloc((size_t)n, 1);
+    for (int32_t i = 0; i < n; ++i) min_d2[i] = INFINITY;
+    int32_t pick = (int32_t)orc_rng_below(rng, (uint64_t)n);
+    for (int32_t c = 0;; ++c) {
+        chosen[pick] = 1;
+        memcpy(C + (int64_t)c * d, X + (int64_t)pick * d, sizeof(float) * (size_t)d);
+        if (c + 1 == k) break;
+        const float *cent = C + (int64_t)c * d;
+        for (int64_t i = 0; i < n; ++i) {
+            const double d2 = orc_l2_sq(X + i * d, cent, d);
+            if (d2 < min_d2[i]) min_d2[i] = d2;
+        }
+        double total = 0.0;
+        for (int32_t i = 0; i < n; ++i) total += min_d2[i];
+        pick = -1;
+        if (total > 0.0) {
+            const double u = orc_rng_uniform(rng) * total;
+            double cum = 0.0;
+            for (int32_t i = 0; i < n; ++i) {
+                cum += min_d2[i];
+                if (cum > u) {
+                    pick = i;
+                    break;
+                }
+            }
+            if (pick < 0)
+                for (int32_t i = n - 1; i >= 0; --i)
+                    if (min_d2[i] > 0.0) {
+                        pick = i;
+                        break;
+                    }
+        }
+        if (pick < 0) {
+            for (int32_t i = 0; i < n; ++i)
+                if (!chosen[i]) {
+                    pick = i;
+                    break;
+                }
+            if (pick < 0) pick = 0;
+        }
+    }
+    free(min_d2);
+    free(chosen);
+}
+
+/* ivf.cpp:121-190 */
+int orc_kmeans(const float *X, int32_t n, int32_t d, int32_t k, int max_iters, uint64_t seed,
+               float *centroids, int32_t *assignment, double *objective, int *iterations) {
+    if (k < 1) return fail(1, "kmeans: k must be >= 1");
+    if (k > n) return fail(1, "kmeans: k exceeds the number of points");
+    orc_rng rng = orc_rng_for_stream(seed, TAG_KMEANS);
+    kmeanspp(X, n, d, k, &rng, centroids);
+    double *best_d2 = malloc(sizeof(double) * (size_t)n);
+    double *sums = malloc(sizeof(double) * (size_t)k * d);
+    int64_t *counts = malloc(sizeof(int64_t) * (size_t)k);
+    char *stolen = malloc((size_t)n);
+    double prev_obj = INFINITY;
+    *iterations = 0;
+    for (int iter = 0; iter < max_iters; ++iter) {
+        const double obj = assign_points(X, n, d, centroids, k, assignment, best_d2);
+        *iterations = iter + 1;
+        memset(sums, 0, sizeof(double) * (size_t)k * d);
+        memset(counts, 0, sizeof(int64_t) * (size_t)k);
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t c = assignment[i];
+            double *s = sums + (int64_t)c * d;
+            for (int32_t j = 0; j < d; ++j) s[j] += X[i * d + j];
+            ++counts[c];
+        }
+        for (int32_t c = 0; c < k; ++c) {
+            if (counts[c] == 0) continue;
+            for (int32_t j = 0; j < d; ++j)
+                centroids[(int64_t)c * d + j] =
+                    (float)(sums[(int64_t)c * d + j] / (double)counts[c]);
+        }
+        memset(stolen, 0, (size_t)n);
+        for (int32_t c = 0; c < k; ++c) {
+            if (counts[c] != 0) continue;
+            double far_d2 = -1.0;
+            int32_t far_i = -1;
+            for (int32_t i = 0; i < n; ++i) {
+                if (stolen[i]) continue;
+                if (best_d2[i] > far_d2) {
+                    far_d2 = best_d2[i];
+                    far_i = i;
+                }
+            }
+            if (far_i < 0) continue;
+            stolen[far_i] = 1;
+            memcpy(centroids + (int64_t)c * d, X + (int64_t)far_i * d, sizeof(float) * (size_t)d);
+        }
+        if (prev_obj < INFINITY) {
+            const double denom = obj > 1e-30 ? obj : 1e-30;
+            if (fabs(prev_obj - obj) / denom < 1e-4) break;
+        }
+        prev_obj = obj;
+    }
+    *objective = assign_points(X, n, d, centroids, k, assignment, best_d2);
+    free(best_d2);
+    free(sums);
+    free(counts);
+    free(stolen);
+    return 0;
+}
+
+/* ----------------------------------------------------------- brute force */
+
+/* bench.cpp:31-61: the K smallest (d2, id) pairs, lexicographic, ascending. */
+int orc_brute_force_knn(const float *base, int32_t n, int32_t d, const float *queries,
+                        int32_t nq, int32_t K, int32_t *ids) {
+    if (K < 1) return fail(1, "brute_force_knn: K must be >= 1");
+    if (K > n) return fail(1, "brute_force_knn: K exceeds dataset size");
+    double *kd = malloc(sizeof(double) * (size_t)K);
+    int32_t *ki = malloc(sizeof(int32_t) * (size_t)K);
+    for (int64_t qi = 0; qi < nq; ++qi) {
+        const float *q = queries + qi * d;
+        int32_t cnt = 0;
+        for (int32_t i = 0; i < n; ++i) {
+            const double d2 = orc_l2_sq(base + (int64_t)i * d, q, d);
+            if (cnt == K && !(d2 < kd[K - 1] || (d2 == kd[K - 1] && i < ki[K - 1]))) continue;
+            int32_t pos = cnt < K ? cnt : K - 1;
+            while (pos > 0 && (kd[pos - 1] > d2 || (kd[pos - 1] == d2 && ki[pos - 1] > i))) {
+                kd[pos] = kd[pos - 1];
+                ki[pos] = ki[pos - 1];
+                --pos;
+            }
+            kd[pos] = d2;
+            ki[pos] = i;
+            if (cnt < K) ++cnt;
+        }
+        memcpy(ids + qi * K, ki, sizeof(int32_t) * (size_t)K);
+    }
+    free(kd);
+    free(ki);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ ivf */
+
+/* ivf.cpp:211-256 (layout only; clustering supplied by the caller). */
+int orc_ivf_layout(int32_t n, int32_t d, int32_t k, int32_t d1, int split, const double *P,
+                   const float *centroids_t, const int32_t *assignment, const float *raw,
+                   const float *t, int64_t *list_off, int32_t *ids_flat, float *vec_t,
+                   float *vec_raw, float *a1_t, float *a2_t, float *a1_raw, float *a2_raw,
+                   float *centroids_raw) {
+    if (split && (d1 < 1 || d1 >= d)) return fail(1, "build_ivf: split layout needs 1 <= d1 < D");
+    for (int32_t c = 0; c <= k; ++c) list_off[c] = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (assignment[i] < 0 || assignment[i] >= k) return fail(1, "layout: bad assignment");
+        list_off[assignment[i] + 1]++;
+    }
+    for (int32_t c = 0; c < k; ++c) list_off[c + 1] += list_off[c];
+    int64_t *fill = malloc(sizeof(int64_t) * (size_t)k);
+    memcpy(fill, list_off, sizeof(int64_t) * (size_t)k);
+    for (int32_t i = 0; i < n; ++i) ids_flat[fill[assignment[i]]++] = i; /* ascending ids */
+    free(fill);
+    const int32_t d2 = d - d1;
+    for (int64_t p = 0; p < n; ++p) {
+        const float *xt = t + (int64_t)ids_flat[p] * d;
+        const float *xr = raw + (int64_t)ids_flat[p] * d;
+        if (vec_t) memcpy(vec_t + p * d, xt, sizeof(float) * (size_t)d);
+        if (vec_raw) memcpy(vec_raw + p * d, xr, sizeof(float) * (size_t)d);
+        if (split) {
+            if (a1_t) memcpy(a1_t + p * d1, xt, sizeof(float) * (size_t)d1);
+            if (a2_t) memcpy(a2_t + p * d2, xt + d1, sizeof(float) * (size_t)d2);
+            if (a1_raw) memcpy(a1_raw + p * d1, xr, sizeof(float) * (size_t)d1);
+            if (a2_raw) memcpy(a2_raw + p * d2, xr + d1, sizeof(float) * (size_t)d2);
+        }
+    }
+    if (centroids_raw)
+        for (int32_t c = 0; c < k; ++c)
+            orc_apply_transpose(P, d, centroids_t + (int64_t)c * d, centroids_raw + (int64_t)c * d);
+    return 0;
+}
+
+typedef struct {
+    double dist;
+    int32_t id;
+} pair_t;
+
+static int pair_lt(pair_t a, pair_t b) { return a.dist < b.dist || (a.dist == b.dist && a.id < b.id); }
+
+/* ivf.cpp:283-292: (l2_sq(centroid, q), id) pairs, partial sort, first nprobe. */
+int orc_probe_order(const float *centroids, int32_t L, int32_t d, const float *q,
+                    int32_t nprobe, int32_t *order) {
+    pair_t *best = malloc(sizeof(pair_t) * (size_t)nprobe);
+    int32_t cnt = 0;
+    for (int32_t c = 0; c < L; ++c) {
+        pair_t p = {orc_l2_sq(centroids + (int64_t)c * d, q, d), c};
+        if (cnt == nprobe && !pair_lt(p, best[nprobe - 1])) continue;
+        int32_t pos = cnt < nprobe ? cnt : nprobe - 1;
+        while (pos > 0 && pair_lt(p, best[pos - 1])) {
+            best[pos] = best[pos - 1];
+            --pos;
+        }
+        best[pos] = p;
+        if (cnt < nprobe) ++cnt;
+    }
+    for (int32_t i = 0; i < nprobe; ++i) order[i] = best[i].id;
+    free(best);
+    return 0;
+}
+
+/* ivf.cpp:262-281: bounded max-heap keyed on (dist, id) pairs; kept here as
+ * an ascending array so that the back is priority_queue::top(). */
+typedef struct {
+    pair_t *a;
+    int32_t cnt, cap;
+} heap_t;
+
+static double heap_threshold(const heap_t *h) { return h->cnt < h->cap ? INFINITY : h->a[h->cnt - 1].dist; }
+
+static void heap_offer(heap_t *h, double dist, int32_t id) {
+    if (h->cnt == h->cap) {
+        if (!(dist < h->a[h->cnt - 1].dist)) return; /* strict: ties not inserted */
+        h->cnt--;                                    /* pop the max pair */
+    }
+    pair_t p = {dist, id};
+    int32_t pos = h->cnt;
+    while (pos > 0 && pair_lt(p, h->a[pos - 1])) {
+        h->a[pos] = h->a[pos - 1];
+        --pos;
+    }
+    h->a[pos] = p;
+    h->cnt++;
+}
+
+int orc_ivf_query(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                  int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
+                  int64_t step, int32_t *ids, double *dists, int32_t *count, uint64_t *stats) {
+    /* ivf.cpp:299-307 */
+    if (K < 1) return fail(1, "ivf_query: K must be >= 1");
+    if (nprobe < 1 || nprobe > idx->k_clusters)
+        return fail(1, "ivf_query: n_probe must be in [1, k_clusters]");
+    const int split_mode = mode == 3 || mode == 4;
+    if (split_mode && !idx->split) return fail(1, "ivf_query: split mode needs a split-layout index");
+    const int transformed = mode == 2 || mode == 3;
+    const float *q = transformed ? q_t : q_raw;
+    if (!q) return fail(1, "ivf_query: missing query vector");
+    if (first < 1 || step < 1) return fail(1, "ivf_query: bad threshold schedule");
+    const int32_t d = idx->d, d1 = idx->d1;
+
+    double *factor = NULL;
+    if (transformed) { /* ivf.cpp:313 */
+        factor = malloc(sizeof(double) * (size_t)d);
+        const int rc = orc_ad_context(eps0, delta_d, d, factor);
+        if (rc) {
+            free(factor);
+            return rc;
+        }
+    }
+    int32_t *probes = malloc(sizeof(int32_t) * (size_t)nprobe);
+    orc_probe_order(transformed ? idx->centroids_t : idx->centroids_raw, idx->k_clusters, d, q,
+                    nprobe, probes);
+
+    heap_t heap = {malloc(sizeof(pair_t) * (size_t)K), 0, K};
+    int64_t total = 0;
+    for (int32_t i = 0; i < nprobe; ++i) total += idx->list_off[probes[i] + 1] - idx->list_off[probes[i]];
+    pair_t *pending = malloc(sizeof(pair_t) * (size_t)(total > 0 ? total : 1));
+    int64_t npend = 0;
+    uint64_t dims = 0;
+    double r = INFINITY;
+
+    /* Split modes precompute the A1 prefix of every candidate first
+     * (ivf.cpp:366-386); contiguous modes scan in one pass. */
+    double *prefix = NULL;
+    if (split_mode) {
+        prefix = malloc(sizeof(double) * (size_t)(total > 0 ? total : 1));
+        const float *a1 = mode == 3 ? idx->a1_t : idx->a1_raw;
+        int64_t i = 0;
+        for (int32_t pi = 0; pi < nprobe; ++pi)
+            for (int64_t p = idx->list_off[probes[pi]]; p < idx->list_off[probes[pi] + 1]; ++p, ++i) {
+                double s = 0.0;
+                for (int32_t j = 0; j < d1; ++j) {
+                    const double diff = (double)a1[p * d1 + j] - (double)q[j];
+                    s += diff * diff;
+                }
+                prefix[i] = s;
+            }
+        dims += (uint64_t)total * (uint64_t)d1;
+    }
+
+    int64_t i = 0;
+    for (int32_t pi = 0; pi < nprobe; ++pi) {
+        const int32_t c = probes[pi];
+        for (int64_t p = idx->list_off[c]; p < idx->list_off[c + 1]; ++p, ++i) {
+            if (i == 0 || (i >= first && (i - first) % step == 0)) {
+                for (int64_t j = 0; j < npend; ++j) heap_offer(&heap, pending[j].dist, pending[j].id);
+                npend = 0;
+                r = heap_threshold(&heap); /* ivf.cpp:331, 391 */
+            }
+            const int32_t id = idx->ids_flat[p];
+            if (!split_mode) {
+                const float *vec = (transformed ? idx->vec_t : idx->vec_raw) + p * d;
+                if (mode == 0) { /* ivf.cpp:334-339 */
+                    const double s = orc_l2_sq(vec, q, d);
+                    dims += (uint64_t)d;
+                    const double dist = sqrt(s);
+                    if (dist <= r) pending[npend++] = (pair_t){dist, id};
+                } else {
+                    const scan_out o = scan(vec, q, d, 0, 0.0, r, mode == 2 ? factor : NULL,
+                                            delta_d, 0);
+                    dims += (uint64_t)o.dims;
+                    if (o.positive) pending[npend++] = (pair_t){o.observed, id};
+                }
+            } else { /* ivf.cpp:389-400 */
+                const float *a2 = mode == 3 ? idx->a2_t : idx->a2_raw;
+                const scan_out o = scan(a2 + p * (d - d1), q + d1, d, d1, prefix[i], r,
+                                        mode == 3 ? factor : NULL, delta_d, 1);
+                dims += (uint64_t)(o.dims - d1);
+                if (o.positive) pending[npend++] = (pair_t){o.observed, id};
+            }
+        }
+    }
+    for (int64_t j = 0; j < npend; ++j) heap_offer(&heap, pending[j].dist, pending[j].id);
+
+    *count = heap.cnt;
+    for (int32_t j = 0; j < heap.cnt; ++j) {
+        ids[j] = heap.a[j].id;
+        dists[j] = heap.a[j].dist;
+    }
+    stats[0] = dims;
+    stats[1] = (uint64_t)total;
+    stats[2] = (uint64_t)total;
+    free(factor);
+    free(probes);
+    free(heap.a);
+    free(pending);
+    free(prefix);
+    return 0;
+}

@@ -1,0 +1,1005 @@
+// C-ABI implementation (include/adsann_b200.h).  Host orchestration only:
+// argument validation with the reference's error classes, device buffers,
+// segment plans, and the kernel launch sequence.  No compute runs on the
+// host: every DCO, distance, transform, selection and k-means step is a
+// kernel in this library.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/adsann_b200.h"
+#include "engine.hpp"
+#include "host.hpp"
+
+namespace ads {
+void synth(const ads_synth_desc& s, float* out, int32_t* comp_out);
+
+int num_sms() {
+    int dev = 0;
+    ADS_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int v = 0;
+    ADS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev] = v;
+    return v;
+}
+}  // namespace ads
+
+using namespace ads;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return ADS_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return ADS_INVALID_ARGUMENT;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return ADS_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ADS_RUNTIME_ERROR;
+    }
+}
+
+void require(bool ok, const char* msg) {
+    if (!ok) throw std::invalid_argument(msg);
+}
+
+// Device buffer that only grows.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <typename T>
+    T* get(size_t count) {
+        const size_t need = sizeof(T) * (count > 0 ? count : 1);
+        if (need > bytes) {
+            if (p) ADS_CUDA(cudaFree(p));
+            p = nullptr;
+            ADS_CUDA(cudaMalloc(&p, need));
+            bytes = need;
+        }
+        return static_cast<T*>(p);
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+template <typename T>
+T* dev_upload(const T* h, size_t count, cudaStream_t st) {
+    T* d = nullptr;
+    ADS_CUDA(cudaMalloc(&d, sizeof(T) * (count > 0 ? count : 1)));
+    if (count) ADS_CUDA(cudaMemcpyAsync(d, h, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    return d;
+}
+}  // namespace
+
+struct ads_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    unsigned long long* counter = nullptr;
+    void* flush = nullptr;
+    size_t flush_bytes = 0;
+    std::mutex mu;
+    void use() const { ADS_CUDA(cudaSetDevice(device)); }
+};
+
+struct ads_transform {
+    ads_ctx* ctx = nullptr;
+    int dim = 0;
+    double* P = nullptr;
+    double* PT = nullptr;
+    DevBuf xin, yout;
+};
+
+struct PlanKey {
+    int mode;
+    double eps0;
+    int dd;
+    bool operator<(const PlanKey& o) const {
+        return std::tie(mode, eps0, dd) < std::tie(o.mode, o.eps0, o.dd);
+    }
+};
+
+struct ads_ivf {
+    ads_ctx* ctx = nullptr;
+    int n = 0, d = 0, k = 0, d1 = 0, layout = 0, d1p = 0;
+    uint64_t seed = 0;
+    bool has_raw = false;
+    float *cent_t = nullptr, *cent_raw = nullptr;
+    int64_t* list_off = nullptr;
+    int32_t* ids = nullptr;
+    float *a1_t = nullptr, *a2_t = nullptr, *a1_raw = nullptr, *a2_raw = nullptr;
+    double* P = nullptr;
+    std::map<PlanKey, std::unique_ptr<DevSegPlan>> plans;
+    DevBuf dist, probes, qrot, qin_t, qin_raw, o_ids, o_dists, o_cnt, o_dims, o_cand;
+    cudaEvent_t ev[5] = {};
+    float last_ms[4] = {0, 0, 0, 0};
+    bool timed = false;
+    ~ads_ivf() {
+        for (void* p : {static_cast<void*>(cent_t), static_cast<void*>(cent_raw),
+                        static_cast<void*>(list_off), static_cast<void*>(ids),
+                        static_cast<void*>(a1_t), static_cast<void*>(a2_t),
+                        static_cast<void*>(a1_raw), static_cast<void*>(a2_raw),
+                        static_cast<void*>(P)})
+            if (p) cudaFree(p);
+        for (auto& kv : plans) kv.second->release();
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+extern "C" {
+
+const char* ads_last_error(void) { return g_err.c_str(); }
+int ads_version(void) { return 1; }
+
+int ads_device_count(int32_t* count) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    *count = n;
+    return ADS_OK;
+}
+
+int ads_rng_draw(uint64_t seed, uint64_t tag, int32_t use_stream, int32_t kind, uint64_t arg,
+                 int64_t count, void* out) {
+    return guard([&] {
+        HostRng r = use_stream ? HostRng::for_stream(seed, tag) : HostRng(seed);
+        for (int64_t i = 0; i < count; ++i) {
+            switch (kind) {
+                case 0: static_cast<uint64_t*>(out)[i] = r.next_u64(); break;
+                case 1: static_cast<double*>(out)[i] = r.uniform(); break;
+                case 2: static_cast<double*>(out)[i] = r.normal(); break;
+                default:
+                    require(arg > 0, "below: n must be > 0");
+                    static_cast<uint64_t*>(out)[i] = r.below(arg);
+            }
+        }
+    });
+}
+
+int ads_generate_orthogonal(int32_t dim, uint64_t seed, double* P_out) {
+    return guard([&] {
+        const std::vector<double> m = generate_orthogonal(dim, seed);
+        std::memcpy(P_out, m.data(), m.size() * sizeof(double));
+    });
+}
+
+int ads_threshold_multiplier(int32_t d, double eps0, double* out) {
+    return guard([&] {
+        require(d >= 1, "threshold_multiplier: d must be >= 1");
+        require(eps0 > 0.0, "threshold_multiplier: epsilon0 must be > 0");
+        *out = 1.0 + eps0 / std::sqrt(static_cast<double>(d));
+    });
+}
+
+int ads_ad_context(double eps0, int32_t delta_d, int32_t dim, double* factor_out) {
+    return guard([&] {
+        const std::vector<double> f = ad_factor(eps0, delta_d, dim);
+        std::memcpy(factor_out, f.data(), f.size() * sizeof(double));
+    });
+}
+
+int ads_synth(const ads_synth_desc* desc, float* out, int32_t* comp_out) {
+    return guard([&] { synth(*desc, out, comp_out); });
+}
+
+// ------------------------------------------------------------------ context
+int ads_ctx_create(int32_t device, ads_ctx** out) {
+    return guard([&] {
+        int n = 0;
+        ADS_CUDA(cudaGetDeviceCount(&n));
+        require(device >= 0 && device < n, "ads_ctx_create: no such CUDA device");
+        auto c = std::make_unique<ads_ctx>();
+        c->device = device;
+        c->use();
+        ADS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        ADS_CUDA(cudaEventCreate(&c->t0));
+        ADS_CUDA(cudaEventCreate(&c->t1));
+        ADS_CUDA(cudaMalloc(&c->counter, sizeof(unsigned long long) * 4));
+        *out = c.release();
+    });
+}
+
+int ads_ctx_destroy(ads_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        ctx->use();
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->flush) cudaFree(ctx->flush);
+        cudaFree(ctx->counter);
+        cudaEventDestroy(ctx->t0);
+        cudaEventDestroy(ctx->t1);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int ads_ctx_sync(ads_ctx* ctx) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ads_dev_alloc(ads_ctx* ctx, int64_t bytes, void** dptr) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaMalloc(dptr, static_cast<size_t>(bytes > 0 ? bytes : 1)));
+    });
+}
+int ads_dev_free(ads_ctx* ctx, void* dptr) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaStreamSynchronize(ctx->stream));
+        ADS_CUDA(cudaFree(dptr));
+    });
+}
+int ads_memcpy_h2d(ads_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        ADS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int ads_memcpy_d2h(ads_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        ADS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int ads_memset_device(ads_ctx* ctx, void* dst, int32_t value, int64_t bytes) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+    });
+}
+int ads_host_alloc_pinned(int64_t bytes, void** hptr) {
+    return guard([&] { ADS_CUDA(cudaMallocHost(hptr, static_cast<size_t>(bytes > 0 ? bytes : 1))); });
+}
+int ads_host_free_pinned(void* hptr) {
+    return guard([&] { ADS_CUDA(cudaFreeHost(hptr)); });
+}
+int ads_timer_start(ads_ctx* ctx) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaEventRecord(ctx->t0, ctx->stream));
+    });
+}
+int ads_timer_stop(ads_ctx* ctx, float* ms) {
+    return guard([&] {
+        ctx->use();
+        ADS_CUDA(cudaEventRecord(ctx->t1, ctx->stream));
+        ADS_CUDA(cudaEventSynchronize(ctx->t1));
+        ADS_CUDA(cudaEventElapsedTime(ms, ctx->t0, ctx->t1));
+    });
+}
+int ads_flush_l2(ads_ctx* ctx) {
+    return guard([&] {
+        ctx->use();
+        if (!ctx->flush) {
+            int l2 = 0;
+            ADS_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
+            ctx->flush_bytes = static_cast<size_t>(l2) * 2;
+            ADS_CUDA(cudaMalloc(&ctx->flush, ctx->flush_bytes));
+        }
+        ADS_CUDA(cudaMemsetAsync(ctx->flush, 0x5a, ctx->flush_bytes, ctx->stream));
+    });
+}
+
+// ------------------------------------------------------------------ transform
+int ads_transform_create(ads_ctx* ctx, const double* P_host, int32_t dim, ads_transform** out) {
+    return guard([&] {
+        require(dim >= 1, "transform: dim must be >= 1");
+        ctx->use();
+        auto t = std::make_unique<ads_transform>();
+        t->ctx = ctx;
+        t->dim = dim;
+        std::vector<double> PT(static_cast<size_t>(dim) * dim);
+        for (int i = 0; i < dim; ++i)
+            for (int j = 0; j < dim; ++j) PT[static_cast<size_t>(j) * dim + i] = P_host[static_cast<size_t>(i) * dim + j];
+        t->P = dev_upload(P_host, PT.size(), ctx->stream);
+        t->PT = dev_upload(PT.data(), PT.size(), ctx->stream);
+        ADS_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = t.release();
+    });
+}
+
+int ads_transform_destroy(ads_transform* t) {
+    return guard([&] {
+        if (!t) return;
+        t->ctx->use();
+        cudaFree(t->P);
+        cudaFree(t->PT);
+        delete t;
+    });
+}
+
+static void apply_host(ads_transform* t, const double* M, const float* X, int64_t n, float* Y) {
+    require(n >= 0, "apply: n must be >= 0");
+    ads_ctx* c = t->ctx;
+    c->use();
+    std::lock_guard<std::mutex> lk(c->mu);
+    const size_t cnt = static_cast<size_t>(n) * t->dim;
+    float* dx = t->xin.get<float>(cnt);
+    float* dy = t->yout.get<float>(cnt);
+    ADS_CUDA(cudaMemcpyAsync(dx, X, cnt * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    launch_apply(M, t->dim, dx, n, dy, c->stream);
+    ADS_CUDA(cudaMemcpyAsync(Y, dy, cnt * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    ADS_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+int ads_apply_dataset(ads_transform* t, const float* X, int64_t n, float* Y) {
+    return guard([&] { apply_host(t, t->P, X, n, Y); });
+}
+int ads_apply_transpose(ads_transform* t, const float* X, int64_t n, float* Y) {
+    return guard([&] { apply_host(t, t->PT, X, n, Y); });
+}
+int ads_apply_dataset_device(ads_transform* t, const float* dX, int64_t n, float* dY) {
+    return guard([&] {
+        t->ctx->use();
+        launch_apply(t->P, t->dim, dX, n, dY, t->ctx->stream);
+    });
+}
+int ads_apply_transpose_device(ads_transform* t, const float* dX, int64_t n, float* dY) {
+    return guard([&] {
+        t->ctx->use();
+        launch_apply(t->PT, t->dim, dX, n, dY, t->ctx->stream);
+    });
+}
+
+// ------------------------------------------------------------------ fixed-threshold DCOs
+namespace {
+
+SegPlan dco_plan(int kind, int D, double eps0, int dd) {
+    if (kind == ADS_DCO_FD) return make_seg_plan(D, 0, {}, nullptr);
+    require(dd >= 1 && dd <= D, "dco: delta_d must be in [1, D]");
+    const std::vector<int> tests = test_points(D, dd, 0, false);
+    if (kind == ADS_DCO_PD) return make_seg_plan(D, 0, tests, nullptr);
+    const std::vector<double> f = ad_factor(eps0, dd, D);
+    return make_seg_plan(D, 0, tests, f.data());
+}
+
+void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int64_t>* host_off) {
+    require(b.dim >= 1, "dco: dimension must be >= 1");
+    require(b.nq >= 0, "dco: nq must be >= 0");
+    require(b.kind >= 0 && b.kind <= 2, "dco: unknown kind");
+    const SegPlan plan = dco_plan(b.kind, b.dim, b.epsilon0, b.delta_d);
+    cudaStream_t st = ctx->stream;
+    DevSegPlan dp;
+    dp.upload(plan, st);
+    DcoLaunch a{};
+    a.X = b.X;
+    a.n_rows = b.n_rows;
+    a.D = b.dim;
+    a.Q = b.Q;
+    a.nq = b.nq;
+    a.cand_off = b.cand_off;
+    a.cand_rows = b.cand_rows;
+    a.win_start = b.win_start;
+    a.win_len = b.win_len;
+    a.r = b.r;
+    a.kind = b.kind;
+    a.segs = dp.segs;
+    a.tfac = dp.tfac;
+    a.nseg = dp.nseg;
+    a.ntest = dp.ntest;
+    a.vec = dp.vec;
+    a.positive = b.positive;
+    a.dims = b.dims;
+    a.dist_sq = b.dist_sq;
+    a.observed = b.observed;
+    a.dims_per_query = reinterpret_cast<unsigned long long*>(b.dims_per_query);
+    a.counter = ctx->counter;
+    constexpr int64_t kTile = 2048;
+    a.tile = kTile;
+    int64_t* dt = nullptr;
+    if (b.cand_rows) {
+        require(host_off != nullptr, "dco: candidate offsets missing");
+        std::vector<int64_t> tq, tl, th;
+        for (int q = 0; q < b.nq; ++q) {
+            const int64_t cnt = (*host_off)[q + 1] - (*host_off)[q];
+            require(cnt >= 0, "dco: cand_off must be non-decreasing");
+            require(cnt < (int64_t(1) << 31), "dco: too many candidates for one query");
+            for (int64_t lo = 0; lo < cnt; lo += kTile) {
+                tq.push_back(q);
+                tl.push_back(lo);
+                th.push_back(lo + kTile < cnt ? lo + kTile : cnt);
+            }
+        }
+        a.ntiles = static_cast<int64_t>(tq.size());
+        std::vector<int64_t> all;
+        all.insert(all.end(), tq.begin(), tq.end());
+        all.insert(all.end(), tl.begin(), tl.end());
+        all.insert(all.end(), th.begin(), th.end());
+        dt = dev_upload(all.data(), all.size(), st);
+        a.tile_q = dt;
+        a.tile_lo = dt + a.ntiles;
+        a.tile_hi = dt + 2 * a.ntiles;
+    } else {
+        require(b.win_start != nullptr && b.win_len >= 0, "dco: need cand_rows or windows");
+        require(b.win_len < (int64_t(1) << 31), "dco: window too long");
+        require(b.win_len == 0 || b.n_rows >= 1, "dco: empty database");
+        a.ntiles = b.win_len > 0 ? static_cast<int64_t>(b.nq) * ((b.win_len + kTile - 1) / kTile) : 0;
+    }
+    if (b.dims_per_query) ADS_CUDA(cudaMemsetAsync(b.dims_per_query, 0, sizeof(uint64_t) * b.nq, st));
+    if (a.ntiles > 0) launch_dco_fixed(a, st);
+    ADS_CUDA(cudaStreamSynchronize(st));  // dp / tile table are freed below
+    if (dt) cudaFree(dt);
+    dp.release();
+}
+
+}  // namespace
+
+int ads_dco_fixed_device(ads_ctx* ctx, const ads_dco_batch* b) {
+    return guard([&] {
+        ctx->use();
+        std::vector<int64_t> off;
+        if (b->cand_rows) {
+            off.resize(static_cast<size_t>(b->nq) + 1);
+            ADS_CUDA(cudaMemcpyAsync(off.data(), b->cand_off, sizeof(int64_t) * off.size(),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+            ADS_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        run_dco_device(ctx, *b, b->cand_rows ? &off : nullptr);
+    });
+}
+
+int ads_dco_fixed(ads_ctx* ctx, const ads_dco_batch* hb) {
+    return guard([&] {
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        const ads_dco_batch& b = *hb;
+        require(b.dim >= 1 && b.nq >= 0 && b.n_rows >= 0, "dco: bad shape");
+        int64_t total = 0;
+        std::vector<int64_t> off;
+        if (b.cand_rows) {
+            off.assign(b.cand_off, b.cand_off + b.nq + 1);
+            total = off[b.nq] - off[0];
+            require(off[0] == 0, "dco: cand_off[0] must be 0");
+            for (int64_t i = 0; i < total; ++i)
+                require(b.cand_rows[i] >= 0 && b.cand_rows[i] < b.n_rows, "dco: candidate row out of range");
+        } else {
+            require(b.win_start != nullptr, "dco: need cand_rows or windows");
+            total = static_cast<int64_t>(b.nq) * b.win_len;
+            for (int q = 0; q < b.nq; ++q)
+                require(b.win_start[q] >= 0 && b.win_start[q] < (b.n_rows > 0 ? b.n_rows : 1),
+                        "dco: window start out of range");
+        }
+        ads_dco_batch d = b;
+        std::vector<void*> owned;
+        auto up = [&](const void* h, size_t bytes) -> void* {
+            void* p = nullptr;
+            ADS_CUDA(cudaMalloc(&p, bytes > 0 ? bytes : 1));
+            if (bytes) ADS_CUDA(cudaMemcpyAsync(p, h, bytes, cudaMemcpyHostToDevice, st));
+            owned.push_back(p);
+            return p;
+        };
+        auto alloc = [&](size_t bytes) -> void* {
+            void* p = nullptr;
+            ADS_CUDA(cudaMalloc(&p, bytes > 0 ? bytes : 1));
+            owned.push_back(p);
+            return p;
+        };
+        try {
+            d.X = static_cast<const float*>(up(b.X, sizeof(float) * b.n_rows * b.dim));
+            d.Q = static_cast<const float*>(up(b.Q, sizeof(float) * b.nq * static_cast<size_t>(b.dim)));
+            d.r = static_cast<const double*>(up(b.r, sizeof(double) * b.nq));
+            if (b.cand_rows) {
+                d.cand_off = static_cast<const int64_t*>(up(b.cand_off, sizeof(int64_t) * (b.nq + 1)));
+                d.cand_rows = static_cast<const int64_t*>(up(b.cand_rows, sizeof(int64_t) * total));
+            } else {
+                d.win_start = static_cast<const int64_t*>(up(b.win_start, sizeof(int64_t) * b.nq));
+            }
+            d.positive = b.positive ? static_cast<uint8_t*>(alloc(total)) : nullptr;
+            d.dims = b.dims ? static_cast<int32_t*>(alloc(sizeof(int32_t) * total)) : nullptr;
+            d.dist_sq = b.dist_sq ? static_cast<double*>(alloc(sizeof(double) * total)) : nullptr;
+            d.observed = b.observed ? static_cast<double*>(alloc(sizeof(double) * total)) : nullptr;
+            d.dims_per_query = b.dims_per_query ? static_cast<uint64_t*>(alloc(sizeof(uint64_t) * b.nq)) : nullptr;
+            run_dco_device(ctx, d, b.cand_rows ? &off : nullptr);
+            auto down = [&](void* h, const void* dv, size_t bytes) {
+                if (h && bytes) ADS_CUDA(cudaMemcpyAsync(h, dv, bytes, cudaMemcpyDeviceToHost, st));
+            };
+            down(b.positive, d.positive, total);
+            down(b.dims, d.dims, sizeof(int32_t) * total);
+            down(b.dist_sq, d.dist_sq, sizeof(double) * total);
+            down(b.observed, d.observed, sizeof(double) * total);
+            down(b.dims_per_query, d.dims_per_query, sizeof(uint64_t) * b.nq);
+            ADS_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaStreamSynchronize(st);
+            for (void* p : owned) cudaFree(p);
+            throw;
+        }
+        for (void* p : owned) cudaFree(p);
+    });
+}
+
+int ads_dco(ads_ctx* ctx, int32_t kind, const float* o, int32_t n_o, const float* q, int32_t n_q,
+            double r, double eps0, int32_t delta_d, int32_t* positive, double* distance,
+            double* observed, int32_t* dims_used) {
+    return guard([&] {
+        // validate_query (dco.cpp:23-30), then the per-kind checks (dco.cpp:86-87, 32-37).
+        require(n_o == n_q, "dco: vector lengths differ");
+        require(n_o > 0, "dco: empty vectors");
+        require(r >= 0.0 && std::isfinite(r), "dco: threshold must be finite and >= 0");
+        require(kind >= 0 && kind <= 2, "dco: unknown kind");
+        if (kind == ADS_DCO_PD) require(delta_d >= 1 && delta_d <= n_o, "pd_scan: delta_d must be in [1, D]");
+        if (kind == ADS_DCO_AD) (void)ad_factor(eps0, delta_d, n_o);
+        ads_dco_batch b{};
+        const int64_t off[2] = {0, 1};
+        const int64_t rows[1] = {0};
+        b.X = o;
+        b.n_rows = 1;
+        b.dim = n_o;
+        b.Q = q;
+        b.nq = 1;
+        b.cand_off = off;
+        b.cand_rows = rows;
+        b.r = &r;
+        b.kind = kind;
+        b.epsilon0 = eps0;
+        b.delta_d = kind == ADS_DCO_FD ? n_o : delta_d;
+        uint8_t pos = 0;
+        int32_t dims = 0;
+        double obs = 0.0;
+        b.positive = &pos;
+        b.dims = &dims;
+        b.observed = &obs;
+        const int rc = ads_dco_fixed(ctx, &b);
+        if (rc != ADS_OK) throw std::runtime_error(g_err);
+        *positive = pos;
+        *observed = obs;
+        *dims_used = dims;
+        *distance = pos ? obs : std::nan("");
+    });
+}
+
+// ------------------------------------------------------------------ exact k-NN
+int ads_brute_force_knn_device(ads_ctx* ctx, const float* dbase, int64_t n, int32_t d,
+                               const float* dqueries, int32_t nq, int32_t K, int32_t* dids) {
+    return guard([&] {
+        require(K >= 1, "brute_force_knn: K must be >= 1");
+        require(K <= n, "brute_force_knn: K exceeds dataset size");
+        ctx->use();
+        launch_brute_knn(dbase, n, d, dqueries, nq, K, dids, ctx->stream);
+    });
+}
+
+int ads_brute_force_knn(ads_ctx* ctx, const float* base, int64_t n, int32_t d,
+                        const float* queries, int32_t nq, int32_t K, int32_t* ids) {
+    return guard([&] {
+        require(K >= 1, "brute_force_knn: K must be >= 1");
+        require(K <= n, "brute_force_knn: K exceeds dataset size");
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        float* db = dev_upload(base, static_cast<size_t>(n) * d, st);
+        float* dq = dev_upload(queries, static_cast<size_t>(nq) * d, st);
+        int32_t* di = nullptr;
+        ADS_CUDA(cudaMalloc(&di, sizeof(int32_t) * (static_cast<size_t>(nq) * K + 1)));
+        launch_brute_knn(db, n, d, dq, nq, K, di, st);
+        ADS_CUDA(cudaMemcpyAsync(ids, di, sizeof(int32_t) * nq * K, cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        cudaFree(db);
+        cudaFree(dq);
+        cudaFree(di);
+    });
+}
+
+// ------------------------------------------------------------------ k-means
+int ads_kmeans(ads_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k, int32_t max_iters,
+               uint64_t seed, int32_t init, float* centroids, int32_t* assignment, double* objective,
+               int32_t* iterations) {
+    return guard([&] {
+        require(k >= 1, "kmeans: k must be >= 1");
+        require(k <= n, "kmeans: k exceeds the number of points");
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        float* dx = dev_upload(X, static_cast<size_t>(n) * d, st);
+        float* dc = nullptr;
+        int32_t* da = nullptr;
+        ADS_CUDA(cudaMalloc(&dc, sizeof(float) * k * static_cast<size_t>(d)));
+        ADS_CUDA(cudaMalloc(&da, sizeof(int32_t) * n));
+        KmeansOut o{};
+        try {
+            o = run_kmeans(dx, n, d, k, max_iters, seed, init, dc, da, st);
+        } catch (...) {
+            cudaFree(dx);
+            cudaFree(dc);
+            cudaFree(da);
+            throw;
+        }
+        ADS_CUDA(cudaMemcpyAsync(centroids, dc, sizeof(float) * k * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaMemcpyAsync(assignment, da, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        cudaFree(dx);
+        cudaFree(dc);
+        cudaFree(da);
+        *objective = o.objective;
+        *iterations = o.iterations;
+    });
+}
+
+// ------------------------------------------------------------------ IVF
+static void ivf_alloc_common(ads_ivf* x) {
+    for (auto& e : x->ev) ADS_CUDA(cudaEventCreate(&e));
+}
+
+int ads_ivf_create(ads_ctx* ctx, const ads_ivf_desc* desc, ads_ivf** out) {
+    return guard([&] {
+        const ads_ivf_desc& s = *desc;
+        require(s.n >= 1 && s.d >= 1 && s.k_clusters >= 1, "ivf: bad shape");
+        require(s.centroids_t && s.list_off && s.ids_flat, "ivf: missing arrays");
+        require(s.a1_t || s.vec_t, "ivf: missing transformed vectors");
+        if (s.layout == 1) require(s.d1 >= 1 && s.d1 < s.d, "build_ivf: split layout needs 1 <= d1 < D");
+        require(s.list_off[0] == 0 && s.list_off[s.k_clusters] == s.n, "ivf: list offsets do not cover n");
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        auto x = std::make_unique<ads_ivf>();
+        x->ctx = ctx;
+        x->n = s.n;
+        x->d = s.d;
+        x->k = s.k_clusters;
+        x->d1 = s.d1;
+        x->layout = s.layout;
+        x->seed = s.seed;
+        ivf_alloc_common(x.get());
+        const int D = s.d;
+        x->d1p = s.a1_t ? s.d1 : (s.layout == 1 ? s.d1 : (D > 32 ? 32 : D));
+        const int d1p = x->d1p, d2p = D - d1p;
+        const size_t n = static_cast<size_t>(s.n);
+        x->cent_t = dev_upload(s.centroids_t, static_cast<size_t>(s.k_clusters) * D, st);
+        x->list_off = dev_upload(s.list_off, static_cast<size_t>(s.k_clusters) + 1, st);
+        x->ids = dev_upload(s.ids_flat, n, st);
+        auto split_up = [&](const float* a1, const float* a2, const float* vec, float** o1, float** o2) {
+            ADS_CUDA(cudaMalloc(o1, sizeof(float) * n * d1p));
+            ADS_CUDA(cudaMalloc(o2, sizeof(float) * (n * d2p > 0 ? n * d2p : 1)));
+            if (a1) {
+                ADS_CUDA(cudaMemcpyAsync(*o1, a1, sizeof(float) * n * d1p, cudaMemcpyHostToDevice, st));
+                if (d2p) ADS_CUDA(cudaMemcpyAsync(*o2, a2, sizeof(float) * n * d2p, cudaMemcpyHostToDevice, st));
+            } else {
+                ADS_CUDA(cudaMemcpy2DAsync(*o1, sizeof(float) * d1p, vec, sizeof(float) * D,
+                                           sizeof(float) * d1p, n, cudaMemcpyHostToDevice, st));
+                if (d2p)
+                    ADS_CUDA(cudaMemcpy2DAsync(*o2, sizeof(float) * d2p, vec + d1p, sizeof(float) * D,
+                                               sizeof(float) * d2p, n, cudaMemcpyHostToDevice, st));
+            }
+        };
+        split_up(s.a1_t, s.a2_t, s.vec_t, &x->a1_t, &x->a2_t);
+        if ((s.a1_raw || s.vec_raw) && s.centroids_raw) {
+            x->has_raw = true;
+            x->cent_raw = dev_upload(s.centroids_raw, static_cast<size_t>(s.k_clusters) * D, st);
+            split_up(s.a1_raw, s.a2_raw, s.vec_raw, &x->a1_raw, &x->a2_raw);
+        }
+        if (s.P) x->P = dev_upload(s.P, static_cast<size_t>(D) * D, st);
+        ADS_CUDA(cudaStreamSynchronize(st));
+        *out = x.release();
+    });
+}
+
+int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int32_t d,
+                  const double* P, int32_t k, uint64_t seed, int32_t layout, int32_t d1,
+                  int32_t max_iters, int32_t init, ads_ivf** out) {
+    return guard([&] {
+        // ivf.cpp:195-200
+        require(n >= 1 && d >= 1, "build_ivf: bad shape");
+        require(P != nullptr, "build_ivf: matrix dimension does not match the data");
+        if (layout == 1) require(d1 >= 1 && d1 < d, "build_ivf: split layout needs 1 <= d1 < D");
+        require(k >= 1, "kmeans: k must be >= 1");
+        require(k <= n, "kmeans: k exceeds the number of points");
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        auto x = std::make_unique<ads_ivf>();
+        x->ctx = ctx;
+        x->n = n;
+        x->d = d;
+        x->k = k;
+        x->d1 = d1;
+        x->layout = layout;
+        x->seed = seed;
+        ivf_alloc_common(x.get());
+        x->d1p = layout == 1 ? d1 : (d > 32 ? 32 : d);
+        const int d1p = x->d1p, d2p = d - d1p;
+        const size_t N = static_cast<size_t>(n);
+        float* dt = dev_upload(t, N * d, st);
+        float* dr = raw ? dev_upload(raw, N * d, st) : nullptr;
+        int32_t* asg = nullptr;
+        ADS_CUDA(cudaMalloc(&asg, sizeof(int32_t) * N));
+        ADS_CUDA(cudaMalloc(&x->cent_t, sizeof(float) * k * static_cast<size_t>(d)));
+        x->P = dev_upload(P, static_cast<size_t>(d) * d, st);
+        try {
+            (void)run_kmeans(dt, n, d, k, max_iters, seed, init, x->cent_t, asg, st);  // ivf.cpp:210
+            ADS_CUDA(cudaMalloc(&x->list_off, sizeof(int64_t) * (k + 1)));
+            ADS_CUDA(cudaMalloc(&x->ids, sizeof(int32_t) * N));
+            build_lists(asg, n, k, x->list_off, x->ids, st);  // ivf.cpp:213-214, 229-241
+            ADS_CUDA(cudaMalloc(&x->a1_t, sizeof(float) * N * d1p));
+            ADS_CUDA(cudaMalloc(&x->a2_t, sizeof(float) * (N * d2p > 0 ? N * d2p : 1)));
+            gather_split(dt, x->ids, n, d, d1p, x->a1_t, x->a2_t, st);
+            if (dr) {
+                x->has_raw = true;
+                ADS_CUDA(cudaMalloc(&x->a1_raw, sizeof(float) * N * d1p));
+                ADS_CUDA(cudaMalloc(&x->a2_raw, sizeof(float) * (N * d2p > 0 ? N * d2p : 1)));
+                gather_split(dr, x->ids, n, d, d1p, x->a1_raw, x->a2_raw, st);
+                // centroids_raw = P^T centroids_t (ivf.cpp:216-226)
+                std::vector<double> PT(static_cast<size_t>(d) * d);
+                for (int i = 0; i < d; ++i)
+                    for (int j = 0; j < d; ++j) PT[static_cast<size_t>(j) * d + i] = P[static_cast<size_t>(i) * d + j];
+                double* dPT = dev_upload(PT.data(), PT.size(), st);
+                ADS_CUDA(cudaMalloc(&x->cent_raw, sizeof(float) * k * static_cast<size_t>(d)));
+                launch_apply(dPT, d, x->cent_t, k, x->cent_raw, st);
+                ADS_CUDA(cudaStreamSynchronize(st));
+                cudaFree(dPT);
+            }
+            ADS_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaStreamSynchronize(st);
+            cudaFree(dt);
+            if (dr) cudaFree(dr);
+            cudaFree(asg);
+            throw;
+        }
+        cudaFree(dt);
+        if (dr) cudaFree(dr);
+        cudaFree(asg);
+        *out = x.release();
+    });
+}
+
+int ads_ivf_destroy(ads_ivf* idx) {
+    return guard([&] {
+        if (!idx) return;
+        idx->ctx->use();
+        cudaStreamSynchronize(idx->ctx->stream);
+        delete idx;
+    });
+}
+
+int ads_ivf_meta(ads_ivf* x, int64_t* meta) {
+    return guard([&] {
+        meta[0] = x->n;
+        meta[1] = x->d;
+        meta[2] = x->k;
+        meta[3] = x->d1;
+        meta[4] = x->layout;
+        meta[5] = static_cast<int64_t>(x->seed);
+        meta[6] = x->has_raw;
+    });
+}
+
+int ads_ivf_export(ads_ivf* x, float* centroids_t, float* centroids_raw, int64_t* list_off,
+                   int32_t* ids_flat, float* a1_t, float* a2_t, float* a1_raw, float* a2_raw) {
+    return guard([&] {
+        x->ctx->use();
+        cudaStream_t st = x->ctx->stream;
+        const size_t n = x->n, D = x->d, d1p = x->d1p, d2p = D - d1p, k = x->k;
+        auto down = [&](void* h, const void* d, size_t bytes) {
+            if (h && d && bytes) ADS_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+        };
+        down(centroids_t, x->cent_t, sizeof(float) * k * D);
+        down(centroids_raw, x->cent_raw, sizeof(float) * k * D);
+        down(list_off, x->list_off, sizeof(int64_t) * (k + 1));
+        down(ids_flat, x->ids, sizeof(int32_t) * n);
+        down(a1_t, x->a1_t, sizeof(float) * n * d1p);
+        down(a2_t, x->a2_t, sizeof(float) * n * d2p);
+        down(a1_raw, x->a1_raw, sizeof(float) * n * d1p);
+        down(a2_raw, x->a2_raw, sizeof(float) * n * d2p);
+        ADS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+void ads_search_opts_default(ads_search_opts* o) {
+    o->first = 0;  // 0 -> K
+    o->step = 256;
+    o->warps_per_cta = 4;
+    o->ctas_per_sm = 0;
+    o->time_stages = 0;
+}
+
+namespace {
+
+DevSegPlan& ivf_plan(ads_ivf* x, int mode, double eps0, int dd) {
+    const bool fd = mode == ADS_MODE_FD;
+    const PlanKey key{mode, fd ? 0.0 : eps0, fd ? 0 : dd};
+    auto it = x->plans.find(key);
+    if (it != x->plans.end()) return *it->second;
+    const int D = x->d;
+    const bool split = mode == ADS_MODE_AD_SPLIT || mode == ADS_MODE_PD_SPLIT;
+    SegPlan p;
+    if (fd) {
+        p = make_seg_plan(D, x->d1p, {}, nullptr);
+    } else {
+        const std::vector<int> tests = test_points(D, dd, split ? x->d1 : 0, split);
+        if (mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT) {
+            const std::vector<double> f = ad_factor(eps0, dd, D);
+            p = make_seg_plan(D, x->d1p, tests, f.data());
+        } else {
+            p = make_seg_plan(D, x->d1p, tests, nullptr);
+        }
+    }
+    auto dp = std::make_unique<DevSegPlan>();
+    dp->upload(p, x->ctx->stream);
+    DevSegPlan& ref = *dp;
+    x->plans.emplace(key, std::move(dp));
+    return ref;
+}
+
+void validate_search(ads_ivf* x, bool has_qt, bool has_qraw, int32_t K, int32_t nprobe, int32_t mode,
+                     double eps0, int32_t dd) {
+    // ivf.cpp:299-307, then AdContext (ivf.cpp:313 -> dco.cpp:32-37).
+    require(K >= 1, "ivf_query: K must be >= 1");
+    require(nprobe >= 1 && nprobe <= x->k, "ivf_query: n_probe must be in [1, k_clusters]");
+    require(mode >= 0 && mode <= 4, "ivf_query: unknown mode");
+    const bool split = mode == ADS_MODE_AD_SPLIT || mode == ADS_MODE_PD_SPLIT;
+    require(!split || x->layout == 1, "ivf_query: split mode needs a split-layout index");
+    const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
+    if (transformed) {
+        require(has_qt || (has_qraw && x->P), "ivf_query: missing query vector");
+        (void)ad_factor(eps0, dd, x->d);
+    } else {
+        require(has_qraw, "ivf_query: missing query vector");
+        require(x->has_raw, "ivf_query: index holds no raw vectors for this mode");
+        if (mode != ADS_MODE_FD) require(dd >= 1, "ivf_query: delta_d must be >= 1");
+    }
+}
+
+void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq, int32_t K,
+                   int32_t nprobe, int32_t mode, double eps0, int32_t dd, const ads_search_opts* opts,
+                   int32_t* dids, double* ddists, int32_t* dcnt, uint64_t* ddims, uint64_t* dcand) {
+    ads_search_opts o;
+    ads_search_opts_default(&o);
+    if (opts) o = *opts;
+    if (o.first <= 0) o.first = K;
+    require(o.warps_per_cta >= 1 && o.warps_per_cta <= 16, "search: warps_per_cta in [1, 16]");
+    cudaStream_t st = x->ctx->stream;
+    const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
+    const int D = x->d;
+    x->timed = o.time_stages != 0;
+    if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[0], st));
+    const float* Qs = transformed ? dQt : dQraw;
+    if (transformed && !dQt) {  // rotate on device (apply, transform.cpp:99-117)
+        float* qr = x->qrot.get<float>(static_cast<size_t>(nq) * D);
+        launch_apply(x->P, D, dQraw, nq, qr, st);
+        Qs = qr;
+    }
+    if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[1], st));
+    double* dist = x->dist.get<double>(static_cast<size_t>(nq) * x->k);
+    int32_t* probes = x->probes.get<int32_t>(static_cast<size_t>(nq) * nprobe);
+    launch_coarse_dist(Qs, nq, transformed ? x->cent_t : x->cent_raw, x->k, D, dist, st);
+    if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[2], st));
+    launch_select_probes(dist, nq, x->k, nprobe, probes, st);
+    if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[3], st));
+    DevSegPlan& plan = ivf_plan(x, mode, eps0, dd);
+    SearchLaunch a{};
+    a.a1 = transformed ? x->a1_t : x->a1_raw;
+    a.a2 = transformed ? x->a2_t : x->a2_raw;
+    a.d1 = x->d1p;
+    a.D = D;
+    a.ids = x->ids;
+    a.list_off = x->list_off;
+    a.Q = Qs;
+    a.nq = nq;
+    a.probes = probes;
+    a.nprobe = nprobe;
+    a.K = K;
+    a.final_fd = mode == ADS_MODE_FD;
+    a.segs = plan.segs;
+    a.tfac = plan.tfac;
+    a.nseg = plan.nseg;
+    a.ntest = plan.ntest;
+    a.vec = plan.vec;
+    a.first = o.first;
+    a.step = o.step;
+    a.warps = o.warps_per_cta;
+    a.ctas_per_sm = o.ctas_per_sm;
+    a.out_ids = dids;
+    a.out_dists = ddists;
+    a.out_cnt = dcnt;
+    a.out_dims = reinterpret_cast<unsigned long long*>(ddims);
+    a.out_cand = reinterpret_cast<unsigned long long*>(dcand);
+    a.counter = x->ctx->counter;
+    launch_ivf_search(a, st);
+    if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[4], st));
+}
+
+}  // namespace
+
+int ads_ivf_search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq, int32_t K,
+                          int32_t nprobe, int32_t mode, double eps0, int32_t dd,
+                          const ads_search_opts* opts, int32_t* dids, double* ddists,
+                          int32_t* dcnt, uint64_t* ddims, uint64_t* dcand) {
+    return guard([&] {
+        validate_search(x, dQt != nullptr, dQraw != nullptr, K, nprobe, mode, eps0, dd);
+        x->ctx->use();
+        std::lock_guard<std::mutex> lk(x->ctx->mu);
+        search_device(x, dQt, dQraw, nq, K, nprobe, mode, eps0, dd, opts, dids, ddists, dcnt, ddims, dcand);
+    });
+}
+
+int ads_ivf_search(ads_ivf* x, const float* Qt, const float* Qraw, int32_t nq, int32_t K,
+                   int32_t nprobe, int32_t mode, double eps0, int32_t dd, const ads_search_opts* opts,
+                   int32_t* ids, double* dists, int32_t* counts, uint64_t* dims, uint64_t* cands) {
+    return guard([&] {
+        const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
+        const bool use_qt = transformed && Qt != nullptr;
+        const bool use_qraw = Qraw != nullptr && (!transformed || !use_qt);
+        validate_search(x, Qt != nullptr, Qraw != nullptr, K, nprobe, mode, eps0, dd);
+        require(nq >= 0, "ivf_query: nq must be >= 0");
+        x->ctx->use();
+        std::lock_guard<std::mutex> lk(x->ctx->mu);
+        cudaStream_t st = x->ctx->stream;
+        const size_t qn = static_cast<size_t>(nq) * x->d;
+        float* dqt = use_qt ? x->qin_t.get<float>(qn) : nullptr;
+        float* dqr = use_qraw ? x->qin_raw.get<float>(qn) : nullptr;
+        if (dqt) ADS_CUDA(cudaMemcpyAsync(dqt, Qt, qn * sizeof(float), cudaMemcpyHostToDevice, st));
+        if (dqr) ADS_CUDA(cudaMemcpyAsync(dqr, Qraw, qn * sizeof(float), cudaMemcpyHostToDevice, st));
+        const size_t rk = static_cast<size_t>(nq) * K;
+        int32_t* di = x->o_ids.get<int32_t>(rk);
+        double* dd_ = x->o_dists.get<double>(rk);
+        int32_t* dc = x->o_cnt.get<int32_t>(nq);
+        uint64_t* dm = x->o_dims.get<uint64_t>(nq);
+        uint64_t* dn = x->o_cand.get<uint64_t>(nq);
+        if (nq > 0)
+            search_device(x, dqt, dqr, nq, K, nprobe, mode, eps0, dd, opts, di, dd_, dc, dm, dn);
+        auto down = [&](void* h, const void* d, size_t bytes) {
+            if (h && bytes) ADS_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+        };
+        down(ids, di, rk * sizeof(int32_t));
+        down(dists, dd_, rk * sizeof(double));
+        down(counts, dc, nq * sizeof(int32_t));
+        down(dims, dm, nq * sizeof(uint64_t));
+        down(cands, dn, nq * sizeof(uint64_t));
+        ADS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ads_ivf_probe_order(ads_ivf* x, const float* Q, int32_t nq, int32_t nprobe, int32_t transformed,
+                        int32_t* probes) {
+    return guard([&] {
+        require(nprobe >= 1 && nprobe <= x->k, "ivf_query: n_probe must be in [1, k_clusters]");
+        require(transformed || x->has_raw, "probe_order: no raw centroids");
+        x->ctx->use();
+        std::lock_guard<std::mutex> lk(x->ctx->mu);
+        cudaStream_t st = x->ctx->stream;
+        const size_t qn = static_cast<size_t>(nq) * x->d;
+        float* dq = x->qin_t.get<float>(qn);
+        ADS_CUDA(cudaMemcpyAsync(dq, Q, qn * sizeof(float), cudaMemcpyHostToDevice, st));
+        double* dist = x->dist.get<double>(static_cast<size_t>(nq) * x->k);
+        int32_t* dp = x->probes.get<int32_t>(static_cast<size_t>(nq) * nprobe);
+        launch_coarse_dist(dq, nq, transformed ? x->cent_t : x->cent_raw, x->k, x->d, dist, st);
+        launch_select_probes(dist, nq, x->k, nprobe, dp, st);
+        ADS_CUDA(cudaMemcpyAsync(probes, dp, sizeof(int32_t) * nq * nprobe, cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ads_ivf_last_timings(ads_ivf* x, float* ms4) {
+    return guard([&] {
+        require(x->timed, "no timed search recorded (set opts.time_stages)");
+        x->ctx->use();
+        ADS_CUDA(cudaEventSynchronize(x->ev[4]));
+        for (int i = 0; i < 4; ++i) ADS_CUDA(cudaEventElapsedTime(&ms4[i], x->ev[i], x->ev[i + 1]));
+    });
+}
+
+}  // extern "C"

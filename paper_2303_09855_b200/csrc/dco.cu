@@ -1,0 +1,154 @@
+// Fixed-threshold batched DCO kernel: one ad_scan / pd_scan_kernel / l2_sq
+// per (query, candidate row) against a caller-given per-query threshold r
+// (dco.hpp:86-177; the fixed-threshold study bench.cpp:303-392; BASELINE
+// config 4).  Persistent CTAs pull tiles (query, candidate range) from a
+// global counter; warps refill lanes from the tile with a shared counter.
+#include "engine.hpp"
+#include "scan_engine.cuh"
+
+namespace ads {
+
+namespace {
+
+constexpr int kDcoWarps = 4;
+
+struct DcoSmem {
+    double r, r_sq;
+    int64_t tile_q, tile_lo, tile_hi, base;
+    int next;
+    int stop;
+};
+
+template <int VEC>
+__global__ void __launch_bounds__(kDcoWarps * 32) dco_fixed_kernel(DcoLaunch a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ DcoSmem sh;
+    // dynamic smem: wbuf [warps*1024 floats] | qseg [nseg*33 doubles] | thr [ntest] | segs [nseg]
+    float* wbuf_all = reinterpret_cast<float*>(smem_raw);
+    double* qseg = reinterpret_cast<double*>(wbuf_all + kDcoWarps * 1024);
+    double* thr = qseg + a.nseg * kQPitch;
+    Seg* segs = reinterpret_cast<Seg*>(thr + (a.ntest > 0 ? a.ntest : 1));
+
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    float* wbuf = wbuf_all + warp * 1024;
+    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int64_t t = static_cast<int64_t>(atomicAdd(a.counter, 1ull));
+            sh.stop = t >= a.ntiles;
+            if (!sh.stop) {
+                if (a.tile_q) {
+                    sh.tile_q = a.tile_q[t];
+                    sh.tile_lo = a.tile_lo[t];
+                    sh.tile_hi = a.tile_hi[t];
+                    sh.base = a.cand_off[sh.tile_q];
+                } else {
+                    const int64_t tpq = (a.win_len + a.tile - 1) / a.tile;
+                    sh.tile_q = t / tpq;
+                    sh.tile_lo = (t % tpq) * a.tile;
+                    sh.tile_hi = sh.tile_lo + a.tile < a.win_len ? sh.tile_lo + a.tile : a.win_len;
+                    sh.base = sh.tile_q * a.win_len;
+                }
+                const double r = a.r[sh.tile_q];
+                sh.r = r;
+                sh.r_sq = __dmul_rn(r, r);  // dco.hpp:125
+                sh.next = static_cast<int>(sh.tile_lo);
+            }
+        }
+        __syncthreads();
+        if (sh.stop) break;
+        const int64_t q = sh.tile_q;
+        stage_query(qseg, segs, a.nseg, a.Q + q * a.D);
+        for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = __dmul_rn(a.tfac[i], sh.r_sq);
+        __syncthreads();
+
+        const int hi = static_cast<int>(sh.tile_hi);
+        const double r = sh.r, r_sq = sh.r_sq;
+        int64_t row = -1;
+        int j = -1, seg = 0;
+        double s = 0.0;
+        unsigned long long my_dims = 0;
+        for (;;) {
+            const unsigned need = __ballot_sync(kFull, j < 0);
+            if (need) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&sh.next, __popc(need));
+                base = __shfl_sync(kFull, base, 0);
+                if (j < 0) {
+                    const int cand = base + __popc(need & ((1u << lane) - 1u));
+                    if (cand < hi) {
+                        j = cand;
+                        if (a.cand_rows) {
+                            row = a.cand_rows[sh.base + cand];
+                        } else {
+                            row = a.win_start[q] + cand;
+                            row %= a.n_rows;
+                        }
+                        seg = 0;
+                        s = 0.0;
+                    }
+                }
+            }
+            if (!__any_sync(kFull, j >= 0)) break;
+            Seg sg = segs[seg];
+            const float* src = a.X + row * a.D + sg.col;
+            gather_lines<VEC>(wbuf, src, j >= 0 ? sg.len : 0);
+            if (j >= 0) {
+                s = accumulate_line<VEC>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                const int d = sg.col + sg.len;
+                bool done = false, pos = false;
+                double obs = 0.0;
+                if (sg.test >= 0 && s > thr[sg.test]) {  // dco.hpp:141
+                    done = true;
+                    obs = a.kind == 2 ? __dsqrt_rn(__ddiv_rn(__dmul_rn(s, static_cast<double>(a.D)),
+                                                              static_cast<double>(d)))
+                                      : __dsqrt_rn(s);
+                } else if (seg == a.nseg - 1) {  // d == D: exact (dco.hpp:145, dco.cpp:70-81)
+                    done = true;
+                    obs = __dsqrt_rn(s);
+                    pos = a.kind == 0 ? obs <= r : s <= r_sq;
+                }
+                if (done) {
+                    const int64_t g = sh.base + j;
+                    if (a.positive) a.positive[g] = pos;
+                    if (a.dims) a.dims[g] = d;
+                    if (a.dist_sq) a.dist_sq[g] = pos ? s : __longlong_as_double(0x7ff8000000000000ll);
+                    if (a.observed) a.observed[g] = obs;
+                    my_dims += static_cast<unsigned long long>(d);
+                    j = -1;
+                } else {
+                    ++seg;
+                }
+            }
+        }
+        if (a.dims_per_query) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) my_dims += __shfl_xor_sync(kFull, my_dims, o);
+            if (lane == 0 && my_dims) atomicAdd(a.dims_per_query + q, my_dims);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_dco_fixed(const DcoLaunch& a, cudaStream_t st) {
+    const size_t smem = sizeof(float) * kDcoWarps * 1024 + sizeof(double) * a.nseg * kQPitch +
+                        sizeof(double) * (a.ntest > 0 ? a.ntest : 1) + sizeof(Seg) * a.nseg;
+    auto kern = a.vec == 4 ? dco_fixed_kernel<4> : dco_fixed_kernel<1>;
+    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    int occ = 0;
+    ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDcoWarps * 32, smem));
+    if (occ < 1) throw std::invalid_argument("dco: dimension too large for shared memory");
+    ADS_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
+    int64_t grid = static_cast<int64_t>(num_sms()) * occ;
+    if (grid > a.ntiles) grid = a.ntiles;
+    if (grid < 1) return;
+    kern<<<static_cast<unsigned>(grid), kDcoWarps * 32, smem, st>>>(a);
+    ADS_LAUNCH_CHECK();
+}
+
+}  // namespace ads

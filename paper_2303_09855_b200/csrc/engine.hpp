@@ -1,0 +1,129 @@
+// Internal host-side interface between the C ABI (capi.cu) and the kernel
+// launchers.  Not installed; the public boundary is include/adsann_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ads {
+
+// ---------------------------------------------------------------- segments
+// Host-built description of how one candidate's D coordinates are walked:
+// cut at every hypothesis-test point, at the A1/A2 split and every 32 floats.
+struct SegPlan {
+    std::vector<Seg> segs;
+    std::vector<double> test_factor;  // thr[t] = test_factor[t] * r^2
+    int vec = 4;                      // 16-byte copies when every cut is 4-aligned
+    int D = 0;
+};
+
+// tests: sorted coordinate counts in (0, D) at which a test runs; factor[d]
+// gives the multiplier there (nullptr -> 1.0, the exact partial scan).
+SegPlan make_seg_plan(int D, int split_at, const std::vector<int>& tests, const double* factor);
+// Test points of ad_scan / pd_scan_kernel started at d_start with or without
+// the start test (dco.hpp:122-177).
+std::vector<int> test_points(int D, int delta_d, int d_start, bool test_at_start);
+// AdContext::factor (dco.cpp:54-61), host fp64.
+std::vector<double> ad_factor(double eps0, int delta_d, int D);
+
+struct DevSegPlan {
+    Seg* segs = nullptr;
+    double* tfac = nullptr;
+    int nseg = 0, ntest = 0, vec = 4;
+    void upload(const SegPlan& p, cudaStream_t st);
+    void release();
+};
+
+// ---------------------------------------------------------------- kernels
+struct DcoLaunch {
+    const float* X;
+    int64_t n_rows;
+    int D;
+    const float* Q;
+    int nq;
+    const int64_t* cand_off;   // device, nullable (window mode)
+    const int64_t* cand_rows;  // device, nullable
+    const int64_t* win_start;  // device, nullable
+    int64_t win_len;
+    const double* r;           // device
+    const int64_t* tile_q;     // device tile table (CSR mode) or nullptr
+    const int64_t* tile_lo;
+    const int64_t* tile_hi;
+    int64_t ntiles;
+    int64_t tile;              // candidates per tile (window mode)
+    int kind;                  // 0 fd, 1 pd, 2 ad
+    const Seg* segs;
+    const double* tfac;
+    int nseg, ntest, vec;
+    uint8_t* positive;
+    int32_t* dims;
+    double* dist_sq;
+    double* observed;
+    unsigned long long* dims_per_query;
+    unsigned long long* counter;  // device scratch, zeroed by the launcher
+};
+void launch_dco_fixed(const DcoLaunch& a, cudaStream_t st);
+
+struct SearchLaunch {
+    const float* a1;
+    const float* a2;
+    int d1;            // physical split (A1 row stride)
+    int D;
+    const int32_t* ids;
+    const int64_t* list_off;
+    const float* Q;    // nq x D, search space
+    int nq;
+    const int32_t* probes;  // nq x nprobe
+    int nprobe;
+    int K;
+    int final_fd;      // 1: sqrt(s) <= r (kFd), 0: s <= r^2
+    const Seg* segs;
+    const double* tfac;
+    int nseg, ntest, vec;
+    int64_t first, step;
+    int warps;         // per CTA
+    int ctas_per_sm;
+    int32_t* out_ids;
+    double* out_dists;
+    int32_t* out_cnt;
+    unsigned long long* out_dims;
+    unsigned long long* out_cand;
+    unsigned long long* counter;
+};
+void launch_ivf_search(const SearchLaunch& a, cudaStream_t st);
+
+// Exact fp64 centroid distances (nq x L, l2_sq order) and top-nprobe by (d2, id).
+void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,
+                        cudaStream_t st);
+void launch_select_probes(const double* dist, int nq, int L, int nprobe, int32_t* probes,
+                          cudaStream_t st);
+
+// y = P x (fp64, reference order), P row-major dim x dim on device (double).
+void launch_apply(const double* P, int dim, const float* X, int64_t n, float* Y,
+                  cudaStream_t st);
+
+// brute_force_knn: K smallest (d2, id) pairs per query.
+void launch_brute_knn(const float* base, int64_t n, int D, const float* Q, int nq, int K,
+                      int32_t* ids, cudaStream_t st);
+
+// k-means pieces (kmeans.cu).
+struct KmeansOut {
+    double objective;
+    int iterations;
+};
+KmeansOut run_kmeans(const float* dX, int64_t n, int d, int k, int max_iters, uint64_t seed,
+                     int init, float* dC, int32_t* dAssign, cudaStream_t st);
+// Bucket layout (ivf.cpp:211-256) from an assignment: list_off (k+1), ids_flat,
+// and gathered A1/A2 copies of `src` (n x D row-major by id) split at d1.
+void build_lists(const int32_t* dAssign, int64_t n, int k, int64_t* dListOff, int32_t* dIds,
+                 cudaStream_t st);
+void gather_split(const float* src, const int32_t* dIds, int64_t n, int D, int d1, float* a1,
+                  float* a2, cudaStream_t st);
+
+int num_sms();
+
+}  // namespace ads

@@ -1,0 +1,468 @@
+// IVF/IVF++ batched search on sm_100a (ivf_query, ivf.cpp:296-419).
+//
+//   coarse_dist_kernel   exact fp64 query-centroid distances (l2_sq order,
+//                        ivf.cpp:287), tiled through shared memory
+//   select_rows_kernel   per-row top-k by (d2, index) pairs: radix select +
+//                        ordered tie fill + bitonic sort (partial_sort,
+//                        ivf.cpp:288; also brute_force_knn's pair order)
+//   ivf_search_kernel    one CTA per query (persistent).  The query's probed
+//                        lists form one candidate stream in probe order;
+//                        warps refill lanes from it and run the DCO engine
+//                        (scan_engine.cuh) against the per-query threshold
+//                        table.  The running K-th distance r is refreshed at
+//                        deterministic stream positions (0, first,
+//                        first+step, ...): positives of a chunk are offered
+//                        to the bounded (dist, id) heap in candidate order
+//                        with the reference's strict rule (ivf.cpp:273-280),
+//                        then thr[t] = factor[d_t] * r^2 is rebuilt.
+#include <cfloat>
+
+#include "engine.hpp"
+#include "scan_engine.cuh"
+
+namespace ads {
+
+namespace {
+
+constexpr double kInf = __builtin_huge_val();
+
+// ---------------------------------------------------------------- coarse distances
+constexpr int kCT = 128;  // centroids per CTA (one per thread)
+constexpr int kQT = 8;    // queries per CTA
+constexpr int kDK = 32;   // dims per stage
+
+__global__ void __launch_bounds__(kCT) coarse_dist_kernel(const float* __restrict__ Q, int nq,
+                                                          const float* __restrict__ C, int L,
+                                                          int D, double* __restrict__ out) {
+    __shared__ float ct[kCT * (kDK + 1)];
+    __shared__ double qt[kQT][kDK];
+    const int c0 = blockIdx.x * kCT;
+    const int q0 = blockIdx.y * kQT;
+    const int tid = threadIdx.x;
+    double acc[kQT];
+#pragma unroll
+    for (int i = 0; i < kQT; ++i) acc[i] = 0.0;
+    for (int d0 = 0; d0 < D; d0 += kDK) {
+        const int len = D - d0 < kDK ? D - d0 : kDK;
+        for (int idx = tid; idx < kCT * kDK; idx += kCT) {
+            const int c = idx / kDK, k = idx % kDK;
+            float v = 0.f;
+            if (c0 + c < L && k < len) v = C[static_cast<int64_t>(c0 + c) * D + d0 + k];
+            ct[c * (kDK + 1) + k] = v;
+        }
+        for (int idx = tid; idx < kQT * kDK; idx += kCT) {
+            const int qq = idx / kDK, k = idx % kDK;
+            double v = 0.0;
+            if (q0 + qq < nq && k < len) v = static_cast<double>(Q[static_cast<int64_t>(q0 + qq) * D + d0 + k]);
+            qt[qq][k] = v;
+        }
+        __syncthreads();
+        for (int k = 0; k < len; ++k) {
+            const float cv = ct[tid * (kDK + 1) + k];
+#pragma unroll
+            for (int qq = 0; qq < kQT; ++qq) acc[qq] = sq_diff_acc(acc[qq], cv, qt[qq][k]);
+        }
+        __syncthreads();
+    }
+    if (c0 + tid < L) {
+#pragma unroll
+        for (int qq = 0; qq < kQT; ++qq)
+            if (q0 + qq < nq) out[static_cast<int64_t>(q0 + qq) * L + c0 + tid] = acc[qq];
+    }
+}
+
+// ---------------------------------------------------------------- per-row top-k select
+constexpr int kSelThreads = 256;
+
+// keys: non-negative doubles as uint64 (order-preserving).  Output the kk
+// smallest (key, col) pairs of each row, ascending.  Dynamic smem holds the
+// padded sort buffer: P2 * (8 + 4) bytes.
+__global__ void __launch_bounds__(kSelThreads) select_rows_kernel(const double* __restrict__ dist,
+                                                                  int64_t L, int kk, int P2,
+                                                                  int32_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    unsigned long long* sk = reinterpret_cast<unsigned long long*>(sm);
+    int32_t* si = reinterpret_cast<int32_t*>(sk + P2);
+    __shared__ unsigned hist[256];
+    __shared__ unsigned long long s_prefix, s_mask;
+    __shared__ int s_rank, s_nsel, s_eqbase;
+    __shared__ int warp_cnt[kSelThreads / 32];
+
+    const double* row = dist + static_cast<int64_t>(blockIdx.x) * L;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_prefix = 0;
+        s_mask = 0;
+        s_rank = kk;
+        s_nsel = 0;
+        s_eqbase = 0;
+    }
+    __syncthreads();
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += kSelThreads) hist[i] = 0;
+        __syncthreads();
+        const unsigned long long prefix = s_prefix, mask = s_mask;
+        for (int64_t c = tid; c < L; c += kSelThreads) {
+            const unsigned long long key = dkey(row[c]);
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255ull], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int rank = s_rank;
+            unsigned cum = 0;
+            int digit = 255;
+            for (int b = 0; b < 256; ++b) {
+                if (static_cast<int>(cum + hist[b]) >= rank) {
+                    digit = b;
+                    break;
+                }
+                cum += hist[b];
+            }
+            s_rank = rank - static_cast<int>(cum);
+            s_prefix = prefix | (static_cast<unsigned long long>(digit) << shift);
+            s_mask = mask | (255ull << shift);
+        }
+        __syncthreads();
+    }
+    const unsigned long long T = s_prefix;
+    const int need_eq = s_rank;  // how many keys == T to take (lowest indices)
+    // keys strictly below T: all of them (kk - need_eq of them)
+    for (int64_t c = tid; c < L; c += kSelThreads) {
+        const unsigned long long key = dkey(row[c]);
+        if (key < T) {
+            const int slot = atomicAdd(&s_nsel, 1);
+            sk[slot] = key;
+            si[slot] = static_cast<int32_t>(c);
+        }
+    }
+    __syncthreads();
+    const int nlt = s_nsel;
+    // keys == T in ascending column order until need_eq are taken
+    for (int64_t base = 0; base < L; base += kSelThreads) {
+        if (s_eqbase >= need_eq) break;  // uniform (read after barrier)
+        const int64_t c = base + tid;
+        const bool eq = c < L && dkey(row[c]) == T;
+        const unsigned b = __ballot_sync(kFull, eq);
+        if ((tid & 31) == 0) warp_cnt[tid >> 5] = __popc(b);
+        __syncthreads();
+        int before = s_eqbase;
+        for (int w = 0; w < (tid >> 5); ++w) before += warp_cnt[w];
+        before += __popc(b & ((1u << (tid & 31)) - 1u));
+        if (eq && before < need_eq) {
+            sk[nlt + before] = T;
+            si[nlt + before] = static_cast<int32_t>(c);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < kSelThreads / 32; ++w) tot += warp_cnt[w];
+            s_eqbase += tot;
+        }
+        __syncthreads();
+    }
+    for (int i = kk + tid; i < P2; i += kSelThreads) {
+        sk[i] = ~0ull;
+        si[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    // bitonic sort by (key, idx)
+    for (int size = 2; size <= P2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < P2 / 2; i += kSelThreads) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long ka = sk[lo], kb = sk[hi];
+                const int32_t ia = si[lo], ib = si[hi];
+                const bool a_gt_b = ka > kb || (ka == kb && ia > ib);
+                if (a_gt_b == up) {
+                    sk[lo] = kb;
+                    sk[hi] = ka;
+                    si[lo] = ib;
+                    si[hi] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = tid; i < kk; i += kSelThreads) out[static_cast<int64_t>(blockIdx.x) * kk + i] = si[i];
+}
+
+// ---------------------------------------------------------------- search
+struct SearchShared {
+    double r, r_sq;
+    int q, stop, total, next, cnt;
+    unsigned long long dims;
+};
+
+__device__ __forceinline__ bool pair_lt(double da, int32_t ia, double db, int32_t ib) {
+    return da < db || (da == db && ia < ib);
+}
+
+// ivf.cpp:273-280 offer(), executed by one full warp on the shared sorted array.
+__device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double dist, int32_t id) {
+    const unsigned lane = lane_id();
+    const int c = *cnt;
+    if (c == K && !(dist < topd[K - 1])) return;  // strict: ties at the max are not inserted
+    const int ceff = c == K ? K - 1 : c;           // pop the max pair when full
+    int pos = 0;
+    for (int base = 0; base < ceff; base += 32) {
+        const int j = base + static_cast<int>(lane);
+        const bool lt = j < ceff && pair_lt(topd[j], topi[j], dist, id);
+        pos += __popc(__ballot_sync(kFull, lt));
+    }
+    for (int top = ceff - 1; top >= pos; top -= 32) {
+        const int j = top - static_cast<int>(lane);
+        const bool valid = j >= pos;
+        double v = 0.0;
+        int32_t vi = 0;
+        if (valid) {
+            v = topd[j];
+            vi = topi[j];
+        }
+        __syncwarp();
+        if (valid) {
+            topd[j + 1] = v;
+            topi[j + 1] = vi;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        topd[pos] = dist;
+        topi[pos] = id;
+        *cnt = ceff + 1;
+    }
+    __syncwarp();
+}
+
+template <int VEC>
+__global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ SearchShared sh;
+    const int nwarps = blockDim.x >> 5;
+    // dynamic layout (8-byte items first)
+    float* wbuf_all = reinterpret_cast<float*>(smem_raw);
+    double* qseg = reinterpret_cast<double*>(wbuf_all + nwarps * 1024);
+    double* thr = qseg + a.nseg * kQPitch;
+    double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
+    double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
+    double* pend_d = topd + a.K;
+    int64_t* lstart = reinterpret_cast<int64_t*>(pend_d + chunk_cap);
+    Seg* segs = reinterpret_cast<Seg*>(lstart + a.nprobe);
+    int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
+    int32_t* pend_i = topi + a.K;
+    int32_t* pre = pend_i + chunk_cap;
+    unsigned* pflag = reinterpret_cast<unsigned*>(pre + a.nprobe + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    float* wbuf = wbuf_all + warp * 1024;
+    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
+    for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) tfac[i] = a.tfac[i];
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int q = static_cast<int>(atomicAdd(a.counter, 1ull));
+            sh.q = q;
+            sh.stop = q >= a.nq;
+            sh.cnt = 0;
+            sh.r = kInf;
+            sh.r_sq = kInf;
+            sh.dims = 0;
+        }
+        __syncthreads();
+        if (sh.stop) break;
+        const int qi = sh.q;
+        stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = kInf;
+        if (warp == 0) {  // probed lists -> stream prefix offsets
+            int carry = 0;
+            for (int base = 0; base < a.nprobe; base += 32) {
+                const int i = base + static_cast<int>(lane);
+                int len = 0;
+                if (i < a.nprobe) {
+                    const int p = a.probes[static_cast<int64_t>(qi) * a.nprobe + i];
+                    const int64_t s0 = a.list_off[p];
+                    lstart[i] = s0;
+                    len = static_cast<int>(a.list_off[p + 1] - s0);
+                }
+                int incl = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(kFull, incl, o);
+                    if (static_cast<int>(lane) >= o) incl += v;
+                }
+                if (i < a.nprobe) pre[i + 1] = carry + incl;
+                carry += __shfl_sync(kFull, incl, 31);
+            }
+            if (lane == 0) {
+                pre[0] = 0;
+                sh.total = carry;
+            }
+        }
+        __syncthreads();
+        const int total = sh.total;
+        unsigned long long my_dims = 0;
+
+        for (int lo = 0; lo < total;) {
+            const int64_t span = lo == 0 ? a.first : a.step;
+            const int hi = static_cast<int>(lo + span < total ? lo + span : total);
+            if (threadIdx.x == 0) sh.next = lo;
+            for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
+            __syncthreads();
+            const double r = sh.r, r_sq = sh.r_sq;
+
+            int cand = -1, seg = 0;
+            int64_t pos = 0;
+            double s = 0.0;
+            for (;;) {
+                const unsigned need = __ballot_sync(kFull, cand < 0);
+                if (need) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&sh.next, __popc(need));
+                    base = __shfl_sync(kFull, base, 0);
+                    if (cand < 0) {
+                        const int i = base + __popc(need & ((1u << lane) - 1u));
+                        if (i < hi) {
+                            int l = 0, h = a.nprobe - 1;  // last list with pre[k] <= i
+                            while (l < h) {
+                                const int mid = (l + h + 1) >> 1;
+                                if (pre[mid] <= i) l = mid;
+                                else h = mid - 1;
+                            }
+                            cand = i;
+                            pos = lstart[l] + (i - pre[l]);
+                            seg = 0;
+                            s = 0.0;
+                        }
+                    }
+                }
+                if (!__any_sync(kFull, cand >= 0)) break;
+                const Seg sg = segs[seg];
+                const float* src = sg.arr == 0
+                                       ? a.a1 + pos * a.d1 + sg.col
+                                       : a.a2 + pos * (a.D - a.d1) + (sg.col - a.d1);
+                gather_lines<VEC>(wbuf, src, cand >= 0 ? sg.len : 0);
+                if (cand >= 0) {
+                    s = accumulate_line<VEC>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                    if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
+                        my_dims += static_cast<unsigned long long>(sg.col + sg.len);
+                        cand = -1;
+                    } else if (seg == a.nseg - 1) {  // d == D (dco.hpp:145; ivf.cpp:335-338)
+                        my_dims += static_cast<unsigned long long>(a.D);
+                        const double dist = __dsqrt_rn(s);
+                        const bool positive = a.final_fd ? dist <= r : s <= r_sq;
+                        if (positive) {
+                            const int slot = cand - lo;
+                            pend_d[slot] = dist;
+                            pend_i[slot] = a.ids[pos];
+                            atomicOr(&pflag[slot >> 5], 1u << (slot & 31));
+                        }
+                        cand = -1;
+                    } else {
+                        ++seg;
+                    }
+                }
+            }
+            __syncthreads();
+            if (warp == 0) {  // offer the chunk's positives in candidate order
+                const int nw = (hi - lo + 31) / 32;
+                for (int w = 0; w < nw; ++w) {
+                    unsigned bits = pflag[w];
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const int slot = w * 32 + b;
+                        warp_offer(topd, topi, &sh.cnt, a.K, pend_d[slot], pend_i[slot]);
+                    }
+                }
+                if (sh.cnt == a.K) {  // ivf.cpp:268-270; dco.hpp:125
+                    const double rn = topd[a.K - 1];
+                    const double rsq = __dmul_rn(rn, rn);
+                    for (int i = static_cast<int>(lane); i < a.ntest; i += 32) thr[i] = __dmul_rn(tfac[i], rsq);
+                    if (lane == 0) {
+                        sh.r = rn;
+                        sh.r_sq = rsq;
+                    }
+                }
+            }
+            __syncthreads();
+            lo = hi;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) my_dims += __shfl_xor_sync(kFull, my_dims, o);
+        if (lane == 0) atomicAdd(&sh.dims, my_dims);
+        __syncthreads();
+        const int cnt = sh.cnt;
+        for (int i = threadIdx.x; i < a.K; i += blockDim.x) {
+            const int64_t o = static_cast<int64_t>(qi) * a.K + i;
+            a.out_ids[o] = i < cnt ? topi[i] : -1;
+            a.out_dists[o] = i < cnt ? topd[i] : __longlong_as_double(0x7ff8000000000000ll);
+        }
+        if (threadIdx.x == 0) {
+            a.out_cnt[qi] = cnt;
+            a.out_dims[qi] = sh.dims;
+            if (a.out_cand) a.out_cand[qi] = static_cast<unsigned long long>(total);
+        }
+    }
+}
+
+size_t search_smem(const SearchLaunch& a, int chunk_cap) {
+    const int nt = a.ntest > 0 ? a.ntest : 1;
+    size_t b = sizeof(float) * a.warps * 1024;
+    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + chunk_cap);
+    b += sizeof(int64_t) * a.nprobe;
+    b += sizeof(Seg) * a.nseg;
+    b += sizeof(int32_t) * (a.K + chunk_cap + a.nprobe + 1);
+    b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
+    return b;
+}
+
+}  // namespace
+
+void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,
+                        cudaStream_t st) {
+    if (nq <= 0 || L <= 0) return;
+    dim3 grid((L + kCT - 1) / kCT, (nq + kQT - 1) / kQT);
+    coarse_dist_kernel<<<grid, kCT, 0, st>>>(Q, nq, C, L, D, out);
+    ADS_LAUNCH_CHECK();
+}
+
+void launch_select_probes(const double* dist, int nq, int L, int nprobe, int32_t* probes,
+                          cudaStream_t st) {
+    if (nq <= 0) return;
+    int P2 = 1;
+    while (P2 < nprobe) P2 <<= 1;
+    if (P2 < 2) P2 = 2;
+    const size_t smem = static_cast<size_t>(P2) * (sizeof(unsigned long long) + sizeof(int32_t));
+    if (smem > 200 * 1024) throw std::invalid_argument("select: k too large");
+    ADS_CUDA(cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    select_rows_kernel<<<nq, kSelThreads, smem, st>>>(dist, L, nprobe, P2, probes);
+    ADS_LAUNCH_CHECK();
+}
+
+void launch_ivf_search(const SearchLaunch& a_in, cudaStream_t st) {
+    SearchLaunch a = a_in;
+    if (a.nq <= 0) return;
+    const int64_t cap64 = a.first > a.step ? a.first : a.step;
+    if (a.first < 1 || a.step < 1) throw std::invalid_argument("search: threshold schedule must be >= 1");
+    if (cap64 > 16384) throw std::invalid_argument("search: threshold refresh interval too long (max 16384)");
+    const int cap = static_cast<int>(cap64);
+    const size_t smem = search_smem(a, cap);
+    auto kern = a.vec == 4 ? ivf_search_kernel<4> : ivf_search_kernel<1>;
+    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    int occ = 0;
+    ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, a.warps * 32, smem));
+    if (occ < 1) throw std::invalid_argument("search: configuration exceeds shared memory");
+    if (a.ctas_per_sm > 0 && a.ctas_per_sm < occ) occ = a.ctas_per_sm;
+    ADS_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
+    int64_t grid = static_cast<int64_t>(num_sms()) * occ;
+    if (grid > a.nq) grid = a.nq;
+    kern<<<static_cast<unsigned>(grid), a.warps * 32, smem, st>>>(a, cap);
+    ADS_LAUNCH_CHECK();
+}
+
+}  // namespace ads

@@ -1,0 +1,250 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle.
+
+The oracle is the C restatement pinned bit-for-bit to the reference
+(test_oracle_pins.py).  Because the kernels use the reference's fp64
+operation order, every comparison here is EXACT (decisions, dims,
+distances, ids) — stricter than the north star's 1e-5 boundary band.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import MODES, MODE_ID, assert_same_results, gpu_index, make_fixture, oracle_index
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------------ transform
+@pytest.mark.parametrize("d,n", [(1, 5), (7, 33), (64, 1000), (128, 517), (200, 64)])
+def test_apply_dataset_bitexact(eng, orc, d, n):
+    rng = np.random.default_rng(d * 7 + n)
+    X = rng.normal(0, 3, (n, d)).astype(np.float32)
+    m = eng.generate_orthogonal(d, 11)
+    assert np.array_equal(m.entries, orc.generate_orthogonal(d, 11))
+    Y = eng.apply_dataset(m, X)
+    np.testing.assert_array_equal(Y, orc.apply_dataset(m.entries, X))
+    yt = eng.apply_transpose(m, X[0])
+    np.testing.assert_array_equal(yt, orc.apply_transpose(m.entries, X[0]))
+    np.testing.assert_array_equal(eng.apply_prefix(m, X[1], d // 2),
+                                  orc.apply_prefix(m.entries, X[1], d // 2))
+
+
+# ------------------------------------------------------------------ fixed-threshold DCOs
+@pytest.mark.parametrize("D,dd,eps,kind", [
+    (128, 32, 2.1, "ad"), (256, 32, 2.1, "ad"), (96, 32, 2.1, "ad"), (960, 32, 2.1, "ad"),
+    (128, 16, 1.5, "ad"), (48, 48, 2.1, "ad"), (100, 20, 2.1, "ad"),   # partial last block
+    (30, 7, 2.0, "ad"), (161, 1, 0.7, "ad"), (13, 13, 1e6, "ad"),      # 4-byte gather path
+    (128, 32, 2.1, "pd"), (40, 9, 2.1, "pd"), (64, 32, 2.1, "fd"), (33, 1, 2.1, "fd"),
+])
+def test_dco_fixed_bitexact(eng, orc, D, dd, eps, kind):
+    rng = np.random.default_rng(D * 1000 + dd)
+    n, nq, per = 700, 9, 300
+    X = rng.normal(0, 1, (n, D)).astype(np.float32)
+    Q = rng.normal(0, 1, (nq, D)).astype(np.float32)
+    rows = rng.integers(0, n, nq * per).astype(np.int64)
+    off = np.arange(0, nq * per + 1, per, dtype=np.int64)
+    # thresholds around the typical distance so decisions are mixed; include r=0 and r=inf
+    r = np.sqrt(2.0 * D) * rng.uniform(0.7, 1.05, nq)
+    r[0] = 0.0
+    r[1] = math.inf
+    cfg = eng.DcoConfig(eps, dd)
+    res = eng.dco_fixed(X, Q, r, cand_off=off, cand_rows=rows, kind=kind, cfg=cfg)
+    qidx = np.repeat(np.arange(nq, dtype=np.int32), per)
+    pos, dims, dsq, obs = orc.ad_scan_pairs(X, Q, rows, qidx, np.repeat(r, per), eps, dd,
+                                            pd_mode=(kind == "pd"))
+    if kind == "fd":  # l2_sq + sqrt(s) <= r (dco.cpp:70-81)
+        s = np.array([orc.scan_kernel(1, X[rw], Q[q], D, 0, 0.0, math.inf, eps, D, False)[1]
+                      for rw, q in zip(rows, qidx)])
+        obs = np.sqrt(s)
+        pos = (obs <= np.repeat(r, per)).astype(np.uint8)
+        dims = np.full(len(rows), D, np.int32)
+        dsq = np.where(pos == 1, s, np.nan)
+    np.testing.assert_array_equal(res.positive.astype(np.uint8), pos)
+    np.testing.assert_array_equal(res.dims, dims)
+    np.testing.assert_array_equal(res.observed, obs)
+    np.testing.assert_array_equal(np.isnan(res.dist_sq), np.isnan(dsq))
+    ok = ~np.isnan(dsq)
+    np.testing.assert_array_equal(res.dist_sq[ok], dsq[ok])
+    per_q = dims.reshape(nq, per).sum(axis=1).astype(np.uint64)
+    np.testing.assert_array_equal(res.dims_per_query, per_q)
+
+
+def test_dco_fixed_windows(eng, orc):
+    """Config-4 style windows (wrapping row ranges) == explicit rows."""
+    rng = np.random.default_rng(5)
+    n, D, nq, win = 5000, 256, 6, 1777
+    X = rng.normal(0, 1, (n, D)).astype(np.float32)
+    Q = rng.normal(0, 1, (nq, D)).astype(np.float32)
+    start = rng.integers(0, n, nq).astype(np.int64)
+    r = np.full(nq, np.sqrt(2 * D) * 0.93)
+    a = eng.dco_fixed(X, Q, r, win_start=start, win_len=win)
+    rows = ((start[:, None] + np.arange(win)[None, :]) % n).reshape(-1)
+    qidx = np.repeat(np.arange(nq, dtype=np.int32), win)
+    pos, dims, dsq, obs = orc.ad_scan_pairs(X, Q, rows, qidx, np.repeat(r, win), 2.1, 32)
+    np.testing.assert_array_equal(a.positive.astype(np.uint8), pos)
+    np.testing.assert_array_equal(a.dims, dims)
+    np.testing.assert_array_equal(a.observed, obs)
+
+
+def test_single_dco_kats(eng, orc):
+    """test_dco.cpp KATs through the validated single-DCO API."""
+    o, q = [3.0, 4.0], [0.0, 0.0]
+    hit = eng.fd_scan(o, q, 5.0)
+    assert hit.positive and hit.distance == 5.0 and hit.dims_used == 2
+    miss = eng.fd_scan(o, q, 4.9)
+    assert not miss.positive and miss.distance is None and miss.observed == 5.0
+    pd = eng.pd_scan(o, q, 2.0, 1)
+    assert not pd.positive and pd.dims_used == 1 and pd.observed == 3.0
+    m = eng.generate_orthogonal(64, 19)
+    rng = np.random.default_rng(23)
+    a = eng.apply(m, rng.normal(size=64))
+    b = eng.apply(m, rng.normal(size=64))
+    z = eng.ad_sampling(a, b, 0.0, eng.DcoConfig(2.1, 16))
+    assert not z.positive and z.dims_used == 16
+    s = eng.ad_sampling(a, a, 0.0, eng.DcoConfig(2.1, 16))
+    assert s.positive and s.distance == 0.0 and s.dims_used == 64
+    for kind, args in (("ad", (2.1, 16)), ("pd", (2.1, 8)), ("fd", (2.1, 1))):
+        for r in (0.0, 3.0, 11.3, 50.0):
+            out = {"ad": lambda: eng.ad_sampling(a, b, r, eng.DcoConfig(*args)),
+                   "pd": lambda: eng.pd_scan(a, b, r, args[1]),
+                   "fd": lambda: eng.fd_scan(a, b, r)}[kind]()
+            exp = orc.dco(kind, a, b, r, *args)
+            assert (out.positive, out.distance, out.observed, out.dims_used) == exp
+    with pytest.raises(ValueError):
+        eng.fd_scan([1.0, 2.0], [1.0], 1.0)
+    with pytest.raises(ValueError):
+        eng.fd_scan([1.0, 2.0], [1.0, 2.0], -1.0)
+    with pytest.raises(ValueError):
+        eng.pd_scan([1.0, 2.0], [1.0, 2.0], 1.0, 3)
+    with pytest.raises(ValueError):
+        eng.ad_sampling([1.0, 2.0], [1.0, 2.0], 1.0, eng.DcoConfig(0.0, 1))
+    with pytest.raises(ValueError):
+        eng.ad_sampling([1.0, 2.0], [1.0, 2.0], 1.0, eng.DcoConfig(2.1, 0))
+
+
+# ------------------------------------------------------------------ IVF search
+CASES = [
+    # n, d, blobs, k, d1, dd, K
+    (2000, 64, 16, 40, 32, 32, 10),
+    (3000, 128, 32, 50, 32, 32, 20),
+    (1500, 48, 8, 20, 16, 16, 5),     # persistence-test shape
+    (1200, 30, 8, 12, 10, 7, 7),      # unaligned -> 4-byte gathers
+    (1000, 96, 8, 16, 40, 24, 9),     # d1 != delta_d
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_ivf_reference_schedule_bitexact(eng, orc, case):
+    """first=step=1 (r re-read before every candidate) == adsann::ivf_query exactly."""
+    n, d, blobs, k, d1, dd, K = case
+    raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 25, 57 + d)
+    lay = oracle_index(orc, raw, t, P, k, 59, d1=d1)
+    idx = gpu_index(eng, lay, P)
+    cfg = eng.DcoConfig(2.1, dd)
+    for mode in MODES:
+        for nprobe in (1, 5, k):
+            res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg,
+                                      first=1, step=1)
+            assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, dd, 1, 1)
+
+
+@pytest.mark.parametrize("first,step", [(0, 256), (0, 64), (1, 1000), (37, 5)])
+def test_ivf_batched_schedule_bitexact(eng, orc, first, step):
+    """Batched threshold refresh == the oracle's same schedule, bit for bit."""
+    raw, t, qr, qt, P = make_fixture(orc, 4000, 64, 16, 40, 91)
+    lay = oracle_index(orc, raw, t, P, 50, 93, d1=32)
+    idx = gpu_index(eng, lay, P)
+    K = 10
+    for mode in ("ad-split", "ad", "pd-split", "fd"):
+        for nprobe in (3, 17):
+            res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]),
+                                      eng.DcoConfig(), first=first, step=step)
+            f = first if first > 0 else K
+            assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, 32, f, step)
+
+
+def test_ivf_rotation_on_device(eng, orc):
+    """Q_t omitted -> queries rotated on the GPU with P; identical results."""
+    raw, t, qr, qt, P = make_fixture(orc, 2000, 64, 16, 30, 7)
+    lay = oracle_index(orc, raw, t, P, 30, 8, d1=32)
+    idx = gpu_index(eng, lay, P)
+    a = eng.ivf_query_batch(idx, None, qr, 10, 6, eng.IvfMode.kAdSplit)
+    b = eng.ivf_query_batch(idx, qt, qr, 10, 6, eng.IvfMode.kAdSplit)
+    np.testing.assert_array_equal(a.ids, b.ids)
+    np.testing.assert_array_equal(a.dists, b.dists)
+    np.testing.assert_array_equal(a.dims, b.dims)
+
+
+def test_probe_order_bitexact(eng, orc):
+    raw, t, qr, qt, P = make_fixture(orc, 3000, 64, 8, 40, 3)
+    lay = oracle_index(orc, raw, t, P, 300, 4, d1=32, iters=3)
+    idx = gpu_index(eng, lay, P)
+    for nprobe in (1, 7, 64, 300):
+        got = idx.probe_order(qt, nprobe, transformed=True)
+        for qi in range(qt.shape[0]):
+            np.testing.assert_array_equal(got[qi], orc.probe_order(lay["centroids_t"], qt[qi], nprobe))
+    got = idx.probe_order(qr, 9, transformed=False)
+    for qi in range(qr.shape[0]):
+        np.testing.assert_array_equal(got[qi], orc.probe_order(lay["centroids_raw"], qr[qi], 9))
+
+
+def test_ivf_validation(eng, orc):
+    raw, t, qr, qt, P = make_fixture(orc, 100, 8, 2, 1, 73)
+    lay = oracle_index(orc, raw, t, P, 5, 75, split=False)
+    idx = gpu_index(eng, lay, P)
+    M = eng.IvfMode
+    with pytest.raises(ValueError):
+        eng.ivf_query(idx, None, qr[0], 0, 1, M.kFd)
+    with pytest.raises(ValueError):
+        eng.ivf_query(idx, None, qr[0], 1, 0, M.kFd)
+    with pytest.raises(ValueError):
+        eng.ivf_query(idx, None, qr[0], 1, 6, M.kFd)
+    with pytest.raises(ValueError):
+        eng.ivf_query(idx, None, qr[0], 1, 1, M.kAdSplit)
+    idx_noP = eng.IvfIndex.from_arrays(n=lay["n"], d=lay["d"], k_clusters=lay["k"], d1=lay["d1"],
+                                       layout=0, centroids_t=lay["centroids_t"],
+                                       list_off=lay["list_off"], ids_flat=lay["ids_flat"],
+                                       vec_t=lay["vec_t"])
+    with pytest.raises(ValueError):
+        eng.ivf_query(idx_noP, None, qr[0], 1, 1, M.kAd)
+
+
+# ------------------------------------------------------------------ build side
+@pytest.mark.parametrize("n,d,k,iters,seed", [(500, 12, 10, 25, 21), (20, 8, 20, 25, 7),
+                                               (100, 6, 1, 25, 9), (3000, 64, 37, 10, 5)])
+def test_kmeans_bitexact(eng, orc, n, d, k, iters, seed):
+    rng = np.random.default_rng(seed)
+    X = rng.normal(0, 3, (n, d)).astype(np.float32)
+    got = eng.kmeans(X, k, iters, seed)
+    cent, asg, obj, it = orc.kmeans(X, k, iters, seed)
+    np.testing.assert_array_equal(got.centroids, cent)
+    np.testing.assert_array_equal(got.assignment, asg)
+    assert got.objective == obj and got.iterations == it
+
+
+def test_build_ivf_matches_reference_layout(eng, orc):
+    raw, t, qr, qt, P = make_fixture(orc, 2500, 32, 8, 10, 45)
+    m = eng.TransformMatrix(32, 46, P)
+    idx = eng.build_ivf(raw, t, m, 20, 47, eng.IvfLayout.kSplit, 8, max_iters=25)
+    ex = idx.export()
+    cent, asg, _, _ = orc.kmeans(t, 20, 25, 47)
+    lay = orc.ivf_layout(raw, t, P, cent, asg, 20, 8, True)
+    for nm in ("centroids_t", "centroids_raw", "list_off", "ids_flat", "a1_t", "a2_t", "a1_raw", "a2_raw"):
+        np.testing.assert_array_equal(ex[nm], lay[nm], err_msg=nm)
+    with pytest.raises(ValueError):
+        eng.build_ivf(raw, t, m, 20, 1, eng.IvfLayout.kSplit, 0)
+    with pytest.raises(ValueError):
+        eng.build_ivf(raw, t, m, 20, 1, eng.IvfLayout.kSplit, 32)
+
+
+@pytest.mark.parametrize("n,d,nq,K", [(3000, 64, 30, 10), (500, 17, 5, 500), (2000, 128, 12, 100)])
+def test_brute_force_knn_bitexact(eng, orc, n, d, nq, K):
+    rng = np.random.default_rng(n + d)
+    base = rng.normal(0, 1, (n, d)).astype(np.float32)
+    base[7] = base[3]  # exact duplicate -> tie broken by id
+    q = rng.normal(0, 1, (nq, d)).astype(np.float32)
+    q[0] = base[3]
+    np.testing.assert_array_equal(eng.brute_force_knn(base, q, K), orc.brute_force_knn(base, q, K))
+    with pytest.raises(ValueError):
+        eng.brute_force_knn(base, q, n + 1)
