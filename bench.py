@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""bench.py — IVF++ ADSampling queries/sec at fixed recall@K on B200.
+
+Metric (BASELINE.json): "IVF++ ADSampling queries/sec at fixed recall@K;
+scanned GB/s vs HBM peak".  Workload: configs[1] (1M x 128, 4096 lists,
+10 000 queries, K=100) at the headline nprobe.  One step = one batch of all
+queries through the whole hot path on the GPU: query rotation (apply, fp64),
+coarse quantizer (fp64 centroid distances + top-nprobe), ADSampling scan
+with top-K (ivf_query, split layout).  Inputs are HBM-resident when the timed
+region starts (`value`); `e2e` repeats the step through the host API with
+pinned host buffers, H2D of the queries and D2H of the results inside.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--nprobe 64]
+    python bench.py --impl reference ...   # the reference's CPU ivf_query (oracle/_ref)
+    python bench.py --mode dco ...         # config-4 fixed-threshold DCO microbench
+
+N > 1 (torchrun): query-sharded replicas (weak scaling): every rank holds the
+index and answers its own 10 000-query batch; no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+# ---------------------------------------------------------------- distributed plumbing
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")  # control plane only: barriers, max-over-ranks
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def allmax(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------- workload setup
+def setup(cfg, dev, rank, log):
+    import paper_2303_09855_b200 as ads
+    from paper_2303_09855_b200 import configs
+
+    t0 = time.time()
+    base, q = configs.generate(cfg, role_base=rank)
+    m = ads.generate_orthogonal(cfg.d, cfg.seed)
+    ctx = ads.Context.default(dev)
+    t = ads.Transform(m, ctx).apply_dataset(base)
+    t1 = time.time()
+    idx = ads.build_ivf(base, t, m, cfg.nlist, cfg.seed, ads.IvfLayout.kSplit, 32,
+                        max_iters=cfg.kmeans_iters, init=cfg.kmeans_init, ctx=ctx)
+    t2 = time.time()
+    gt = ads.brute_force_knn(base, q, cfg.K, ctx=ctx)
+    t3 = time.time()
+    log(f"setup: data+rotate {t1 - t0:.1f}s, build_ivf {t2 - t1:.1f}s, ground truth {t3 - t2:.1f}s")
+    return ads, ctx, base, t, q, m, idx, gt
+
+
+def cpu_baseline_reference(cfg, base, t, m, idx, q, gt, nprobe, budget_s=12.0, log=print):
+    """The reference's ivf_query (oracle/_ref, or the oracle port) on the same index,
+    run_timed protocol (rotation inside the loop), all host threads, bounded sample."""
+    from paper_2303_09855_b200 import configs
+
+    ex = idx.export()
+    asg = configs.list_assignment(ex["list_off"], ex["ids_flat"])
+    cores = os.cpu_count() or 1
+    from oracle import load_oracle, load_ref, ref_available
+
+    if ref_available():
+        ref = load_ref()
+        h = ref.assemble_ivf(base, t, m.entries, ex["centroids_t"], asg, seed=cfg.seed, split=True, d1=32)
+        kind = "reference"
+
+        def run(mode, qs, nthreads):
+            ids, dists, dims, secs = h.query_batch(None, qs, cfg.K, nprobe, mode, 2.1, 32,
+                                                   nthreads=nthreads, P=m.entries)
+            return ids, dims, secs
+    else:  # oracle port, single thread per query loop
+        orc = load_oracle()
+        lay = orc.ivf_layout(base, t, m.entries, ex["centroids_t"], asg, cfg.nlist, 32, True)
+        kind, cores = "port", 1
+
+        def run(mode, qs, nthreads):
+            qt = orc.apply_dataset(m.entries, qs)
+            t0 = time.perf_counter()
+            ids = np.full((len(qs), cfg.K), -1, np.int32)
+            dims = np.zeros(len(qs), np.uint64)
+            for i in range(len(qs)):
+                a, _, s = orc.ivf_query(lay, qt[i], qs[i], cfg.K, nprobe, mode)
+                ids[i, :len(a)] = a
+                dims[i] = s[0]
+            return ids, dims, time.perf_counter() - t0
+
+    # size the sample to ~budget_s of CPU work
+    probe = min(64, len(q))
+    _, _, s = run("ad-split", q[:probe], cores)
+    per_q = s / probe
+    ns = int(max(probe, min(len(q), budget_s / max(per_q, 1e-9))))
+    ids, dims, secs = run("ad-split", q[:ns], cores)
+    rec = float(np.mean([len(np.intersect1d(ids[i], gt[i])) for i in range(ns)]) / cfg.K)
+    fd_ns = min(ns, max(probe, ns // 3))
+    _, _, fd_secs = run("fd", q[:fd_ns], cores)
+    log(f"cpu baseline ({kind}): {ns} queries IVF++ {ns / secs:.0f} QPS, FD {fd_ns / fd_secs:.0f} QPS")
+    return {"value": ns / secs, "unit": "queries/s", "cores": cores, "kind": kind,
+            "sample": f"first {ns} of {len(q)} queries, ivf_query kAdSplit, rotation inside the loop "
+                      f"(run_timed protocol), {cores} host threads over queries, same index",
+            "recall_at_k": rec, "fd_value": fd_ns / fd_secs,
+            "fd_sample": f"first {fd_ns} queries, ivf_query kFd"}, ids, ns
+
+
+# ---------------------------------------------------------------- search bench
+def run_search(args, D: Dist):
+    import paper_2303_09855_b200 as ads  # noqa: F401
+    from paper_2303_09855_b200 import configs
+
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
+    cfg = configs.CONFIGS[args.config]
+    if args.nq:
+        cfg.nq = args.nq
+    if args.kmeans_init >= 0:
+        cfg.kmeans_init = args.kmeans_init
+    if args.kmeans_iters:
+        cfg.kmeans_iters = args.kmeans_iters
+    nprobe = args.nprobe or cfg.nprobe
+    dev = D.local
+    ads, ctx, base, t, q, m, idx, gt = setup(cfg, dev, D.rank, log)
+    K, nq, d = cfg.K, cfg.nq, cfg.d
+    mode = ads.IvfMode.kAdSplit
+    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True)
+
+    # HBM-resident inputs / outputs
+    dq = ads.DeviceArray.from_host(ctx, q)
+    d_ids = ads.DeviceArray(ctx, (nq, K), np.int32)
+    d_dst = ads.DeviceArray(ctx, (nq, K), np.float64)
+    d_cnt = ads.DeviceArray(ctx, (nq,), np.int32)
+    d_dims = ads.DeviceArray(ctx, (nq,), np.uint64)
+    d_cand = ads.DeviceArray(ctx, (nq,), np.uint64)
+    import ctypes as C
+
+    from paper_2303_09855_b200 import _lib as L
+
+    def step():
+        L.check(L.ads_ivf_search_device(idx.h, None, C.c_void_p(dq.ptr), nq, K, nprobe, int(mode),
+                                        2.1, 32, C.byref(opts), C.c_void_p(d_ids.ptr),
+                                        C.c_void_p(d_dst.ptr), C.c_void_p(d_cnt.ptr),
+                                        C.c_void_p(d_dims.ptr), C.c_void_p(d_cand.ptr)))
+
+    for _ in range(args.warmup):
+        ctx.flush_l2()
+        step()
+    ctx.sync()
+    clocks = ClockSampler(dev)
+    step_ms, scan_ms, stage_ms = [], [], []
+    D.barrier()
+    ctx.sync()
+    clocks.start()
+    for _ in range(args.steps):
+        ctx.flush_l2()  # L2 flushed between timed steps (outside the events)
+        ctx.timer_start()
+        step()
+        step_ms.append(ctx.timer_stop())
+        st = idx.last_timings()
+        stage_ms.append(st)
+        scan_ms.append(float(st[3]))
+    ctx.sync()
+    clk = clocks.stop()
+    D.barrier()
+    total_ms = D.allmax(float(np.sum(step_ms)))
+    dims = d_dims.to_host()
+    ids = d_ids.to_host()
+    recall = float(np.mean([len(np.intersect1d(ids[i][ids[i] >= 0], gt[i])) for i in range(nq)]) / K)
+    scanned = 4.0 * float(dims.sum())  # algorithmic bytes per step
+
+    # end to end through the host API with pinned buffers
+    qh = ads.PinnedArray((nq, d), np.float32)
+    qh.array[:] = q
+    out = {nm: ads.PinnedArray(shape, dt) for nm, shape, dt in (
+        ("ids", (nq, K), np.int32), ("dists", (nq, K), np.float64), ("cnt", (nq,), np.int32),
+        ("dims", (nq,), np.uint64), ("cand", (nq,), np.uint64))}
+
+    def e2e_step():
+        L.check(L.ads_ivf_search(idx.h, None, C.c_void_p(qh.ptr), nq, K, nprobe, int(mode), 2.1, 32,
+                                 C.byref(opts), C.c_void_p(out["ids"].ptr), C.c_void_p(out["dists"].ptr),
+                                 C.c_void_p(out["cnt"].ptr), C.c_void_p(out["dims"].ptr),
+                                 C.c_void_p(out["cand"].ptr)))
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    e2e_s = []
+    D.barrier()
+    for _ in range(args.steps):
+        ctx.flush_l2()
+        ctx.sync()
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_total = D.allmax(float(np.sum(e2e_s)))
+    assert np.array_equal(out["ids"].array, ids), "e2e and device-resident results differ"
+
+    world_q = nq * D.world * args.steps
+    value = world_q / (total_ms / 1e3)
+    peaks = measured_peaks()
+    scan_avg = float(np.mean(scan_ms))
+    achieved = scanned / (scan_avg / 1e3) / 1e9
+    stage = np.mean(np.array(stage_ms), axis=0)
+    res = {
+        "metric": "IVF++ ADSampling queries/sec at fixed recall@K",
+        "value": value, "unit": "queries/s", "n_gpus": D.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(cfg.describe(), nprobe=nprobe, recall_at_k=recall,
+                       parallelism=f"replicas{D.world}" if D.world > 1 else "single-gpu",
+                       l2="flushed between timed steps (and index 512 MB > 126 MB L2)",
+                       threshold_refresh={"first": K, "step": args.step}),
+        "e2e": {"value": world_q / e2e_total, "unit": "queries/s",
+                "h2d_bytes_per_step": nq * d * 4,
+                "d2h_bytes_per_step": nq * K * (4 + 8) + nq * (4 + 8 + 8)},
+        "gpu_launches": 4 * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "kernel": "ivf_search_kernel<4>", "peak_source": peaks["source"] + ", copy (burst)",
+                     "algorithmic_bytes_per_launch": scanned,
+                     "scanned_gbs_whole_step": scanned / (float(np.mean(step_ms)) / 1e3) / 1e9},
+        "stages_ms": {"rotate": float(stage[0]), "coarse": float(stage[1]), "select": float(stage[2]),
+                      "scan": float(stage[3])},
+        "dims_per_query": float(dims.mean()), "dims_fraction": float(dims.mean()) / (
+            float(d_cand.to_host().mean()) * d),
+        "clocks": clk,
+    }
+    if D.rank == 0 and not args.no_cpu_baseline:
+        cb, _, _ = cpu_baseline_reference(cfg, base, t, m, idx, q, gt, nprobe, args.cpu_budget, log)
+        res["cpu_baseline"] = cb
+    if args.sweep and D.rank == 0:
+        sw = []
+        for np_ in cfg.sweep:
+            r1 = ads.ivf_query_batch(idx, None, q, K, np_, mode, opts=opts)
+            rf = ads.ivf_query_batch(idx, None, q, K, np_, ads.IvfMode.kFd, opts=opts)
+            ctx.sync()
+            ctx.timer_start()
+            step_np = ads.ivf_query_batch(idx, None, q, K, np_, mode, opts=opts)
+            ms = ctx.timer_stop()
+            sw.append({"nprobe": np_, "recall": ads.recall_batch(r1.ids, gt, K),
+                       "fd_recall": ads.recall_batch(rf.ids, gt, K),
+                       "dims_frac": float(r1.dims.sum()) / float(rf.dims.sum()),
+                       "e2e_qps": nq / (ms / 1e3)})
+            del step_np
+        res["sweep"] = sw
+    return res
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, D: Dist):
+    """The reference's own ivf_query (compiled from /root/reference by oracle/Makefile),
+    on this arm's config, all host threads.  Its index is the one the reference's
+    build_ivf produces (k-means reproduced bit-exactly on the GPU as untimed setup)."""
+    from paper_2303_09855_b200 import configs
+
+    if D.rank != 0:
+        return None
+    log = lambda *a: print(*a, file=sys.stderr, flush=True)  # noqa: E731
+    from oracle import ref_available
+
+    cfg = configs.CONFIGS[args.config]
+    if args.nq:
+        cfg.nq = args.nq
+    nprobe = args.nprobe or cfg.nprobe
+    ads, ctx, base, t, q, m, idx, gt = setup(cfg, 0, 0, log)
+    ex = idx.export()
+    asg = configs.list_assignment(ex["list_off"], ex["ids_flat"])
+    cores = os.cpu_count() or 1
+    if ref_available():
+        from oracle import load_ref
+
+        h = load_ref().assemble_ivf(base, t, m.entries, ex["centroids_t"], asg, seed=cfg.seed,
+                                    split=True, d1=32)
+        kind = "reference"
+    else:
+        return {"impl": "reference", "unavailable": "oracle/_ref/libadsann_ref.so not built"}
+    # bounded sample per step: ~args.cpu_budget / steps seconds each
+    _, _, _, s = h.query_batch(None, q[:64], cfg.K, nprobe, "ad-split", nthreads=cores, P=m.entries)
+    per_q = s / 64
+    ns = int(max(64, min(nq_cap(cfg), args.cpu_budget / max(1, args.steps + args.warmup) / per_q)))
+    for w in range(args.warmup):
+        h.query_batch(None, q[:ns], cfg.K, nprobe, "ad-split", nthreads=cores, P=m.entries)
+    secs = []
+    recs = []
+    for s_ in range(args.steps):
+        lo = (s_ * ns) % max(1, cfg.nq - ns + 1)
+        ids, _, _, sec = h.query_batch(None, q[lo:lo + ns], cfg.K, nprobe, "ad-split",
+                                       nthreads=cores, P=m.entries)
+        secs.append(sec)
+        recs.append(np.mean([len(np.intersect1d(ids[i], gt[lo + i])) for i in range(ns)]) / cfg.K)
+    v = ns * args.steps / float(np.sum(secs))
+    return {"metric": "IVF++ ADSampling queries/sec at fixed recall@K", "value": v,
+            "unit": "queries/s", "n_gpus": D.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean(secs)), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": dict(cfg.describe(), nprobe=nprobe, recall_at_k=float(np.mean(recs))),
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": kind,
+                             "sample": f"{ns} queries per step, ivf_query kAdSplit with rotation "
+                                       f"inside the loop (run_timed protocol), {cores} host threads"},
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def nq_cap(cfg):
+    return cfg.nq
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="search", choices=["search", "dco"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--nprobe", type=int, default=0)
+    ap.add_argument("--nq", type=int, default=0)
+    ap.add_argument("--step", type=int, default=256, help="threshold refresh interval")
+    ap.add_argument("--warps", type=int, default=4)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--kmeans-init", type=int, default=-1, help="override (profiling runs: 1)")
+    ap.add_argument("--kmeans-iters", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    D = Dist()
+    try:
+        if args.impl == "reference":
+            res = run_reference(args, D)
+        elif args.mode == "dco":
+            from bench_dco import run_dco
+
+            res = run_dco(args, D)
+        else:
+            res = run_search(args, D)
+        if D.rank == 0 and res is not None:
+            print(json.dumps(res), flush=True)
+    finally:
+        D.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -62,22 +62,63 @@ __global__ void min_update_kernel(const double* d2, double* min_d2, int64_t n) {
     if (i < n && d2[i] < min_d2[i]) min_d2[i] = d2[i];
 }
 
-// ivf.cpp:85-115, one thread.
-__global__ void kpp_pick_kernel(KppState* st, const double* __restrict__ min_d2,
-                                const unsigned char* __restrict__ chosen, int64_t n) {
+// ivf.cpp:85-115.  The sequential fp64 sum is inherently serial; thread 0
+// runs the dependent add chain while the other threads stage the next chunk
+// of min_d2 in shared memory.  The walk `cum += min_d2[i]; if (cum > u)`
+// revisits the same rounded prefix sums, which are non-decreasing, so the
+// prefix of the first pass is stored and the walk becomes a binary search.
+constexpr int kPickThreads = 256;
+constexpr int kPickChunk = 2048;
+
+__global__ void __launch_bounds__(kPickThreads) kpp_pick_kernel(KppState* st,
+                                                                const double* __restrict__ min_d2,
+                                                                const unsigned char* __restrict__ chosen,
+                                                                double* __restrict__ cum, int64_t n) {
+    __shared__ double buf[2][kPickChunk];
+    __shared__ double s_total;
+    const int tid = threadIdx.x;
+    const int64_t nchunks = (n + kPickChunk - 1) / kPickChunk;
+    for (int i = tid; i < kPickChunk; i += kPickThreads) buf[0][i] = i < n ? min_d2[i] : 0.0;
+    __syncthreads();
     double total = 0.0;
-    for (int64_t i = 0; i < n; ++i) total = __dadd_rn(total, min_d2[i]);
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t base = c * kPickChunk;
+        if (tid == 0) {
+            const double* b = buf[c & 1];
+            const int len = static_cast<int>(n - base < kPickChunk ? n - base : kPickChunk);
+            int i = 0;
+            for (; i + 8 <= len; i += 8) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    total = __dadd_rn(total, b[i + u]);
+                    cum[base + i + u] = total;
+                }
+            }
+            for (; i < len; ++i) {
+                total = __dadd_rn(total, b[i]);
+                cum[base + i] = total;
+            }
+        } else if (c + 1 < nchunks) {
+            const int64_t nb = base + kPickChunk;
+            for (int i = tid - 1; i < kPickChunk; i += kPickThreads - 1)
+                buf[(c + 1) & 1][i] = nb + i < n ? min_d2[nb + i] : 0.0;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) s_total = total;
+    __syncthreads();
+    if (tid != 0) return;
+    total = s_total;
     int64_t pick = -1;
     if (total > 0.0) {
         const double u = __dmul_rn(static_cast<double>(next_u64(&st->rng) >> 11) * 0x1.0p-53, total);
-        double cum = 0.0;
-        for (int64_t i = 0; i < n; ++i) {
-            cum = __dadd_rn(cum, min_d2[i]);
-            if (cum > u) {
-                pick = i;
-                break;
-            }
+        int64_t lo = 0, hi = n;  // first i with cum[i] > u, or n
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (cum[mid] > u) hi = mid;
+            else lo = mid + 1;
         }
+        if (lo < n) pick = lo;
         if (pick < 0)
             for (int64_t i = n - 1; i >= 0; --i)
                 if (min_d2[i] > 0.0) {
@@ -376,7 +417,7 @@ KmeansOut run_kmeans(const float* dX, int64_t n, int d, int k, int max_iters, ui
             if (c + 1 == k) break;
             launch_coarse_dist(crow, 1, dX, static_cast<int>(n), d, dtmp, st);
             min_update_kernel<<<blocks_for(n, 256), 256, 0, st>>>(dtmp, min_d2, n);
-            kpp_pick_kernel<<<1, 1, 0, st>>>(kst, min_d2, flags, n);
+            kpp_pick_kernel<<<1, kPickThreads, 0, st>>>(kst, min_d2, flags, dtmp, n);
         }
         ADS_CUDA(cudaStreamSynchronize(st));  // buf must outlive the copy
         ADS_LAUNCH_CHECK();
