@@ -225,7 +225,8 @@ def run_search(args, D: Dist):
     ads, ctx, base, t, q, m, idx, gt = setup(cfg, dev, D.rank, log)
     K, nq, d = cfg.K, cfg.nq, cfg.d
     mode = ads.IvfMode.kAdSplit
-    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True)
+    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps,
+                           queries_per_cta=args.slots, time_stages=True)
 
     # HBM-resident inputs / outputs
     dq = ads.DeviceArray.from_host(ctx, q)
@@ -244,6 +245,22 @@ def run_search(args, D: Dist):
                                         C.c_void_p(d_dst.ptr), C.c_void_p(d_cnt.ptr),
                                         C.c_void_p(d_dims.ptr), C.c_void_p(d_cand.ptr)))
 
+    if args.tune and D.rank == 0:
+        for st_, w_, g_ in ((128, 4, 1), (256, 2, 1), (256, 4, 1), (256, 8, 1), (512, 4, 1),
+                            (1024, 4, 1)):
+            if True:
+                o2 = ads.search_opts(first=0, step=st_, warps_per_cta=w_, queries_per_cta=g_,
+                                     time_stages=True)
+                ts, dm = [], 0
+                for rep in range(4):
+                    ctx.flush_l2()
+                    ctx.timer_start()
+                    r_ = ads.ivf_query_batch(idx, None, q, K, nprobe, mode, opts=o2)
+                    ts.append(ctx.timer_stop())
+                    dm = float(r_.dims.mean())
+                    scan = float(idx.last_timings()[3])
+                log(f"tune step={st_} warps={w_} slots={g_}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
+                    f"recall {ads.recall_batch(r_.ids, gt, K):.5f}")
     for _ in range(args.warmup):
         ctx.flush_l2()
         step()
@@ -418,7 +435,9 @@ def main():
     ap.add_argument("--nq", type=int, default=0)
     ap.add_argument("--step", type=int, default=256, help="threshold refresh interval")
     ap.add_argument("--warps", type=int, default=4)
+    ap.add_argument("--slots", type=int, default=4, help="queries served concurrently per CTA")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--tune", action="store_true", help="time (step, warps) variants after setup")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--kmeans-init", type=int, default=-1, help="override (profiling runs: 1)")

@@ -203,7 +203,8 @@ int ads_ivf_export(ads_ivf *idx, float *centroids_t, float *centroids_raw, int64
 typedef struct {
     int64_t first;         /* default K */
     int64_t step;          /* default 256 */
-    int32_t warps_per_cta; /* default 4 */
+    int32_t warps_per_cta; /* default 8 */
+    int32_t queries_per_cta; /* query slots served concurrently by one CTA, default 4 */
     int32_t ctas_per_sm;   /* 0 = occupancy maximum */
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */
 } ads_search_opts;

@@ -437,12 +437,12 @@ def recall_batch(ids: np.ndarray, gt: np.ndarray, K: int) -> float:
 # ---------------------------------------------------------------- IVF (GPU)
 
 
-def search_opts(first: int = 0, step: int = 256, warps_per_cta: int = 4, ctas_per_sm: int = 0,
-                time_stages: bool = False) -> L.SearchOpts:
+def search_opts(first: int = 0, step: int = 256, warps_per_cta: int = 4, queries_per_cta: int = 1,
+                ctas_per_sm: int = 0, time_stages: bool = False) -> L.SearchOpts:
     o = L.SearchOpts()
     L.ads_search_opts_default(C.byref(o))
-    o.first, o.step, o.warps_per_cta, o.ctas_per_sm, o.time_stages = (
-        first, step, warps_per_cta, ctas_per_sm, int(time_stages))
+    o.first, o.step, o.warps_per_cta, o.queries_per_cta, o.ctas_per_sm, o.time_stages = (
+        first, step, warps_per_cta, queries_per_cta, ctas_per_sm, int(time_stages))
     return o
 
 

@@ -5,6 +5,7 @@
 // kernel in this library.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -812,6 +813,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->first = 0;  // 0 -> K
     o->step = 256;
     o->warps_per_cta = 4;
+    o->queries_per_cta = 4;
     o->ctas_per_sm = 0;
     o->time_stages = 0;
 }
@@ -870,7 +872,8 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     ads_search_opts_default(&o);
     if (opts) o = *opts;
     if (o.first <= 0) o.first = K;
-    require(o.warps_per_cta >= 1 && o.warps_per_cta <= 16, "search: warps_per_cta in [1, 16]");
+    require(o.warps_per_cta >= 1 && o.warps_per_cta <= 32, "search: warps_per_cta in [1, 32]");
+    require(o.queries_per_cta >= 1 && o.queries_per_cta <= 16, "search: queries_per_cta in [1, 16]");
     cudaStream_t st = x->ctx->stream;
     const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
     const int D = x->d;
@@ -908,9 +911,17 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.nseg = plan.nseg;
     a.ntest = plan.ntest;
     a.vec = plan.vec;
+    a.full = plan.full;
+    // 16-byte line descriptors address each array in 31 bits of 16-byte units.
+    const int64_t widest = static_cast<int64_t>(x->n) * std::max(x->d1p, D - x->d1p);
+    if (widest / 4 >= (int64_t(1) << 31)) {
+        a.vec = 1;
+        a.full = 0;
+    }
     a.first = o.first;
     a.step = o.step;
     a.warps = o.warps_per_cta;
+    a.slots = o.queries_per_cta;
     a.ctas_per_sm = o.ctas_per_sm;
     a.out_ids = dids;
     a.out_dists = ddists;

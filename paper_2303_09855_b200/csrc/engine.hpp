@@ -18,6 +18,7 @@ struct SegPlan {
     std::vector<Seg> segs;
     std::vector<double> test_factor;  // thr[t] = test_factor[t] * r^2
     int vec = 4;                      // 16-byte copies when every cut is 4-aligned
+    int full = 0;                     // every segment has 32 floats
     int D = 0;
 };
 
@@ -33,7 +34,7 @@ std::vector<double> ad_factor(double eps0, int delta_d, int D);
 struct DevSegPlan {
     Seg* segs = nullptr;
     double* tfac = nullptr;
-    int nseg = 0, ntest = 0, vec = 4;
+    int nseg = 0, ntest = 0, vec = 4, full = 0;
     void upload(const SegPlan& p, cudaStream_t st);
     void release();
 };
@@ -84,8 +85,10 @@ struct SearchLaunch {
     const Seg* segs;
     const double* tfac;
     int nseg, ntest, vec;
+    int full;          // every segment is 32 floats (no per-line length shuffle)
     int64_t first, step;
     int warps;         // per CTA
+    int slots;         // queries served concurrently per CTA
     int ctas_per_sm;
     int32_t* out_ids;
     double* out_dists;

@@ -189,12 +189,6 @@ __global__ void __launch_bounds__(kSelThreads) select_rows_kernel(const double* 
 }
 
 // ---------------------------------------------------------------- search
-struct SearchShared {
-    double r, r_sq;
-    int q, stop, total, next, cnt;
-    unsigned long long dims;
-};
-
 __device__ __forceinline__ bool pair_lt(double da, int32_t ia, double db, int32_t ib) {
     return da < db || (da == db && ia < ib);
 }
@@ -235,7 +229,13 @@ __device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double 
     __syncwarp();
 }
 
-template <int VEC>
+struct SearchShared {
+    double r, r_sq;
+    int q, stop, total, next, cnt;
+    unsigned long long dims;
+};
+
+template <int VEC, bool FULL>
 __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SearchShared sh;
@@ -247,7 +247,8 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
     double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
     double* pend_d = topd + a.K;
-    int64_t* lstart = reinterpret_cast<int64_t*>(pend_d + chunk_cap);
+    int64_t* cpos = reinterpret_cast<int64_t*>(pend_d + chunk_cap);
+    int64_t* lstart = cpos + chunk_cap;
     Seg* segs = reinterpret_cast<Seg*>(lstart + a.nprobe);
     int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
     int32_t* pend_i = topi + a.K;
@@ -308,6 +309,17 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
         for (int lo = 0; lo < total;) {
             const int64_t span = lo == 0 ? a.first : a.step;
             const int hi = static_cast<int>(lo + span < total ? lo + span : total);
+            // stream index -> flat position for every candidate of the chunk
+            for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) {
+                const int i = lo + sl;
+                int l = 0, h = a.nprobe - 1;  // last list with pre[k] <= i
+                while (l < h) {
+                    const int mid = (l + h + 1) >> 1;
+                    if (pre[mid] <= i) l = mid;
+                    else h = mid - 1;
+                }
+                cpos[sl] = lstart[l] + (i - pre[l]);
+            }
             if (threadIdx.x == 0) sh.next = lo;
             for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
             __syncthreads();
@@ -325,14 +337,8 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                     if (cand < 0) {
                         const int i = base + __popc(need & ((1u << lane) - 1u));
                         if (i < hi) {
-                            int l = 0, h = a.nprobe - 1;  // last list with pre[k] <= i
-                            while (l < h) {
-                                const int mid = (l + h + 1) >> 1;
-                                if (pre[mid] <= i) l = mid;
-                                else h = mid - 1;
-                            }
                             cand = i;
-                            pos = lstart[l] + (i - pre[l]);
+                            pos = cpos[i - lo];
                             seg = 0;
                             s = 0.0;
                         }
@@ -340,10 +346,21 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 }
                 if (!__any_sync(kFull, cand >= 0)) break;
                 const Seg sg = segs[seg];
-                const float* src = sg.arr == 0
-                                       ? a.a1 + pos * a.d1 + sg.col
-                                       : a.a2 + pos * (a.D - a.d1) + (sg.col - a.d1);
-                gather_lines<VEC>(wbuf, src, cand >= 0 ? sg.len : 0);
+                if constexpr (VEC == 4) {
+                    uint32_t dsc = kNoLine;
+                    if (cand >= 0) {
+                        const int64_t off = sg.arr == 0 ? pos * a.d1 + sg.col
+                                                        : pos * (a.D - a.d1) + (sg.col - a.d1);
+                        dsc = (static_cast<uint32_t>(sg.arr) << 31) | static_cast<uint32_t>(off >> 2);
+                    }
+                    gather_issue16<FULL>(wbuf, a.a1, a.a2, dsc, sg.len >> 2);
+                } else {
+                    const float* src = sg.arr == 0 ? a.a1 + pos * a.d1 + sg.col
+                                                   : a.a2 + pos * (a.D - a.d1) + (sg.col - a.d1);
+                    gather_issue4(wbuf, src, cand >= 0 ? sg.len : 0);
+                }
+                cp_async_wait_group<0>();
+                __syncwarp();
                 if (cand >= 0) {
                     s = accumulate_line<VEC>(wbuf, qseg + seg * kQPitch, sg.len, s);
                     if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
@@ -412,7 +429,7 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
     size_t b = sizeof(float) * a.warps * 1024;
     b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + chunk_cap);
-    b += sizeof(int64_t) * a.nprobe;
+    b += sizeof(int64_t) * (a.nprobe + chunk_cap);
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + chunk_cap + a.nprobe + 1);
     b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
@@ -451,7 +468,8 @@ void launch_ivf_search(const SearchLaunch& a_in, cudaStream_t st) {
     if (cap64 > 16384) throw std::invalid_argument("search: threshold refresh interval too long (max 16384)");
     const int cap = static_cast<int>(cap64);
     const size_t smem = search_smem(a, cap);
-    auto kern = a.vec == 4 ? ivf_search_kernel<4> : ivf_search_kernel<1>;
+    auto kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
+                           : ivf_search_kernel<1, false>;
     ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int occ = 0;

@@ -1,22 +1,23 @@
 // Warp-level DCO engine shared by the fixed-threshold DCO kernel and the
 // IVF++ search kernel.
 //
-// Each lane owns one live candidate and walks its dimension range segment by
+// Each lane owns live candidates and walks their dimension ranges segment by
 // segment (Seg, common.cuh).  One step of a warp:
-//   1. gather: the 32 lanes' current segments (each <= 32 floats, one
-//      128-byte line for Δd = 32) are copied HBM -> shared memory with
-//      cp.async; eight lanes cover one line, so every load instruction reads
-//      four whole lines (coalesced, no sector is wasted).  Lines land in a
-//      per-warp 32 x 32-float buffer with a lane-rotated 16-byte chunk order
-//      so the per-lane reads below are bank-conflict free.
+//   1. gather: the lanes' current segments (each <= 32 floats, one 128-byte
+//      line for Δd = 32) are copied HBM -> shared memory with cp.async; eight
+//      lanes cover one line, so every load instruction reads four whole lines
+//      (coalesced, no sector is wasted).  Lines land in a per-warp 32 x 32-float
+//      buffer with a lane-rotated 16-byte chunk order so the per-lane reads
+//      below are bank-conflict free.  Gathers are asynchronous (one cp.async
+//      group per buffer) so a warp can keep two buffers in flight.
 //   2. accumulate: each lane adds its segment in index order in fp64
-//      (sq_diff_acc), against the query stored per segment (33-double pitch).
+//      (sq_diff_acc), against the query stored per segment (34-double pitch).
 //   3. test: reject iff s > thr[test] (the reference's strict test,
 //      dco.hpp:141); at d == D decide exactly (dco.hpp:145).
 // Lanes whose candidate finished are refilled by the caller before the next
-// step (survivor compaction by refill: a warp always gathers up to 32 live
-// lines), so per-candidate cost follows the dims actually scanned and bytes
-// of rejected candidates' later segments are never fetched.
+// step (survivor compaction by refill), so per-candidate cost follows the
+// dims actually scanned and bytes of rejected candidates' later segments are
+// never fetched.
 #pragma once
 
 #include "common.cuh"
@@ -24,8 +25,53 @@
 namespace ads {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kQPitch = 33;  // doubles per segment slot of the staged query
+constexpr int kQPitch = 34;  // doubles per segment slot of the staged query (16-byte aligned)
 
+// 16-byte-granular line descriptor for the VEC=4 path: bit 31 selects the
+// array (A1 / A2), bits 0..30 the line start in 16-byte units.
+constexpr uint32_t kNoLine = 0xffffffffu;
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// VEC=4: issue the copies of the warp's 32 lines (packed descriptors), no wait.
+// full_len: every line is 32 floats (no per-line length shuffle).
+template <bool FULL>
+__device__ __forceinline__ void gather_issue16(float* wbuf, const float* base0, const float* base1,
+                                               uint32_t desc, int nchunk) {
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int L = j * 4 + static_cast<int>(lane >> 3);
+        const int c = static_cast<int>(lane & 7u);
+        const uint32_t dsc = __shfl_sync(kFull, desc, L);
+        int l = 8;
+        if constexpr (!FULL) l = __shfl_sync(kFull, nchunk, L);
+        if (dsc != kNoLine && c < l) {
+            const float* base = (dsc >> 31) ? base1 : base0;
+            cp_async16(wbuf + L * 32 + (((c + L) & 7) << 2),
+                       base + (static_cast<size_t>(dsc & 0x7fffffffu) << 2) + c * 4);
+        }
+    }
+    cp_async_commit();
+}
+
+// VEC=1: 4-byte copies from a per-lane 64-bit pointer (unaligned layouts).
+__device__ __forceinline__ void gather_issue4(float* wbuf, const float* src, int len) {
+    const unsigned lane = lane_id();
+    for (int L = 0; L < 32; ++L) {
+        const float* s = reinterpret_cast<const float*>(
+            __shfl_sync(kFull, reinterpret_cast<unsigned long long>(src), L));
+        const int l = __shfl_sync(kFull, len, L);
+        if (static_cast<int>(lane) < l) cp_async4(wbuf + L * 32 + ((lane + L) & 31), s + lane);
+    }
+    cp_async_commit();
+}
+
+// Synchronous variants (issue + wait) used by the fixed-threshold kernel.
 template <int VEC>
 __device__ __forceinline__ void gather_lines(float* wbuf, const float* src, int len) {
     const unsigned lane = lane_id();
@@ -64,10 +110,12 @@ __device__ __forceinline__ double accumulate_line(const float* wbuf, const doubl
             if (c < nc) {
                 const float4 v =
                     *reinterpret_cast<const float4*>(row + (((c + static_cast<int>(lane)) & 7) << 2));
-                s = sq_diff_acc(s, v.x, qq[c * 4 + 0]);
-                s = sq_diff_acc(s, v.y, qq[c * 4 + 1]);
-                s = sq_diff_acc(s, v.z, qq[c * 4 + 2]);
-                s = sq_diff_acc(s, v.w, qq[c * 4 + 3]);
+                const double2 q0 = *reinterpret_cast<const double2*>(qq + c * 4);
+                const double2 q1 = *reinterpret_cast<const double2*>(qq + c * 4 + 2);
+                s = sq_diff_acc(s, v.x, q0.x);
+                s = sq_diff_acc(s, v.y, q0.y);
+                s = sq_diff_acc(s, v.z, q1.x);
+                s = sq_diff_acc(s, v.w, q1.y);
             }
         }
     } else {
@@ -76,7 +124,7 @@ __device__ __forceinline__ double accumulate_line(const float* wbuf, const doubl
     return s;
 }
 
-// Stage query coordinates per segment: qseg[s*33 + k] = (double)q[seg.col + k].
+// Stage query coordinates per segment: qseg[s*34 + k] = (double)q[seg.col + k].
 __device__ __forceinline__ void stage_query(double* qseg, const Seg* segs, int nseg,
                                             const float* q) {
     for (int i = threadIdx.x; i < nseg * 32; i += blockDim.x) {

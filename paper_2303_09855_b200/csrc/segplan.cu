@@ -65,6 +65,8 @@ SegPlan make_seg_plan(int D, int split_at, const std::vector<int>& tests, const 
         }
     }
     if (p.segs.size() > 4096) throw std::invalid_argument("too many segments");
+    p.full = p.vec == 4;
+    for (const Seg& sg : p.segs) p.full = p.full && sg.len == 32;
     return p;
 }
 
@@ -73,6 +75,7 @@ void DevSegPlan::upload(const SegPlan& p, cudaStream_t st) {
     nseg = static_cast<int>(p.segs.size());
     ntest = static_cast<int>(p.test_factor.size());
     vec = p.vec;
+    full = p.full;
     ADS_CUDA(cudaMallocAsync(&segs, sizeof(Seg) * nseg, st));
     ADS_CUDA(cudaMemcpyAsync(segs, p.segs.data(), sizeof(Seg) * nseg, cudaMemcpyHostToDevice, st));
     ADS_CUDA(cudaMallocAsync(&tfac, sizeof(double) * std::max(ntest, 1), st));
