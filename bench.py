@@ -35,16 +35,22 @@ sys.path.insert(0, ROOT)
 
 # ---------------------------------------------------------------- distributed plumbing
 class Dist:
-    def __init__(self):
+    def __init__(self, backend="gloo"):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.nccl = None
         if self.world > 1:
+            import torch
             import torch.distributed as dist
 
-            dist.init_process_group("gloo")  # control plane only: barriers, max-over-ranks
+            # control plane (barriers, max-over-ranks) on gloo; data path on NCCL
+            dist.init_process_group("gloo")
             self.pg = dist
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+                self.nccl = dist.new_group(backend="nccl")
 
     def barrier(self):
         if self.pg:
@@ -364,6 +370,133 @@ def run_search(args, D: Dist):
     return res
 
 
+# ---------------------------------------------------------------- list-sharded search (N > 1)
+def run_search_sharded(args, D: Dist):
+    """IVF lists partitioned over the N GPUs (LPT on list sizes); every rank scans
+    all queries over its own lists, the per-rank top-K go through one NCCL
+    all-gather per result array on the engine's stream and a merge kernel keeps
+    the K smallest (dist, id) pairs.  Weak scaling: the job answers N x nq
+    queries per step (each rank contributes its own nq-query batch)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2303_09855_b200 as ads
+    from paper_2303_09855_b200 import _lib as L
+    from paper_2303_09855_b200 import configs
+    from paper_2303_09855_b200.shard import merge_topk_device, partition_lists, shard_index
+
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
+    cfg = configs.CONFIGS[args.config]
+    if args.nq:
+        cfg.nq = args.nq
+    if args.kmeans_init >= 0:
+        cfg.kmeans_init = args.kmeans_init
+    if args.kmeans_iters:
+        cfg.kmeans_iters = args.kmeans_iters
+    nprobe = args.nprobe or cfg.nprobe
+    W, K, d = D.world, cfg.K, cfg.d
+    torch.cuda.set_device(D.local)
+    t0 = time.time()
+    base, _ = configs.generate(cfg, nq=1)
+    qs = np.concatenate([configs.generate(cfg, role_base=r, nq=cfg.nq)[1] for r in range(W)])
+    nq = qs.shape[0]
+    m = ads.generate_orthogonal(d, cfg.seed)
+    ctx = ads.Context.default(D.local)
+    t = ads.Transform(m, ctx).apply_dataset(base)
+    full = ads.build_ivf(base, t, m, cfg.nlist, cfg.seed, ads.IvfLayout.kSplit, 32,
+                         max_iters=cfg.kmeans_iters, init=cfg.kmeans_init, ctx=ctx)
+    sizes = np.diff(full.export()["list_off"])
+    owner = partition_lists(sizes, W)
+    local = shard_index(full, owner, D.rank)
+    del full
+    gt = ads.brute_force_knn(base, qs, K, ctx=ctx) if D.rank == 0 else None
+    log(f"sharded setup {time.time() - t0:.1f}s: {W} ranks, local rows {local.n} "
+        f"(max/min shard rows {np.bincount(owner, weights=sizes).max():.0f}/"
+        f"{np.bincount(owner, weights=sizes).min():.0f})")
+
+    dev = torch.device("cuda", D.local)
+    stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
+    dq = torch.from_numpy(qs).to(dev)
+    li = torch.empty((nq, K), dtype=torch.int32, device=dev)
+    ld = torch.empty((nq, K), dtype=torch.float64, device=dev)
+    lc = torch.empty((nq,), dtype=torch.int32, device=dev)
+    lm = torch.empty((nq,), dtype=torch.int64, device=dev)
+    ln = torch.empty((nq,), dtype=torch.int64, device=dev)
+    gi = torch.empty((W, nq, K), dtype=torch.int32, device=dev)
+    gd = torch.empty((W, nq, K), dtype=torch.float64, device=dev)
+    oi = torch.empty((nq, K), dtype=torch.int32, device=dev)
+    od = torch.empty((nq, K), dtype=torch.float64, device=dev)
+    oc = torch.empty((nq,), dtype=torch.int32, device=dev)
+    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True)
+    mode = ads.IvfMode.kAdSplit
+    torch.cuda.synchronize()
+
+    def step():
+        L.check(L.ads_ivf_search_device(local.h, None, C.c_void_p(dq.data_ptr()), nq, K, nprobe,
+                                        int(mode), 2.1, 32, C.byref(opts), C.c_void_p(li.data_ptr()),
+                                        C.c_void_p(ld.data_ptr()), C.c_void_p(lc.data_ptr()),
+                                        C.c_void_p(lm.data_ptr()), C.c_void_p(ln.data_ptr())))
+        with torch.cuda.stream(stream):
+            D.pg.all_gather_into_tensor(gi, li, group=D.nccl)
+            D.pg.all_gather_into_tensor(gd, ld, group=D.nccl)
+        merge_topk_device(ctx, gd.data_ptr(), gi.data_ptr(), W, nq, K, oi.data_ptr(),
+                          od.data_ptr(), oc.data_ptr())
+
+    for _ in range(args.warmup):
+        ctx.flush_l2()
+        step()
+    ctx.sync()
+    clocks = ClockSampler(D.local)
+    D.barrier()
+    ctx.sync()
+    clocks.start()
+    ms = []
+    for _ in range(args.steps):
+        ctx.flush_l2()
+        D.barrier()
+        ctx.timer_start()
+        step()
+        ms.append(ctx.timer_stop())
+    clk = clocks.stop()
+    total_ms = D.allmax(float(np.sum(ms)))
+    dims = D.allsum(float(lm.sum().item()))
+    res = {
+        "metric": "IVF++ ADSampling queries/sec at fixed recall@K", "value": nq * args.steps / (total_ms / 1e3),
+        "unit": "queries/s", "n_gpus": W, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(cfg.describe(), nprobe=nprobe, nq_total=nq,
+                       parallelism=f"list-sharded x{W} + NCCL all-gather + merge"),
+        "gpu_launches": 5 * args.steps + 2 * args.steps,
+        "scanned_gb_per_step_all_ranks": 4.0 * dims / 1e9,
+        "clocks": clk,
+    }
+    if D.rank == 0:
+        ids = oi.cpu().numpy()
+        res["config"]["recall_at_k"] = float(np.mean([len(np.intersect1d(ids[i][ids[i] >= 0], gt[i]))
+                                                      for i in range(nq)]) / K)
+    # e2e: host queries in, merged results out (pinned buffers), same collective path
+    qh = ads.PinnedArray((nq, d), np.float32)
+    qh.array[:] = qs
+    hout = ads.PinnedArray((nq, K), np.int32)
+    e2e = []
+    for _ in range(args.steps):
+        D.barrier()
+        t1 = time.perf_counter()
+        dq.copy_(torch.from_numpy(qh.array), non_blocking=True)
+        torch.cuda.synchronize()
+        step()
+        ctx.sync()
+        torch.cuda.synchronize()
+        hout.array[:] = oi.cpu().numpy()
+        e2e.append(time.perf_counter() - t1)
+    e2e_total = D.allmax(float(np.sum(e2e)))
+    res["e2e"] = {"value": nq * args.steps / e2e_total, "unit": "queries/s",
+                  "h2d_bytes_per_step": nq * d * 4, "d2h_bytes_per_step": nq * K * 4}
+    return res
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, D: Dist):
     """The reference's own ivf_query (compiled from /root/reference by oracle/Makefile),
@@ -441,11 +574,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--kmeans-init", type=int, default=-1, help="override (profiling runs: 1)")
+    ap.add_argument("--shard", default="lists", choices=["lists", "replicas"],
+                    help="N>1: IVF lists partitioned across GPUs + NCCL all-gather merge, or replicas")
+    ap.add_argument("--dco-n", type=int, default=10_000_000)
     ap.add_argument("--kmeans-iters", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    D = Dist()
+    sharded = args.impl == "ours" and args.mode == "search" and args.shard == "lists"
+    D = Dist("nccl" if sharded else "gloo")
     try:
         if args.impl == "reference":
             res = run_reference(args, D)
@@ -453,6 +590,8 @@ def main():
             from bench_dco import run_dco
 
             res = run_dco(args, D)
+        elif sharded and D.world > 1:
+            res = run_search_sharded(args, D)
         else:
             res = run_search(args, D)
         if D.rank == 0 and res is not None:

@@ -85,6 +85,8 @@ typedef struct ads_ctx ads_ctx;
 int ads_ctx_create(int32_t device, ads_ctx **out);
 int ads_ctx_destroy(ads_ctx *ctx);
 int ads_ctx_sync(ads_ctx *ctx);
+/* The context's cudaStream_t (as void*), so a host can enqueue collectives on it. */
+int ads_ctx_stream(ads_ctx *ctx, void **stream);
 /* Device memory helpers (so hosts without torch can stage resident inputs). */
 int ads_dev_alloc(ads_ctx *ctx, int64_t bytes, void **dptr);
 int ads_dev_free(ads_ctx *ctx, void *dptr);
@@ -230,6 +232,22 @@ int ads_ivf_probe_order(ads_ivf *idx, const float *Q, int32_t nq, int32_t nprobe
                         int32_t transformed, int32_t *probes);
 /* Stage times (ms) of the last search with opts.time_stages: [rotate, coarse, select, scan]. */
 int ads_ivf_last_timings(ads_ivf *idx, float *ms4);
+
+/* ------------------------------------------------------------------ list sharding (multi-GPU)
+ * Shard of an index for one GPU: same k_clusters, centroids and P (probe order is
+ * global), but only lists with keep[c] != 0 keep their rows; the others become
+ * empty.  Searching the shard scans the global probe-ordered candidate stream
+ * restricted to the owned lists.  No reference counterpart (the reference is
+ * single-process); the merged result is the K smallest (dist, id) pairs. */
+int ads_ivf_subset(ads_ivf *src, const uint8_t *keep, ads_ivf **out);
+/* Per query, the K smallest (dist, id) pairs (ties by id; NaN / id<0 entries
+ * ignored) among G result lists of K: dists/ids are [G][nq][K] (the layout of
+ * an all-gather of per-shard outputs). */
+int ads_merge_topk(ads_ctx *ctx, const double *dists, const int32_t *ids, int32_t G, int32_t nq,
+                   int32_t K, int32_t *out_ids, double *out_dists, int32_t *out_counts);
+int ads_merge_topk_device(ads_ctx *ctx, const double *ddists, const int32_t *dids, int32_t G,
+                          int32_t nq, int32_t K, int32_t *dout_ids, double *dout_dists,
+                          int32_t *dout_counts);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,7 @@ ads_synth = _sig("ads_synth", [C.POINTER(SynthDesc), vp, vp])
 ads_ctx_create = _sig("ads_ctx_create", [i32, C.POINTER(vp)])
 ads_ctx_destroy = _sig("ads_ctx_destroy", [vp])
 ads_ctx_sync = _sig("ads_ctx_sync", [vp])
+ads_ctx_stream = _sig("ads_ctx_stream", [vp, C.POINTER(vp)])
 ads_dev_alloc = _sig("ads_dev_alloc", [vp, i64, C.POINTER(vp)])
 ads_dev_free = _sig("ads_dev_free", [vp, vp])
 ads_memcpy_h2d = _sig("ads_memcpy_h2d", [vp, vp, vp, i64])
@@ -107,6 +108,9 @@ ads_ivf_search_device = _sig("ads_ivf_search_device", [vp, vp, vp, i32, i32, i32
                                                        C.POINTER(SearchOpts), vp, vp, vp, vp, vp])
 ads_ivf_probe_order = _sig("ads_ivf_probe_order", [vp, vp, i32, i32, i32, vp])
 ads_ivf_last_timings = _sig("ads_ivf_last_timings", [vp, vp])
+ads_ivf_subset = _sig("ads_ivf_subset", [vp, vp, C.POINTER(vp)])
+ads_merge_topk = _sig("ads_merge_topk", [vp, vp, vp, i32, i32, i32, vp, vp, vp])
+ads_merge_topk_device = _sig("ads_merge_topk_device", [vp, vp, vp, i32, i32, i32, vp, vp, vp])
 
 
 def check(rc: int) -> None:

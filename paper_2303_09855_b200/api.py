@@ -134,6 +134,12 @@ class Context:
     def sync(self):
         check(L.ads_ctx_sync(self.h))
 
+    def stream_handle(self) -> int:
+        """cudaStream_t of this context (e.g. for torch.cuda.ExternalStream)."""
+        p = C.c_void_p()
+        check(L.ads_ctx_stream(self.h, C.byref(p)))
+        return p.value or 0
+
     def timer_start(self):
         check(L.ads_timer_start(self.h))
 

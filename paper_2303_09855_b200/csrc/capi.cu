@@ -243,6 +243,10 @@ int ads_ctx_sync(ads_ctx* ctx) {
     });
 }
 
+int ads_ctx_stream(ads_ctx* ctx, void** stream) {
+    return guard([&] { *stream = static_cast<void*>(ctx->stream); });
+}
+
 int ads_dev_alloc(ads_ctx* ctx, int64_t bytes, void** dptr) {
     return guard([&] {
         ctx->use();
@@ -1001,6 +1005,116 @@ int ads_ivf_probe_order(ads_ivf* x, const float* Q, int32_t nq, int32_t nprobe, 
         launch_select_probes(dist, nq, x->k, nprobe, dp, st);
         ADS_CUDA(cudaMemcpyAsync(probes, dp, sizeof(int32_t) * nq * nprobe, cudaMemcpyDeviceToHost, st));
         ADS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ads_ivf_subset(ads_ivf* src, const uint8_t* keep, ads_ivf** out) {
+    return guard([&] {
+        ads_ctx* ctx = src->ctx;
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        const int k = src->k, D = src->d, d1p = src->d1p, d2p = D - d1p;
+        std::vector<int64_t> off(static_cast<size_t>(k) + 1);
+        ADS_CUDA(cudaMemcpyAsync(off.data(), src->list_off, sizeof(int64_t) * (k + 1),
+                                 cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        std::vector<int64_t> noff(static_cast<size_t>(k) + 1, 0);
+        for (int c = 0; c < k; ++c) noff[c + 1] = noff[c] + (keep[c] ? off[c + 1] - off[c] : 0);
+        const int64_t nl = noff[k];
+        auto x = std::make_unique<ads_ivf>();
+        x->ctx = ctx;
+        x->n = static_cast<int>(nl);
+        x->d = D;
+        x->k = k;
+        x->d1 = src->d1;
+        x->layout = src->layout;
+        x->seed = src->seed;
+        x->d1p = d1p;
+        x->has_raw = src->has_raw;
+        ivf_alloc_common(x.get());
+        const size_t nn = static_cast<size_t>(nl > 0 ? nl : 1);
+        ADS_CUDA(cudaMalloc(&x->cent_t, sizeof(float) * k * static_cast<size_t>(D)));
+        ADS_CUDA(cudaMemcpyAsync(x->cent_t, src->cent_t, sizeof(float) * k * static_cast<size_t>(D),
+                                 cudaMemcpyDeviceToDevice, st));
+        x->list_off = dev_upload(noff.data(), noff.size(), st);
+        ADS_CUDA(cudaMalloc(&x->ids, sizeof(int32_t) * nn));
+        ADS_CUDA(cudaMalloc(&x->a1_t, sizeof(float) * nn * d1p));
+        ADS_CUDA(cudaMalloc(&x->a2_t, sizeof(float) * (nn * d2p > 0 ? nn * d2p : 1)));
+        if (x->has_raw) {
+            ADS_CUDA(cudaMalloc(&x->cent_raw, sizeof(float) * k * static_cast<size_t>(D)));
+            ADS_CUDA(cudaMemcpyAsync(x->cent_raw, src->cent_raw, sizeof(float) * k * static_cast<size_t>(D),
+                                     cudaMemcpyDeviceToDevice, st));
+            ADS_CUDA(cudaMalloc(&x->a1_raw, sizeof(float) * nn * d1p));
+            ADS_CUDA(cudaMalloc(&x->a2_raw, sizeof(float) * (nn * d2p > 0 ? nn * d2p : 1)));
+        }
+        if (src->P) {
+            ADS_CUDA(cudaMalloc(&x->P, sizeof(double) * D * static_cast<size_t>(D)));
+            ADS_CUDA(cudaMemcpyAsync(x->P, src->P, sizeof(double) * D * static_cast<size_t>(D),
+                                     cudaMemcpyDeviceToDevice, st));
+        }
+        // owned lists are contiguous row ranges in every flat array: one copy per run of
+        // consecutive owned lists
+        for (int c = 0; c < k;) {
+            if (!keep[c]) {
+                ++c;
+                continue;
+            }
+            int e = c;
+            while (e < k && keep[e]) ++e;
+            const int64_t so = off[c], cnt = off[e] - off[c], dofs = noff[c];
+            if (cnt > 0) {
+                auto cp = [&](void* dst, const void* srcp, size_t w) {
+                    ADS_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + dofs * w,
+                                             static_cast<const char*>(srcp) + so * w, cnt * w,
+                                             cudaMemcpyDeviceToDevice, st));
+                };
+                cp(x->ids, src->ids, sizeof(int32_t));
+                cp(x->a1_t, src->a1_t, sizeof(float) * d1p);
+                if (d2p) cp(x->a2_t, src->a2_t, sizeof(float) * d2p);
+                if (x->has_raw) {
+                    cp(x->a1_raw, src->a1_raw, sizeof(float) * d1p);
+                    if (d2p) cp(x->a2_raw, src->a2_raw, sizeof(float) * d2p);
+                }
+            }
+            c = e;
+        }
+        ADS_CUDA(cudaStreamSynchronize(st));
+        *out = x.release();
+    });
+}
+
+int ads_merge_topk_device(ads_ctx* ctx, const double* ddists, const int32_t* dids, int32_t G,
+                          int32_t nq, int32_t K, int32_t* dout_ids, double* dout_dists,
+                          int32_t* dout_counts) {
+    return guard([&] {
+        require(G >= 1 && K >= 1 && nq >= 0, "merge_topk: bad shape");
+        ctx->use();
+        launch_merge_topk(ddists, dids, G, nq, K, dout_ids, dout_dists, dout_counts, ctx->stream);
+    });
+}
+
+int ads_merge_topk(ads_ctx* ctx, const double* dists, const int32_t* ids, int32_t G, int32_t nq,
+                   int32_t K, int32_t* out_ids, double* out_dists, int32_t* out_counts) {
+    return guard([&] {
+        require(G >= 1 && K >= 1 && nq >= 0, "merge_topk: bad shape");
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        const size_t in = static_cast<size_t>(G) * nq * K, o = static_cast<size_t>(nq) * K;
+        double* dd = dev_upload(dists, in, st);
+        int32_t* di = dev_upload(ids, in, st);
+        int32_t *oi = nullptr, *oc = nullptr;
+        double* od = nullptr;
+        ADS_CUDA(cudaMalloc(&oi, sizeof(int32_t) * (o + 1)));
+        ADS_CUDA(cudaMalloc(&od, sizeof(double) * (o + 1)));
+        ADS_CUDA(cudaMalloc(&oc, sizeof(int32_t) * (nq + 1)));
+        launch_merge_topk(dd, di, G, nq, K, oi, od, oc, st);
+        ADS_CUDA(cudaMemcpyAsync(out_ids, oi, sizeof(int32_t) * o, cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaMemcpyAsync(out_dists, od, sizeof(double) * o, cudaMemcpyDeviceToHost, st));
+        if (out_counts) ADS_CUDA(cudaMemcpyAsync(out_counts, oc, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        for (void* p : {static_cast<void*>(dd), static_cast<void*>(di), static_cast<void*>(oi),
+                        static_cast<void*>(od), static_cast<void*>(oc)})
+            cudaFree(p);
     });
 }
 

@@ -127,6 +127,10 @@ void build_lists(const int32_t* dAssign, int64_t n, int k, int64_t* dListOff, in
 void gather_split(const float* src, const int32_t* dIds, int64_t n, int D, int d1, float* a1,
                   float* a2, cudaStream_t st);
 
+// Per query, K smallest (dist, id) pairs among G lists of K ([G][nq][K]).
+void launch_merge_topk(const double* dists, const int32_t* ids, int G, int nq, int K,
+                       int32_t* out_ids, double* out_dists, int32_t* out_cnt, cudaStream_t st);
+
 int num_sms();
 
 }  // namespace ads

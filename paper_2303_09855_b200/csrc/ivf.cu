@@ -483,4 +483,79 @@ void launch_ivf_search(const SearchLaunch& a_in, cudaStream_t st) {
     ADS_LAUNCH_CHECK();
 }
 
+namespace {
+// One CTA per query: load the G*K (dist, id) entries, bitonic-sort by
+// (dist, id) with invalid entries (NaN dist or id < 0) as +inf, keep K.
+__global__ void __launch_bounds__(256) merge_topk_kernel(const double* __restrict__ dists,
+                                                         const int32_t* __restrict__ ids, int G,
+                                                         int nq, int K, int P2,
+                                                         int32_t* __restrict__ out_ids,
+                                                         double* __restrict__ out_dists,
+                                                         int32_t* __restrict__ out_cnt) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double* kd = reinterpret_cast<double*>(sm);
+    int32_t* ki = reinterpret_cast<int32_t*>(kd + P2);
+    __shared__ int s_cnt;
+    const int q = blockIdx.x, tid = threadIdx.x;
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    for (int e = tid; e < P2; e += blockDim.x) {
+        double d = kInf;
+        int32_t id = 0x7fffffff;
+        if (e < G * K) {
+            const int g = e / K, j = e % K;
+            const int64_t o = (static_cast<int64_t>(g) * nq + q) * K + j;
+            const double dv = dists[o];
+            const int32_t iv = ids[o];
+            if (iv >= 0 && dv == dv) {
+                d = dv;
+                id = iv;
+                atomicAdd(&s_cnt, 1);
+            }
+        }
+        kd[e] = d;
+        ki[e] = id;
+    }
+    __syncthreads();
+    for (int size = 2; size <= P2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < P2 / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const double da = kd[lo], db = kd[hi];
+                const int32_t ia = ki[lo], ib = ki[hi];
+                const bool a_gt_b = da > db || (da == db && ia > ib);
+                if (a_gt_b == up) {
+                    kd[lo] = db;
+                    kd[hi] = da;
+                    ki[lo] = ib;
+                    ki[hi] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const int cnt = s_cnt < K ? s_cnt : K;
+    for (int j = tid; j < K; j += blockDim.x) {
+        out_ids[static_cast<int64_t>(q) * K + j] = j < cnt ? ki[j] : -1;
+        out_dists[static_cast<int64_t>(q) * K + j] = j < cnt ? kd[j] : __longlong_as_double(0x7ff8000000000000ll);
+    }
+    if (tid == 0 && out_cnt) out_cnt[q] = cnt;
+}
+}  // namespace
+
+void launch_merge_topk(const double* dists, const int32_t* ids, int G, int nq, int K,
+                       int32_t* out_ids, double* out_dists, int32_t* out_cnt, cudaStream_t st) {
+    if (nq <= 0) return;
+    int P2 = 2;
+    while (P2 < G * K) P2 <<= 1;
+    const size_t smem = static_cast<size_t>(P2) * (sizeof(double) + sizeof(int32_t));
+    if (smem > 200 * 1024) throw std::invalid_argument("merge_topk: G*K too large");
+    ADS_CUDA(cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    merge_topk_kernel<<<nq, 256, smem, st>>>(dists, ids, G, nq, K, P2, out_ids, out_dists, out_cnt);
+    ADS_LAUNCH_CHECK();
+}
+
 }  // namespace ads
