@@ -252,20 +252,20 @@ def run_search(args, D: Dist):
                                         C.c_void_p(d_dims.ptr), C.c_void_p(d_cand.ptr)))
 
     if args.tune and D.rank == 0:
-        for st_, w_, g_ in ((128, 4, 1), (256, 2, 1), (256, 4, 1), (256, 8, 1), (512, 4, 1),
-                            (1024, 4, 1)):
+        for st_, w_, g_, sch, b0 in ((256, 4, 64, 0, 0), (8, 8, 64, 1, 1), (16, 8, 64, 1, 1),
+                                     (16, 16, 64, 1, 1), (32, 16, 64, 1, 1), (16, 8, 128, 1, 1),
+                                     (16, 16, 128, 1, 1)):
             if True:
-                o2 = ads.search_opts(first=0, step=st_, warps_per_cta=w_, queries_per_cta=g_,
+                o2 = ads.search_opts(first=b0, step=st_, warps_per_cta=w_, tile=g_, scheduler=sch,
                                      time_stages=True)
                 ts, dm = [], 0
                 for rep in range(4):
                     ctx.flush_l2()
-                    ctx.timer_start()
                     r_ = ads.ivf_query_batch(idx, None, q, K, nprobe, mode, opts=o2)
-                    ts.append(ctx.timer_stop())
+                    ts.append(float(idx.last_timings()[3]))
                     dm = float(r_.dims.mean())
-                    scan = float(idx.last_timings()[3])
-                log(f"tune step={st_} warps={w_} slots={g_}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
+                scan = float(np.min(ts))
+                log(f"tune sched={sch} first={b0} step={st_} warps={w_} tile={g_}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
                     f"recall {ads.recall_batch(r_.ids, gt, K):.5f}")
     for _ in range(args.warmup):
         ctx.flush_l2()

@@ -198,17 +198,23 @@ int ads_ivf_meta(ads_ivf *idx, int64_t *meta);
 int ads_ivf_export(ads_ivf *idx, float *centroids_t, float *centroids_raw, int64_t *list_off,
                    int32_t *ids_flat, float *a1_t, float *a2_t, float *a1_raw, float *a2_raw);
 
-/* Threshold refresh schedule and launch knobs.  The running K-th distance r
- * is re-read before candidate i of a query's probe-ordered stream when i = 0,
- * first, first+step, ...; first = step = 1 is the reference's per-candidate
- * refresh (ivf.cpp:331, 391), larger values batch it. */
+/* Threshold refresh schedule and launch knobs.
+ * scheduler 0 (query-major, one CTA per query): the running K-th distance r is
+ *   re-read before candidate i of a query's probe-ordered stream when i = 0,
+ *   first, first+step, ...; first = step = 1 is the reference's per-candidate
+ *   refresh (ivf.cpp:331, 391), larger values batch it.
+ * scheduler 1 (list-major waves): r is re-read at probe-rank boundaries
+ *   0, first, first+step, ... (first/step count probed LISTS; defaults 1 and
+ *   step as given); each list is read once per wave for all its queries. */
 typedef struct {
-    int64_t first;         /* default K */
-    int64_t step;          /* default 256 */
+    int64_t first;         /* default K (scheduler 0) / 1 list (scheduler 1) */
+    int64_t step;          /* default 256 candidates (scheduler 0) */
     int32_t warps_per_cta; /* default 8 */
     int32_t queries_per_cta; /* query slots served concurrently by one CTA, default 4 */
     int32_t ctas_per_sm;   /* 0 = occupancy maximum */
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */
+    int32_t scheduler;     /* 0 query-major (default), 1 list-major waves (16-byte-aligned layouts) */
+    int32_t tile;          /* list-major: candidates staged per shared-memory tile (default 64) */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 

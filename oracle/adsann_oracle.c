@@ -589,9 +589,33 @@ static void heap_offer(heap_t *h, double dist, int32_t id) {
     h->cnt++;
 }
 
+/* Shared body.  Refresh before candidate i when i == 0, or (waves == NULL)
+ * i >= first && (i - first) % step == 0, or (waves != NULL) i is the stream
+ * position of the first candidate of probe rank waves[j] (j < nwaves). */
+static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                          int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
+                          int64_t step, const int32_t *waves, int32_t nwaves, int32_t *ids,
+                          double *dists, int32_t *count, uint64_t *stats);
+
 int orc_ivf_query(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                   int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                   int64_t step, int32_t *ids, double *dists, int32_t *count, uint64_t *stats) {
+    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, NULL, 0,
+                          ids, dists, count, stats);
+}
+
+int orc_ivf_query_waves(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                        int32_t nprobe, int mode, double eps0, int32_t delta_d,
+                        const int32_t *wave_ranks, int32_t nwaves, int32_t *ids, double *dists,
+                        int32_t *count, uint64_t *stats) {
+    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, 1, 1, wave_ranks,
+                          nwaves, ids, dists, count, stats);
+}
+
+static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                          int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
+                          int64_t step, const int32_t *waves, int32_t nwaves, int32_t *ids,
+                          double *dists, int32_t *count, uint64_t *stats) {
     /* ivf.cpp:299-307 */
     if (K < 1) return fail(1, "ivf_query: K must be >= 1");
     if (nprobe < 1 || nprobe > idx->k_clusters)
@@ -644,11 +668,23 @@ int orc_ivf_query(const orc_ivf *idx, const float *q_t, const float *q_raw, int3
         dims += (uint64_t)total * (uint64_t)d1;
     }
 
+    /* refresh marks (stream positions) for the wave schedule */
+    char *mark = NULL;
+    if (waves) {
+        mark = calloc((size_t)(total + 1), 1);
+        int64_t pos = 0;
+        int32_t wj = 0;
+        for (int32_t pi = 0; pi < nprobe; ++pi) {
+            while (wj < nwaves && waves[wj] < pi) ++wj;
+            if (wj < nwaves && waves[wj] == pi) mark[pos] = 1;
+            pos += idx->list_off[probes[pi] + 1] - idx->list_off[probes[pi]];
+        }
+    }
     int64_t i = 0;
     for (int32_t pi = 0; pi < nprobe; ++pi) {
         const int32_t c = probes[pi];
         for (int64_t p = idx->list_off[c]; p < idx->list_off[c + 1]; ++p, ++i) {
-            if (i == 0 || (i >= first && (i - first) % step == 0)) {
+            if (i == 0 || (waves ? mark[i] : (i >= first && (i - first) % step == 0))) {
                 for (int64_t j = 0; j < npend; ++j) heap_offer(&heap, pending[j].dist, pending[j].id);
                 npend = 0;
                 r = heap_threshold(&heap); /* ivf.cpp:331, 391 */
@@ -691,5 +727,6 @@ int orc_ivf_query(const orc_ivf *idx, const float *q_t, const float *q_raw, int3
     free(heap.a);
     free(pending);
     free(prefix);
+    free(mark);
     return 0;
 }

@@ -108,6 +108,14 @@ int orc_ivf_query(const orc_ivf *idx, const float *q_t, const float *q_raw, int3
                   int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                   int64_t step, int32_t *ids, double *dists, int32_t *count, uint64_t *stats);
 
+/* Same, with the threshold refreshed at probe-rank wave boundaries: before the
+ * first candidate of probe rank wave_ranks[j] (ascending, wave_ranks[0] = 0)
+ * — the GPU's list-major wave schedule. */
+int orc_ivf_query_waves(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                        int32_t nprobe, int mode, double eps0, int32_t delta_d,
+                        const int32_t *wave_ranks, int32_t nwaves, int32_t *ids, double *dists,
+                        int32_t *count, uint64_t *stats);
+
 /* probe_order, ivf.cpp:283-292 */
 int orc_probe_order(const float *centroids, int32_t L, int32_t d, const float *q,
                     int32_t nprobe, int32_t *order);

@@ -194,6 +194,9 @@ class Oracle(_Common):
                                    C.c_int32, C.c_int64, C.c_int64, _i32p, _f64p,
                                    C.POINTER(C.c_int32), _u64p])
         self._fn("orc_probe_order", [_f32p, C.c_int32, C.c_int32, _f32p, C.c_int32, _i32p])
+        self._fn("orc_ivf_query_waves", [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int, C.c_double,
+                                         C.c_int32, _i32p, C.c_int32, _i32p, _f64p,
+                                         C.POINTER(C.c_int32), _u64p])
 
     def ivf_layout(self, raw, t, P, centroids_t, assignment, k, d1=32, split=True):
         """ivf.cpp:211-256 layout from a clustering → dict of host arrays."""
@@ -220,8 +223,10 @@ class Oracle(_Common):
                                      g("centroids_raw")))
         return out
 
-    def ivf_query(self, index, q_t, q_raw, K, nprobe, mode, eps0=2.1, delta_d=32, first=1, step=1):
-        """Returns (ids, dists, stats[dims, dco, cand]).  first=step=1 == reference."""
+    def ivf_query(self, index, q_t, q_raw, K, nprobe, mode, eps0=2.1, delta_d=32, first=1, step=1,
+                  waves=None):
+        """Returns (ids, dists, stats[dims, dco, cand]).  first=step=1 == reference;
+        waves = ascending probe ranks where the threshold is refreshed (list-major schedule)."""
 
         class _Ivf(C.Structure):
             _fields_ = [("n", C.c_int32), ("d", C.c_int32), ("k", C.c_int32), ("d1", C.c_int32),
@@ -240,8 +245,14 @@ class Oracle(_Common):
         cnt = C.c_int32()
         stats = np.zeros(3, np.uint64)
         m = MODES[mode] if isinstance(mode, str) else mode
-        self._check(self._ivf_query(C.addressof(s), _nullable(qt), _nullable(qr), K, nprobe, m,
-                                    eps0, delta_d, first, step, ids, dists, C.byref(cnt), stats))
+        if waves is not None:
+            w = np.ascontiguousarray(waves, np.int32)
+            self._check(self._ivf_query_waves(C.addressof(s), _nullable(qt), _nullable(qr), K, nprobe,
+                                              m, eps0, delta_d, w, len(w), ids, dists, C.byref(cnt),
+                                              stats))
+        else:
+            self._check(self._ivf_query(C.addressof(s), _nullable(qt), _nullable(qr), K, nprobe, m,
+                                        eps0, delta_d, first, step, ids, dists, C.byref(cnt), stats))
         return ids[:cnt.value].copy(), dists[:cnt.value].copy(), stats
 
     def probe_order(self, centroids, q, nprobe):

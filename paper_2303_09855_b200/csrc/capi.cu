@@ -64,26 +64,6 @@ void require(bool ok, const char* msg) {
     if (!ok) throw std::invalid_argument(msg);
 }
 
-// Device buffer that only grows.
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    template <typename T>
-    T* get(size_t count) {
-        const size_t need = sizeof(T) * (count > 0 ? count : 1);
-        if (need > bytes) {
-            if (p) ADS_CUDA(cudaFree(p));
-            p = nullptr;
-            ADS_CUDA(cudaMalloc(&p, need));
-            bytes = need;
-        }
-        return static_cast<T*>(p);
-    }
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-};
-
 template <typename T>
 T* dev_upload(const T* h, size_t count, cudaStream_t st) {
     T* d = nullptr;
@@ -133,6 +113,7 @@ struct ads_ivf {
     double* P = nullptr;
     std::map<PlanKey, std::unique_ptr<DevSegPlan>> plans;
     DevBuf dist, probes, qrot, qin_t, qin_raw, o_ids, o_dists, o_cnt, o_dims, o_cand;
+    ListMajorScratch lm;
     cudaEvent_t ev[5] = {};
     float last_ms[4] = {0, 0, 0, 0};
     bool timed = false;
@@ -820,6 +801,8 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->queries_per_cta = 4;
     o->ctas_per_sm = 0;
     o->time_stages = 0;
+    o->scheduler = 0;
+    o->tile = 64;
 }
 
 namespace {
@@ -933,7 +916,38 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.out_dims = reinterpret_cast<unsigned long long*>(ddims);
     a.out_cand = reinterpret_cast<unsigned long long*>(dcand);
     a.counter = x->ctx->counter;
-    launch_ivf_search(a, st);
+    if (o.scheduler == 1 && a.vec == 4) {
+        ListMajorLaunch m{};
+        m.a1 = a.a1;
+        m.a2 = a.a2;
+        m.d1 = a.d1;
+        m.D = D;
+        m.ids = a.ids;
+        m.list_off = a.list_off;
+        m.L = x->k;
+        m.Q = Qs;
+        m.nq = nq;
+        m.probes = probes;
+        m.nprobe = nprobe;
+        m.K = K;
+        m.final_fd = a.final_fd;
+        m.segs = a.segs;
+        m.tfac = a.tfac;
+        m.nseg = a.nseg;
+        m.ntest = a.ntest;
+        m.first_lists = static_cast<int>(opts && opts->first > 0 ? opts->first : 1);
+        m.step_lists = static_cast<int>(o.step);
+        m.tile = o.tile;
+        m.warps = o.warps_per_cta;
+        m.out_ids = dids;
+        m.out_dists = ddists;
+        m.out_cnt = dcnt;
+        m.out_dims = reinterpret_cast<unsigned long long*>(ddims);
+        m.out_cand = reinterpret_cast<unsigned long long*>(dcand);
+        launch_listmajor_search(m, x->lm, st);
+    } else {
+        launch_ivf_search(a, st);
+    }
     if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[4], st));
 }
 

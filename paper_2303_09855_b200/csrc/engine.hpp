@@ -99,6 +99,59 @@ struct SearchLaunch {
 };
 void launch_ivf_search(const SearchLaunch& a, cudaStream_t st);
 
+// Device buffer that only grows (scratch owned by index handles).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <typename T>
+    T* get(size_t count) {
+        const size_t need = sizeof(T) * (count > 0 ? count : 1);
+        if (need > bytes) {
+            if (p) ADS_CUDA(cudaFree(p));
+            p = nullptr;
+            ADS_CUDA(cudaMalloc(&p, need));
+            bytes = need;
+        }
+        return static_cast<T*>(p);
+    }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// List-major wave search (listmajor.cu).
+struct ListMajorLaunch {
+    const float* a1;
+    const float* a2;
+    int d1, D;
+    const int32_t* ids;
+    const int64_t* list_off;
+    int L;
+    const float* Q;
+    int nq;
+    const int32_t* probes;
+    int nprobe, K, final_fd;
+    const Seg* segs;
+    const double* tfac;
+    int nseg, ntest;
+    int first_lists, step_lists;  // wave sizes in probed lists
+    int tile, warps;
+    int32_t* out_ids;
+    double* out_dists;
+    int32_t* out_cnt;
+    unsigned long long* out_dims;
+    unsigned long long* out_cand;
+};
+struct ListMajorScratch {
+    DevBuf pre, heap_d, heap_i, heap_c, rr, thr, dims, wcnt, wbase, lcnt, loff, fill, pairs, counter,
+        flag, pdist, pid, tmp;
+};
+void launch_listmajor_search(const ListMajorLaunch& a, ListMajorScratch& s, cudaStream_t st);
+size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int warps);
+
 // Exact fp64 centroid distances (nq x L, l2_sq order) and top-nprobe by (d2, id).
 void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,
                         cudaStream_t st);
