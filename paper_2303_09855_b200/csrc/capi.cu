@@ -81,6 +81,10 @@ struct ads_ctx {
     void* flush = nullptr;
     size_t flush_bytes = 0;
     std::mutex mu;
+    // single-DCO scratch (ads_dco): one pinned staging block + one device block
+    void* h_stage = nullptr;
+    DevBuf d_stage;
+    std::map<std::tuple<int, int, double, int>, std::unique_ptr<DevSegPlan>> dco_plans;
     void use() const { ADS_CUDA(cudaSetDevice(device)); }
 };
 
@@ -209,6 +213,8 @@ int ads_ctx_destroy(ads_ctx* ctx) {
         ctx->use();
         cudaStreamSynchronize(ctx->stream);
         if (ctx->flush) cudaFree(ctx->flush);
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+        for (auto& kv : ctx->dco_plans) kv.second->release();
         cudaFree(ctx->counter);
         cudaEventDestroy(ctx->t0);
         cudaEventDestroy(ctx->t1);
@@ -533,28 +539,73 @@ int ads_dco(ads_ctx* ctx, int32_t kind, const float* o, int32_t n_o, const float
         require(kind >= 0 && kind <= 2, "dco: unknown kind");
         if (kind == ADS_DCO_PD) require(delta_d >= 1 && delta_d <= n_o, "pd_scan: delta_d must be in [1, D]");
         if (kind == ADS_DCO_AD) (void)ad_factor(eps0, delta_d, n_o);
-        ads_dco_batch b{};
-        const int64_t off[2] = {0, 1};
-        const int64_t rows[1] = {0};
-        b.X = o;
-        b.n_rows = 1;
-        b.dim = n_o;
-        b.Q = q;
-        b.nq = 1;
-        b.cand_off = off;
-        b.cand_rows = rows;
-        b.r = &r;
-        b.kind = kind;
-        b.epsilon0 = eps0;
-        b.delta_d = kind == ADS_DCO_FD ? n_o : delta_d;
-        uint8_t pos = 0;
+        ctx->use();
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        cudaStream_t st = ctx->stream;
+        const int D = n_o;
+        const int dd = kind == ADS_DCO_FD ? D : delta_d;
+        const auto key = std::make_tuple(kind, D, kind == ADS_DCO_AD ? eps0 : 0.0, kind == ADS_DCO_FD ? 0 : dd);
+        auto it = ctx->dco_plans.find(key);
+        if (it == ctx->dco_plans.end()) {
+            auto dp = std::make_unique<DevSegPlan>();
+            dp->upload(dco_plan(kind, D, eps0, dd), st);
+            it = ctx->dco_plans.emplace(key, std::move(dp)).first;
+        }
+        const DevSegPlan& dp = *it->second;
+        // staging layout (bytes): X[D] f32 | Q[D] f32 | r f64 | off[2] i64 | row i64 | tile q,lo,hi i64
+        //                         | pos u8 (pad 8) | dims i32 (pad 8) | obs f64 | dpq u64
+        const size_t vbytes = ((sizeof(float) * D + 15) / 16) * 16;
+        const size_t in_bytes = 2 * vbytes + 8 * 7;
+        const size_t out_bytes = 8 * 4;
+        if (!ctx->h_stage) ADS_CUDA(cudaMallocHost(&ctx->h_stage, 1 << 20));
+        require(in_bytes + out_bytes <= (1 << 20), "dco: vector too long for the single-DCO path");
+        unsigned char* h = static_cast<unsigned char*>(ctx->h_stage);
+        unsigned char* d = ctx->d_stage.get<unsigned char>(in_bytes + out_bytes);
+        std::memcpy(h, o, sizeof(float) * D);
+        std::memcpy(h + vbytes, q, sizeof(float) * D);
+        int64_t* hi = reinterpret_cast<int64_t*>(h + 2 * vbytes + 8);
+        std::memcpy(h + 2 * vbytes, &r, 8);
+        hi[0] = 0;  // cand_off
+        hi[1] = 1;
+        hi[2] = 0;  // cand_rows[0]
+        hi[3] = 0;  // tile q
+        hi[4] = 0;  // tile lo
+        hi[5] = 1;  // tile hi
+        ADS_CUDA(cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st));
+        int64_t* di = reinterpret_cast<int64_t*>(d + 2 * vbytes + 8);
+        unsigned char* dout = d + in_bytes;
+        DcoLaunch a{};
+        a.X = reinterpret_cast<const float*>(d);
+        a.n_rows = 1;
+        a.D = D;
+        a.Q = reinterpret_cast<const float*>(d + vbytes);
+        a.nq = 1;
+        a.cand_off = di;
+        a.cand_rows = di + 2;
+        a.r = reinterpret_cast<const double*>(d + 2 * vbytes);
+        a.tile_q = di + 3;
+        a.tile_lo = di + 4;
+        a.tile_hi = di + 5;
+        a.ntiles = 1;
+        a.tile = 1;
+        a.kind = kind;
+        a.segs = dp.segs;
+        a.tfac = dp.tfac;
+        a.nseg = dp.nseg;
+        a.ntest = dp.ntest;
+        a.vec = dp.vec;
+        a.positive = dout;
+        a.dims = reinterpret_cast<int32_t*>(dout + 8);
+        a.observed = reinterpret_cast<double*>(dout + 16);
+        a.counter = ctx->counter;
+        launch_dco_fixed(a, st);
+        ADS_CUDA(cudaMemcpyAsync(h + in_bytes, dout, out_bytes, cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        const uint8_t pos = h[in_bytes];
         int32_t dims = 0;
         double obs = 0.0;
-        b.positive = &pos;
-        b.dims = &dims;
-        b.observed = &obs;
-        const int rc = ads_dco_fixed(ctx, &b);
-        if (rc != ADS_OK) throw std::runtime_error(g_err);
+        std::memcpy(&dims, h + in_bytes + 8, 4);
+        std::memcpy(&obs, h + in_bytes + 16, 8);
         *positive = pos;
         *observed = obs;
         *dims_used = dims;

@@ -169,7 +169,7 @@ __device__ __forceinline__ double seg_acc(const float* row, const double* qq, in
     return s;
 }
 
-__global__ void __launch_bounds__(256) scan_lists_kernel(ScanLists a) {
+__global__ void __launch_bounds__(512) scan_lists_kernel(ScanLists a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_list;
     const int nwarps = blockDim.x >> 5;
