@@ -990,6 +990,7 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
         m.step_lists = static_cast<int>(o.step);
         m.tile = o.tile;
         m.warps = o.warps_per_cta;
+        m.qgroup = o.queries_per_cta;
         m.out_ids = dids;
         m.out_dists = ddists;
         m.out_cnt = dcnt;

@@ -138,7 +138,7 @@ struct ListMajorLaunch {
     const double* tfac;
     int nseg, ntest;
     int first_lists, step_lists;  // wave sizes in probed lists
-    int tile, warps;
+    int tile, warps, qgroup;
     int32_t* out_ids;
     double* out_dists;
     int32_t* out_cnt;
@@ -150,7 +150,7 @@ struct ListMajorScratch {
         flag, pdist, pid, tmp;
 };
 void launch_listmajor_search(const ListMajorLaunch& a, ListMajorScratch& s, cudaStream_t st);
-size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int warps);
+size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int qgroup);
 
 // Exact fp64 centroid distances (nq x L, l2_sq order) and top-nprobe by (d2, id).
 void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,

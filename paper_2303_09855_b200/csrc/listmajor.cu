@@ -126,7 +126,9 @@ struct ScanLists {
     int32_t* pid;
     unsigned long long* dims;
     int tile;              // candidates per shared-memory tile
+    int qgroup;            // queries per group (shared-memory staging)
     unsigned* list_counter;
+    long long nslots, nq;  // bounds (debug checks)
 };
 
 // Shared-memory row pitch (floats) for rows of `w` floats: padded so that
@@ -169,38 +171,36 @@ __device__ __forceinline__ double seg_acc(const float* row, const double* qq, in
     return s;
 }
 
+// One CTA per list (persistent over lists).  For each tile of the list and
+// each group of up to QG queries probing it, all (candidate, query) pairs go
+// through the segments level by level: level 0 enumerates every pair, later
+// levels take the survivors from a CTA-wide queue, so every lane always works
+// on a live pair and no pair waits for another.
+template <int T>
 __global__ void __launch_bounds__(512) scan_lists_kernel(ScanLists a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_list;
-    const int nwarps = blockDim.x >> 5;
+    __shared__ int s_list, s_nout[3];
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
+    (void)warp;
     const int d2 = a.D - a.d1;
-    const int T = a.tile;
+    const int QG = a.qgroup;
     const int nt = a.ntest > 0 ? a.ntest : 1;
-    // layout: tileA1 [T*p1] | tileA2 [T*p2] | per warp: qseg[nseg*34] thr[nt] r,rsq | queues
     const int p1 = lm_pitch(a.d1), p2 = d2 > 0 ? lm_pitch(d2) : 0;
+    // layout: tA1 [T*p1] | tA2 [T*p2] | qstage [QG*nseg*34] | thr [QG*nt] | rr [QG*2]
+    //         | qs_s [2][T*QG] f64 | qs_e [2][T*QG] i32 | gq, gbase, gdims [QG] | segs
     float* tA1 = reinterpret_cast<float*>(smem_raw);
-    float* tA2 = tA1 + static_cast<size_t>(T) * p1;
-    unsigned char* wbase_ptr = reinterpret_cast<unsigned char*>(tA2 + static_cast<size_t>(T) * p2);
-    const size_t per_warp = lm_per_warp(a.nseg, nt, T);
-    unsigned char* mine = wbase_ptr + per_warp * warp;
-    double* qseg = reinterpret_cast<double*>(mine);
-    double* thr = qseg + a.nseg * kQPitch;
-    double* rr = thr + nt;
-    double* qs0 = rr + 2;
-    double* qs1 = qs0 + T;
-    int* qc0 = reinterpret_cast<int*>(qs1 + T);
-    int* qc1 = qc0 + T;
-    Seg* segs = reinterpret_cast<Seg*>(wbase_ptr + per_warp * nwarps);
+    float* tA2 = tA1 + T * p1;
+    double* qstage = reinterpret_cast<double*>(tA2 + T * p2);
+    double* thr = qstage + QG * a.nseg * kQPitch;
+    double* rr = thr + QG * nt;
+    double* qs_s = rr + 2 * QG;
+    int* qs_e = reinterpret_cast<int*>(qs_s + 2 * T * QG);
+    int* gq = qs_e + 2 * T * QG;
+    int* gbase = gq + QG;
+    unsigned* gdims = reinterpret_cast<unsigned*>(gbase + QG);
+    Seg* segs = reinterpret_cast<Seg*>(gdims + QG);
     for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
-#ifdef ADS_DEBUG
-    if (threadIdx.x == 0 && blockIdx.x < 2)
-        printf("START block %d base%%16=%d tA1%%16=%d tA2%%16=%d p1=%d p2=%d T=%d d1=%d D=%d per_warp=%d\n",
-               blockIdx.x, (int)(reinterpret_cast<uintptr_t>(smem_raw) & 15),
-               (int)(reinterpret_cast<uintptr_t>(tA1) & 15), (int)(reinterpret_cast<uintptr_t>(tA2) & 15),
-               p1, p2, T, a.d1, a.D, (int)per_warp);
-#endif
 
     for (;;) {
         __syncthreads();
@@ -219,19 +219,11 @@ __global__ void __launch_bounds__(512) scan_lists_kernel(ScanLists a) {
         const int pb = a.list_pair_off[L], pe = a.list_pair_off[L + 1];
         for (int t0 = 0; t0 < nrows; t0 += T) {
             const int rows = nrows - t0 < T ? nrows - t0 : T;
-            // stage the tile (rows are contiguous in A1 and in A2)
-            {
+            {  // stage the tile: A1 and A2 rows of the list are contiguous
                 const float4* s1 = reinterpret_cast<const float4*>(a.a1 + (row0 + t0) * a.d1);
                 const int c1 = a.d1 / 4, n1 = rows * c1;
                 for (int i = threadIdx.x; i < n1; i += blockDim.x) {
                     const int r = i / c1, c = i - r * c1;
-#ifdef ADS_DEBUG
-                    if ((reinterpret_cast<uintptr_t>(tA1 + r * p1 + c * 4) & 15) != 0 && i < 64)
-                        printf("tA1 dst: base%%16=%d p1=%d c1=%d r=%d c=%d i=%d T=%d d1=%d\n",
-                               (int)(reinterpret_cast<uintptr_t>(smem_raw) & 15), p1, c1, r, c, i, T, a.d1);
-#endif
-                    LM_CHECK((reinterpret_cast<uintptr_t>(tA1 + r * p1 + c * 4) & 15) == 0, "tA1 dst", r);
-                    LM_CHECK((reinterpret_cast<uintptr_t>(s1 + i) & 15) == 0, "tA1 src", row0);
                     cp_async16(tA1 + r * p1 + c * 4, s1 + i);
                 }
                 if (d2 > 0) {
@@ -239,68 +231,82 @@ __global__ void __launch_bounds__(512) scan_lists_kernel(ScanLists a) {
                     const int c2 = d2 / 4, n2 = rows * c2;
                     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
                         const int r = i / c2, c = i - r * c2;
-                        LM_CHECK((reinterpret_cast<uintptr_t>(tA2 + r * p2 + c * 4) & 15) == 0, "tA2 dst", r);
-                        LM_CHECK((reinterpret_cast<uintptr_t>(s2 + i) & 15) == 0, "tA2 src", row0);
                         cp_async16(tA2 + r * p2 + c * 4, s2 + i);
                     }
                 }
-                cp_async_wait_all();
             }
-            __syncthreads();
-            for (int p = pb + warp; p < pe; p += nwarps) {
-                LM_CHECK(p >= 0 && p < 1 << 28, "pair idx", p);
-                const int2 pr = a.pairs[p];
-                LM_CHECK(pr.x >= 0 && pr.y >= 0 && pr.y < a.nprobe, "pair", pr.x);
-                const int q = pr.x, rank = pr.y;
-                const int32_t* pq = a.pre + static_cast<int64_t>(q) * (a.nprobe + 1);
-                // dense slot of candidate t0 of this list for query q
-                const int dbase = a.wbase[q] + (pq[rank] - pq[a.r0]) + t0;
-                LM_CHECK(dbase >= 0, "dbase", dbase);
-                const float* qv = a.Q + static_cast<int64_t>(q) * a.D;
-                for (int i = static_cast<int>(lane); i < a.nseg * 32; i += 32) {
-                    const Seg sg = segs[i >> 5];
-                    const int k = i & 31;
-                    if (k < sg.len) qseg[(i >> 5) * kQPitch + k] = static_cast<double>(qv[sg.col + k]);
-                }
-                for (int i = static_cast<int>(lane); i < a.ntest; i += 32)
-                    thr[i] = a.thr[static_cast<int64_t>(q) * a.ntest + i];
-                if (lane < 2) rr[lane] = a.rr[2 * q + lane];
-                __syncwarp();
-                const double r = rr[0], r_sq = rr[1];
-                unsigned long long my_dims = 0;
-                // level-synchronous passes: queue = candidates alive before segment `sg`
-                int nq_alive = rows;
-                double* sin = qs0;
-                int* cin = qc0;
-                double* sout = qs1;
-                int* cout = qc1;
-                for (int sg = 0; sg < a.nseg && nq_alive > 0; ++sg) {
+            for (int g0 = pb; g0 < pe; g0 += QG) {
+                const int ng = pe - g0 < QG ? pe - g0 : QG;
+                // stage the group's queries, thresholds and dense-slot bases
+                for (int i = threadIdx.x; i < ng * a.nseg * 32; i += blockDim.x) {
+                    const int g = i / (a.nseg * 32), rem = i - g * a.nseg * 32;
+                    const int sg = rem >> 5, k = rem & 31;
                     const Seg sgm = segs[sg];
-                    const double* qq = qseg + sg * kQPitch;
+                    if (k < sgm.len) {
+                        const int q = a.pairs[g0 + g].x;
+                        qstage[(g * a.nseg + sg) * kQPitch + k] =
+                            static_cast<double>(a.Q[static_cast<int64_t>(q) * a.D + sgm.col + k]);
+                    }
+                }
+                for (int i = threadIdx.x; i < ng * nt; i += blockDim.x) {
+                    const int g = i / nt, t = i - g * nt;
+                    if (t < a.ntest) thr[i] = a.thr[static_cast<int64_t>(a.pairs[g0 + g].x) * a.ntest + t];
+                }
+                if (threadIdx.x == 0) s_nout[0] = 0;
+                for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+                    const int2 pr = a.pairs[g0 + g];
+                    LM_CHECK(pr.x >= 0 && pr.x < a.nq && pr.y >= 0 && pr.y < a.nprobe, "pair", pr.x);
+                    const int32_t* pq = a.pre + static_cast<int64_t>(pr.x) * (a.nprobe + 1);
+                    gq[g] = pr.x;
+                    gbase[g] = a.wbase[pr.x] + (pq[pr.y] - pq[a.r0]) + t0;
+                    gdims[g] = 0;
+                    rr[2 * g] = a.rr[2 * pr.x];
+                    rr[2 * g + 1] = a.rr[2 * pr.x + 1];
+                }
+                cp_async_wait_all();
+                __syncthreads();
+                int n_in = ng * T;  // level 0: every (candidate, query) pair, entry = g*T + c
+                int cur = 0;
+                // Survivor counters rotate over three slots: level sg counts into
+                // slot sg%3 and clears slot (sg+1)%3, whose last reader (level
+                // sg-2's total) is separated from this write by the barrier that
+                // ended level sg-1.
+                for (int sg = 0; sg < a.nseg; ++sg) {
+                    if (threadIdx.x == 0) s_nout[(sg + 1) % 3] = 0;
+                    const Seg sgm = segs[sg];
                     const int nch = sgm.len >> 2;
                     const bool last = sg == a.nseg - 1;
-                    int nout = 0;
-                    for (int g0 = 0; g0 < nq_alive; g0 += 32) {
-                        const int k = g0 + static_cast<int>(lane);
-                        bool alive = false, keep = false;
-                        int c = 0;
+                    const double* qin_s = qs_s + cur * T * QG;
+                    const int* qin_e = qs_e + cur * T * QG;
+                    double* qout_s = qs_s + (cur ^ 1) * T * QG;
+                    int* qout_e = qs_e + (cur ^ 1) * T * QG;
+                    const int n_round = (n_in + 31) & ~31;
+                    for (int e = threadIdx.x; e < n_round; e += blockDim.x) {
+                        int entry = 0;
                         double s = 0.0;
-                        if (k < nq_alive) {
-                            alive = true;
-                            c = sg == 0 ? k : cin[k];
-                            s = sg == 0 ? 0.0 : sin[k];
+                        bool live = e < n_in;
+                        if (live) {
+                            entry = sg == 0 ? e : qin_e[e];
+                            s = sg == 0 ? 0.0 : qin_s[e];
+                            if (sg == 0 && (entry % T) >= rows) live = false;
+                        }
+                        const int g = entry / T, c = entry % T;
+                        bool keep = false;
+                        unsigned fin_dims = 0;
+                        if (live) {
                             const float* row = sgm.arr == 0 ? tA1 + c * p1 + sgm.col
                                                             : tA2 + c * p2 + (sgm.col - a.d1);
-                            s = seg_acc(row, qq, nch, s);
-                            if (sgm.test >= 0 && s > thr[sgm.test]) {  // reject (dco.hpp:141)
-                                my_dims += static_cast<unsigned long long>(sgm.col + sgm.len);
-                                const int slot = dbase + c;
+                            s = seg_acc(row, qstage + (g * a.nseg + sg) * kQPitch, nch, s);
+                            const int slot = gbase[g] + c;
+                            LM_CHECK(slot >= 0 && slot < a.nslots, "slot", slot);
+                            LM_CHECK(g < QG && c < T, "entry", entry);
+                            if (sgm.test >= 0 && s > thr[g * nt + sgm.test]) {  // reject (dco.hpp:141)
+                                fin_dims = static_cast<unsigned>(sgm.col + sgm.len);
                                 a.flag[slot] = 0;
                             } else if (last) {  // d == D
-                                my_dims += static_cast<unsigned long long>(a.D);
+                                fin_dims = static_cast<unsigned>(a.D);
                                 const double dist = __dsqrt_rn(s);
-                                const bool positive = a.final_fd ? dist <= r : s <= r_sq;
-                                const int slot = dbase + c;
+                                const bool positive = a.final_fd ? dist <= rr[2 * g] : s <= rr[2 * g + 1];
                                 a.flag[slot] = positive;
                                 if (positive) {
                                     a.pdist[slot] = dist;
@@ -310,28 +316,33 @@ __global__ void __launch_bounds__(512) scan_lists_kernel(ScanLists a) {
                                 keep = true;
                             }
                         }
-                        (void)alive;
-                        const unsigned km = __ballot_sync(kFull, keep);
-                        if (keep) {
-                            const int o = nout + __popc(km & ((1u << lane) - 1u));
-                            cout[o] = c;
-                            sout[o] = s;
+                        // dims: one shared atomic per distinct group among the warp's finishers
+                        const unsigned fm = __ballot_sync(kFull, fin_dims != 0);
+                        if (fin_dims) {
+                            const unsigned same = __match_any_sync(fm, g);
+                            const unsigned tot = __reduce_add_sync(same, fin_dims);
+                            if (static_cast<int>(lane) == __ffs(same) - 1) atomicAdd(&gdims[g], tot);
                         }
-                        nout += __popc(km);
+                        const unsigned km = __ballot_sync(kFull, keep);
+                        int base = 0;
+                        if (lane == 0 && km) base = atomicAdd(&s_nout[sg % 3], __popc(km));
+                        base = __shfl_sync(kFull, base, 0);
+                        if (keep) {
+                            const int o = base + __popc(km & ((1u << lane) - 1u));
+                            LM_CHECK(o < T * QG, "queue", o);
+                            qout_e[o] = entry;
+                            qout_s[o] = s;
+                        }
                     }
-                    __syncwarp();
-                    nq_alive = nout;
-                    double* ts = sin;
-                    sin = sout;
-                    sout = ts;
-                    int* tc = cin;
-                    cin = cout;
-                    cout = tc;
+                    __syncthreads();
+                    n_in = s_nout[sg % 3];
+                    cur ^= 1;
+                    if (n_in == 0) break;
                 }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) my_dims += __shfl_xor_sync(kFull, my_dims, o);
-                if (lane == 0 && my_dims) atomicAdd(a.dims + q, my_dims);
-                __syncwarp();
+                __syncthreads();
+                for (int g = threadIdx.x; g < ng; g += blockDim.x)
+                    if (gdims[g]) atomicAdd(a.dims + gq[g], static_cast<unsigned long long>(gdims[g]));
+                __syncthreads();
             }
             __syncthreads();
         }
@@ -473,11 +484,14 @@ inline unsigned nblk(int64_t n, int t) { return static_cast<unsigned>((n + t - 1
 
 }  // namespace
 
-size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int warps) {
+size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int qgroup) {
     const int nt = ntest > 0 ? ntest : 1;
     const int d2 = D - d1;
-    return sizeof(float) * static_cast<size_t>(tile) * (lm_pitch(d1) + (d2 > 0 ? lm_pitch(d2) : 0)) +
-           lm_per_warp(nseg, nt, tile) * warps + sizeof(Seg) * nseg;
+    size_t b = sizeof(float) * static_cast<size_t>(tile) * (lm_pitch(d1) + (d2 > 0 ? lm_pitch(d2) : 0));
+    b += sizeof(double) * (static_cast<size_t>(qgroup) * nseg * kQPitch + qgroup * nt + 2 * qgroup);
+    b += (sizeof(double) + sizeof(int)) * 2 * static_cast<size_t>(tile) * qgroup;
+    b += sizeof(int) * 3 * qgroup + sizeof(Seg) * nseg;
+    return b;
 }
 
 void launch_listmajor_search(const ListMajorLaunch& a, ListMajorScratch& s, cudaStream_t st) {
@@ -522,11 +536,17 @@ void launch_listmajor_search(const ListMajorLaunch& a, ListMajorScratch& s, cuda
     auto tmp = s.tmp.get<unsigned char>(scan_tmp > scan_tmp2 ? scan_tmp : scan_tmp2);
     const size_t tmp_bytes = scan_tmp > scan_tmp2 ? scan_tmp : scan_tmp2;
 
-    const size_t smem = listmajor_scan_smem(a.tile, a.d1, a.D, a.nseg, a.ntest, a.warps);
-    ADS_CUDA(cudaFuncSetAttribute(scan_lists_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    int qg = a.qgroup > 0 ? a.qgroup : 8;
+    size_t smem = listmajor_scan_smem(a.tile, a.d1, a.D, a.nseg, a.ntest, qg);
+    while (qg > 1 && smem > 110 * 1024) smem = listmajor_scan_smem(a.tile, a.d1, a.D, a.nseg, a.ntest, --qg);
+    auto kern = a.tile <= 16 ? scan_lists_kernel<16>
+              : a.tile <= 32 ? scan_lists_kernel<32>
+              : a.tile <= 64 ? scan_lists_kernel<64> : scan_lists_kernel<128>;
+    const int tile = a.tile <= 16 ? 16 : a.tile <= 32 ? 32 : a.tile <= 64 ? 64 : 128;
+    smem = listmajor_scan_smem(tile, a.d1, a.D, a.nseg, a.ntest, qg);
+    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int occ = 0;
-    ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_lists_kernel, a.warps * 32, smem));
+    ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, a.warps * 32, smem));
     if (occ < 1) throw std::invalid_argument("search: list tile exceeds shared memory");
     const int grid = num_sms() * occ;
     const int mwpb = 8;
@@ -572,10 +592,13 @@ void launch_listmajor_search(const ListMajorLaunch& a, ListMajorScratch& s, cuda
         sl.pdist = pdist;
         sl.pid = pid;
         sl.dims = dims;
-        sl.tile = a.tile;
+        sl.tile = tile;
+        sl.qgroup = qg;
+        sl.nslots = static_cast<long long>(maxtot) + 1;
+        sl.nq = nq;
         sl.list_counter = reinterpret_cast<unsigned*>(ctr + 1);
         ADS_CUDA(cudaMemsetAsync(ctr + 1, 0, sizeof(unsigned long long), st));
-        scan_lists_kernel<<<grid, a.warps * 32, smem, st>>>(sl);
+        kern<<<grid, a.warps * 32, smem, st>>>(sl);
         ADS_LAUNCH_CHECK();
         merge_wave_kernel<<<nblk(nq, mwpb), mwpb * 32, msmem, st>>>(nq, K, a.ntest, wbase, wcnt, flag,
                                                                       pdist, pid, heap_d, heap_i, heap_c,

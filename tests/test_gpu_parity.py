@@ -262,8 +262,8 @@ def _waves(nprobe, b0, B):
 
 @pytest.mark.parametrize("case", [(4000, 64, 16, 50, 32, 32, 10), (3000, 128, 32, 40, 32, 32, 20),
                                   (2000, 96, 8, 30, 32, 32, 7), (1500, 48, 8, 20, 16, 16, 5)])
-@pytest.mark.parametrize("b0,B", [(1, 1), (1, 4), (2, 3), (1, 100)])
-def test_ivf_listmajor_waves_bitexact(eng, orc, case, b0, B):
+@pytest.mark.parametrize("b0,B,qg", [(1, 1, 1), (1, 4, 8), (2, 3, 3), (1, 100, 16)])
+def test_ivf_listmajor_waves_bitexact(eng, orc, case, b0, B, qg):
     """scheduler 1 (lists read once per wave for all their queries) == the oracle
     with the threshold refreshed at the same probe-rank boundaries."""
     n, d, blobs, k, d1, dd, K = case
@@ -273,7 +273,8 @@ def test_ivf_listmajor_waves_bitexact(eng, orc, case, b0, B):
     cfg = eng.DcoConfig(2.1, dd)
     for mode in MODES:
         for nprobe in (1, 6, k):
-            o = eng.search_opts(first=b0, step=B, scheduler=1, warps_per_cta=4, tile=64)
+            o = eng.search_opts(first=b0, step=B, scheduler=1, warps_per_cta=4, tile=64,
+                                queries_per_cta=qg)
             res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg, opts=o)
             w = _waves(nprobe, b0, B)
             for qi in range(qt.shape[0]):
@@ -292,8 +293,8 @@ def test_ivf_listmajor_tiles_smaller_than_lists(eng, orc):
     lay = oracle_index(orc, raw, t, P, 8, 6, d1=32)
     assert np.diff(lay["list_off"]).max() > 64
     idx = gpu_index(eng, lay, P)
-    for tile in (32, 64, 256):
-        o = eng.search_opts(first=1, step=2, scheduler=1, tile=tile, warps_per_cta=8)
+    for tile, qg in ((16, 2), (32, 5), (64, 8), (128, 1)):
+        o = eng.search_opts(first=1, step=2, scheduler=1, tile=tile, warps_per_cta=8, queries_per_cta=qg)
         res = eng.ivf_query_batch(idx, qt, qr, 10, 5, eng.IvfMode.kAdSplit, opts=o)
         for qi in range(qt.shape[0]):
             ids, dists, stats = orc.ivf_query(lay, qt[qi], qr[qi], 10, 5, "ad-split", waves=[0, 1, 3])
