@@ -252,12 +252,13 @@ def run_search(args, D: Dist):
                                         C.c_void_p(d_dims.ptr), C.c_void_p(d_cand.ptr)))
 
     if args.tune and D.rank == 0:
-        for st_, w_, g_, sch, qg in ((256, 4, 64, 0, 1), (8, 8, 64, 1, 8), (16, 8, 64, 1, 8),
-                                     (16, 8, 64, 1, 16), (16, 16, 64, 1, 16), (16, 8, 32, 1, 16),
-                                     (16, 8, 128, 1, 4), (16, 4, 64, 1, 8), (32, 8, 64, 1, 8)):
+        for st_, w_, g_, sch, qg, qo in ((256, 4, 64, 0, 1, 0), (256, 4, 64, 0, 1, 1),
+                                         (128, 4, 64, 0, 1, 1), (512, 4, 64, 0, 1, 1),
+                                         (256, 8, 64, 0, 1, 1), (16, 16, 64, 1, 16, 1)):
             if True:
                 o2 = ads.search_opts(first=1 if sch else 0, step=st_, warps_per_cta=w_, tile=g_,
-                                     scheduler=sch, queries_per_cta=qg, time_stages=True)
+                                     scheduler=sch, queries_per_cta=qg, time_stages=True,
+                                     query_order=qo)
                 ts, dm = [], 0
                 for rep in range(4):
                     ctx.flush_l2()
@@ -265,7 +266,7 @@ def run_search(args, D: Dist):
                     ts.append(float(idx.last_timings()[3]))
                     dm = float(r_.dims.mean())
                 scan = float(np.min(ts))
-                log(f"tune sched={sch} step={st_} warps={w_} tile={g_} qgroup={qg}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
+                log(f"tune sched={sch} order={qo} step={st_} warps={w_} tile={g_} qgroup={qg}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
                     f"recall {ads.recall_batch(r_.ids, gt, K):.5f}")
     for _ in range(args.warmup):
         ctx.flush_l2()

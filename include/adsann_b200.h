@@ -215,6 +215,9 @@ typedef struct {
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */
     int32_t scheduler;     /* 0 query-major (default), 1 list-major waves (16-byte-aligned layouts) */
     int32_t tile;          /* list-major: candidates staged per shared-memory tile (default 64) */
+    int32_t query_order;   /* 1: run the batch's queries in an L2-friendly order (by the
+                              nearest list's position in a nearest-neighbour chain of centroids);
+                              results do not depend on it */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 

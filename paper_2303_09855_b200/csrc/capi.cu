@@ -118,6 +118,8 @@ struct ads_ivf {
     std::map<PlanKey, std::unique_ptr<DevSegPlan>> plans;
     DevBuf dist, probes, qrot, qin_t, qin_raw, o_ids, o_dists, o_cnt, o_dims, o_cand;
     ListMajorScratch lm;
+    int32_t* chain_rank = nullptr;  // L2-locality rank of each list (host chain over centroids)
+    DevBuf order, order_tmp;
     cudaEvent_t ev[5] = {};
     float last_ms[4] = {0, 0, 0, 0};
     bool timed = false;
@@ -126,7 +128,7 @@ struct ads_ivf {
                         static_cast<void*>(list_off), static_cast<void*>(ids),
                         static_cast<void*>(a1_t), static_cast<void*>(a2_t),
                         static_cast<void*>(a1_raw), static_cast<void*>(a2_raw),
-                        static_cast<void*>(P)})
+                        static_cast<void*>(P), static_cast<void*>(chain_rank)})
             if (p) cudaFree(p);
         for (auto& kv : plans) kv.second->release();
         for (auto& e : ev)
@@ -730,6 +732,10 @@ int ads_ivf_create(ads_ctx* ctx, const ads_ivf_desc* desc, ads_ivf** out) {
             split_up(s.a1_raw, s.a2_raw, s.vec_raw, &x->a1_raw, &x->a2_raw);
         }
         if (s.P) x->P = dev_upload(s.P, static_cast<size_t>(D) * D, st);
+        {
+            const std::vector<int32_t> rk = centroid_chain_rank(s.centroids_t, s.k_clusters, D);
+            x->chain_rank = dev_upload(rk.data(), rk.size(), st);
+        }
         ADS_CUDA(cudaStreamSynchronize(st));
         *out = x.release();
     });
@@ -788,6 +794,11 @@ int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int
                 ADS_CUDA(cudaStreamSynchronize(st));
                 cudaFree(dPT);
             }
+            std::vector<float> hc(static_cast<size_t>(k) * d);
+            ADS_CUDA(cudaMemcpyAsync(hc.data(), x->cent_t, sizeof(float) * hc.size(), cudaMemcpyDeviceToHost, st));
+            ADS_CUDA(cudaStreamSynchronize(st));
+            const std::vector<int32_t> rk = centroid_chain_rank(hc.data(), k, d);
+            x->chain_rank = dev_upload(rk.data(), rk.size(), st);
             ADS_CUDA(cudaStreamSynchronize(st));
         } catch (...) {
             cudaStreamSynchronize(st);
@@ -854,6 +865,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->time_stages = 0;
     o->scheduler = 0;
     o->tile = 64;
+    o->query_order = 0;
 }
 
 namespace {
@@ -967,6 +979,12 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.out_dims = reinterpret_cast<unsigned long long*>(ddims);
     a.out_cand = reinterpret_cast<unsigned long long*>(dcand);
     a.counter = x->ctx->counter;
+    a.order = nullptr;
+    if (o.query_order && x->chain_rank && nq > 1) {
+        int32_t* ord = x->order.get<int32_t>(nq);
+        launch_query_order(probes, nq, nprobe, x->chain_rank, x->k, x->order_tmp, ord, st);
+        a.order = ord;
+    }
     if (o.scheduler == 1 && a.vec == 4) {
         ListMajorLaunch m{};
         m.a1 = a.a1;
@@ -1112,6 +1130,10 @@ int ads_ivf_subset(ads_ivf* src, const uint8_t* keep, ads_ivf** out) {
                                      cudaMemcpyDeviceToDevice, st));
             ADS_CUDA(cudaMalloc(&x->a1_raw, sizeof(float) * nn * d1p));
             ADS_CUDA(cudaMalloc(&x->a2_raw, sizeof(float) * (nn * d2p > 0 ? nn * d2p : 1)));
+        }
+        if (src->chain_rank) {
+            ADS_CUDA(cudaMalloc(&x->chain_rank, sizeof(int32_t) * k));
+            ADS_CUDA(cudaMemcpyAsync(x->chain_rank, src->chain_rank, sizeof(int32_t) * k, cudaMemcpyDeviceToDevice, st));
         }
         if (src->P) {
             ADS_CUDA(cudaMalloc(&x->P, sizeof(double) * D * static_cast<size_t>(D)));

@@ -96,6 +96,7 @@ struct SearchLaunch {
     unsigned long long* out_dims;
     unsigned long long* out_cand;
     unsigned long long* counter;
+    const int32_t* order;  // nullable: work item w searches query order[w]
 };
 void launch_ivf_search(const SearchLaunch& a, cudaStream_t st);
 
@@ -183,6 +184,13 @@ void gather_split(const float* src, const int32_t* dIds, int64_t n, int D, int d
 // Per query, K smallest (dist, id) pairs among G lists of K ([G][nq][K]).
 void launch_merge_topk(const double* dists, const int32_t* ids, int G, int nq, int K,
                        int32_t* out_ids, double* out_dists, int32_t* out_cnt, cudaStream_t st);
+
+// L2-locality order of a query batch: stable sort by rank[nearest list].
+void launch_query_order(const int32_t* probes, int nq, int nprobe, const int32_t* rank, int k,
+                        DevBuf& scratch, int32_t* order, cudaStream_t st);
+// Greedy nearest-neighbour chain over the centroids (host, fp32 heuristic):
+// rank[c] = position of list c in the chain.
+std::vector<int32_t> centroid_chain_rank(const float* C, int k, int D);
 
 int num_sms();
 

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -86,6 +87,58 @@ std::vector<double> generate_orthogonal(int dim, uint64_t seed) {
         throw std::runtime_error("generate_orthogonal: orthonormality deviation " + std::to_string(w) +
                                  " exceeds 1e-10");
     return m;
+}
+
+// Greedy nearest-neighbour chain (fp32, heuristic: only used to order work).
+std::vector<int32_t> centroid_chain_rank(const float* C, int k, int D) {
+    std::vector<int32_t> rank(static_cast<size_t>(k), 0);
+    if (k <= 1) return rank;
+    std::vector<char> used(static_cast<size_t>(k), 0);
+    const int nt = std::max(1, std::min<int>(static_cast<int>(std::thread::hardware_concurrency()), 32));
+    std::vector<float> bestd(nt);
+    std::vector<int> besti(nt);
+    int cur = 0;
+    used[0] = 1;
+    for (int step = 1; step < k; ++step) {
+        const float* a = C + static_cast<size_t>(cur) * D;
+        auto scan = [&](int t) {
+            float bd = std::numeric_limits<float>::infinity();
+            int bi = -1;
+            for (int c = t; c < k; c += nt) {
+                if (used[c]) continue;
+                const float* b = C + static_cast<size_t>(c) * D;
+                float s = 0.f;
+                for (int j = 0; j < D; ++j) {
+                    const float df = a[j] - b[j];
+                    s += df * df;
+                }
+                if (s < bd || (s == bd && c < bi)) {
+                    bd = s;
+                    bi = c;
+                }
+            }
+            bestd[t] = bd;
+            besti[t] = bi;
+        };
+        if (static_cast<int64_t>(k) * D < 200000) {
+            for (int t = 0; t < nt; ++t) scan(t);
+        } else {
+            std::vector<std::thread> th;
+            for (int t = 0; t < nt; ++t) th.emplace_back(scan, t);
+            for (auto& x : th) x.join();
+        }
+        int nxt = -1;
+        float nd = std::numeric_limits<float>::infinity();
+        for (int t = 0; t < nt; ++t)
+            if (besti[t] >= 0 && (bestd[t] < nd || (bestd[t] == nd && besti[t] < nxt))) {
+                nd = bestd[t];
+                nxt = besti[t];
+            }
+        used[nxt] = 1;
+        rank[nxt] = step;
+        cur = nxt;
+    }
+    return rank;
 }
 
 }  // namespace ads

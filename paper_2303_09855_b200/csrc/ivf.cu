@@ -17,6 +17,8 @@
 //                        then thr[t] = factor[d_t] * r^2 is rebuilt.
 #include <cfloat>
 
+#include <cub/cub.cuh>
+
 #include "engine.hpp"
 #include "scan_engine.cuh"
 
@@ -264,9 +266,9 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            const int q = static_cast<int>(atomicAdd(a.counter, 1ull));
-            sh.q = q;
-            sh.stop = q >= a.nq;
+            const int w = static_cast<int>(atomicAdd(a.counter, 1ull));
+            sh.stop = w >= a.nq;
+            sh.q = sh.stop ? w : (a.order ? a.order[w] : w);
             sh.cnt = 0;
             sh.r = kInf;
             sh.r_sq = kInf;
@@ -437,6 +439,32 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
 }
 
 }  // namespace
+
+namespace {
+__global__ void order_keys_kernel(const int32_t* probes, int nq, int nprobe, const int32_t* rank,
+                                  int32_t* keys, int32_t* vals) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    keys[q] = rank[probes[static_cast<int64_t>(q) * nprobe]];
+    vals[q] = q;
+}
+}  // namespace
+
+void launch_query_order(const int32_t* probes, int nq, int nprobe, const int32_t* rank, int k,
+                        DevBuf& scratch, int32_t* order, cudaStream_t st) {
+    int bits = 1;
+    while ((1 << bits) < k) ++bits;
+    int32_t* kin = scratch.get<int32_t>(static_cast<size_t>(nq) * 3 + 64);
+    int32_t* kout = kin + nq;
+    int32_t* vin = kout + nq;
+    order_keys_kernel<<<(nq + 255) / 256, 256, 0, st>>>(probes, nq, nprobe, rank, kin, vin);
+    ADS_LAUNCH_CHECK();
+    size_t tmp = 0;
+    ADS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, order, nq, 0, bits, st));
+    static thread_local DevBuf tmpbuf;
+    void* t = tmpbuf.get<unsigned char>(tmp);
+    ADS_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, order, nq, 0, bits, st));
+}
 
 void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,
                         cudaStream_t st) {
