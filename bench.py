@@ -41,7 +41,7 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
         self.nccl = None
-        if self.world > 1:
+        if self.world > 1 or os.environ.get("ADS_FORCE_DIST") == "1":
             import torch
             import torch.distributed as dist
 
@@ -578,6 +578,8 @@ def main():
     ap.add_argument("--shard", default="lists", choices=["lists", "replicas"],
                     help="N>1: IVF lists partitioned across GPUs + NCCL all-gather merge, or replicas")
     ap.add_argument("--dco-n", type=int, default=10_000_000)
+    ap.add_argument("--force-shard", action="store_true",
+                    help="run the list-sharded path even at N=1 (exercises NCCL + merge)")
     ap.add_argument("--kmeans-iters", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -591,7 +593,7 @@ def main():
             from bench_dco import run_dco
 
             res = run_dco(args, D)
-        elif sharded and D.world > 1:
+        elif sharded and (D.world > 1 or args.force_shard):
             res = run_search_sharded(args, D)
         else:
             res = run_search(args, D)
