@@ -218,6 +218,9 @@ typedef struct {
     int32_t query_order;   /* 1: run the batch's queries in an L2-friendly order (by the
                               nearest list's position in a nearest-neighbour chain of centroids);
                               results do not depend on it */
+    int32_t coarse_mode;   /* 0 (default): certified fp32 prefilter + exact fp64 rescoring of the
+                              centroids that can reach the top-nprobe; 1: exact fp64 distance to
+                              every centroid.  Both give probe_order's exact (d2, id) order. */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 

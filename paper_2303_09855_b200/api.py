@@ -445,14 +445,14 @@ def recall_batch(ids: np.ndarray, gt: np.ndarray, K: int) -> float:
 
 def search_opts(first: int = 0, step: int = 256, warps_per_cta: int = 4, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
-                tile: int = 64, query_order: int = 0) -> L.SearchOpts:
+                tile: int = 64, query_order: int = 0, coarse_mode: int = 0) -> L.SearchOpts:
     """scheduler 0: query-major, first/step in candidates; scheduler 1: list-major
     waves, first/step in probed lists (see include/adsann_b200.h)."""
     o = L.SearchOpts()
     L.ads_search_opts_default(C.byref(o))
     o.first, o.step, o.warps_per_cta, o.queries_per_cta, o.ctas_per_sm, o.time_stages = (
         first, step, warps_per_cta, queries_per_cta, ctas_per_sm, int(time_stages))
-    o.scheduler, o.tile, o.query_order = scheduler, tile, query_order
+    o.scheduler, o.tile, o.query_order, o.coarse_mode = scheduler, tile, query_order, coarse_mode
     return o
 
 

@@ -120,6 +120,9 @@ struct ads_ivf {
     ListMajorScratch lm;
     int32_t* chain_rank = nullptr;  // L2-locality rank of each list (host chain over centroids)
     DevBuf order, order_tmp;
+    // coarse prefilter state per centroid space (transformed / raw)
+    CoarseCentroids cc_t, cc_raw;
+    CoarseScratch coarse;
     cudaEvent_t ev[5] = {};
     float last_ms[4] = {0, 0, 0, 0};
     bool timed = false;
@@ -130,6 +133,8 @@ struct ads_ivf {
                         static_cast<void*>(a1_raw), static_cast<void*>(a2_raw),
                         static_cast<void*>(P), static_cast<void*>(chain_rank)})
             if (p) cudaFree(p);
+        cc_t.release();
+        cc_raw.release();
         for (auto& kv : plans) kv.second->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -685,6 +690,36 @@ static void ivf_alloc_common(ads_ivf* x) {
     for (auto& e : x->ev) ADS_CUDA(cudaEventCreate(&e));
 }
 
+// Centred centroid table for the coarse prefilter (coarse.cu): mean in fp64 (host),
+// c~ = fl32(c - mu), |c~|^2 and the largest |c~|.
+static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& out, cudaStream_t st) {
+    std::vector<float> h(static_cast<size_t>(k) * D);
+    ADS_CUDA(cudaMemcpyAsync(h.data(), dC, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, st));
+    ADS_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> mu(static_cast<size_t>(D), 0.0);
+    for (int c = 0; c < k; ++c)
+        for (int j = 0; j < D; ++j) mu[j] += h[static_cast<size_t>(c) * D + j];
+    for (double& v : mu) v /= k;
+    out.mu = dev_upload(mu.data(), mu.size(), st);
+    ADS_CUDA(cudaMalloc(&out.cc, sizeof(float) * h.size()));
+    ADS_CUDA(cudaMalloc(&out.cn2, sizeof(float) * k));
+    double* nrm = nullptr;
+    ADS_CUDA(cudaMalloc(&nrm, sizeof(double) * k));
+    coarse_center(dC, k, D, out.mu, out.cc, out.cn2, nrm, st);
+    std::vector<double> hn(static_cast<size_t>(k));
+    ADS_CUDA(cudaMemcpyAsync(hn.data(), nrm, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    ADS_CUDA(cudaStreamSynchronize(st));
+    cudaFree(nrm);
+    double m = 0.0;
+    for (double v : hn) m = std::max(m, v);
+    out.cmax = m * (1.0 + 1e-12) + 1e-300;
+}
+
+static void ivf_finish_coarse(ads_ivf* x, cudaStream_t st) {
+    centroid_prefilter(x->cent_t, x->k, x->d, x->cc_t, st);
+    if (x->cent_raw) centroid_prefilter(x->cent_raw, x->k, x->d, x->cc_raw, st);
+}
+
 int ads_ivf_create(ads_ctx* ctx, const ads_ivf_desc* desc, ads_ivf** out) {
     return guard([&] {
         const ads_ivf_desc& s = *desc;
@@ -736,6 +771,7 @@ int ads_ivf_create(ads_ctx* ctx, const ads_ivf_desc* desc, ads_ivf** out) {
             const std::vector<int32_t> rk = centroid_chain_rank(s.centroids_t, s.k_clusters, D);
             x->chain_rank = dev_upload(rk.data(), rk.size(), st);
         }
+        ivf_finish_coarse(x.get(), st);
         ADS_CUDA(cudaStreamSynchronize(st));
         *out = x.release();
     });
@@ -799,6 +835,7 @@ int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int
             ADS_CUDA(cudaStreamSynchronize(st));
             const std::vector<int32_t> rk = centroid_chain_rank(hc.data(), k, d);
             x->chain_rank = dev_upload(rk.data(), rk.size(), st);
+            ivf_finish_coarse(x.get(), st);
             ADS_CUDA(cudaStreamSynchronize(st));
         } catch (...) {
             cudaStreamSynchronize(st);
@@ -866,6 +903,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->scheduler = 0;
     o->tile = 64;
     o->query_order = 0;
+    o->coarse_mode = 0;
 }
 
 namespace {
@@ -936,11 +974,18 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
         Qs = qr;
     }
     if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[1], st));
-    double* dist = x->dist.get<double>(static_cast<size_t>(nq) * x->k);
     int32_t* probes = x->probes.get<int32_t>(static_cast<size_t>(nq) * nprobe);
-    launch_coarse_dist(Qs, nq, transformed ? x->cent_t : x->cent_raw, x->k, D, dist, st);
-    if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[2], st));
-    launch_select_probes(dist, nq, x->k, nprobe, probes, st);
+    const float* cent = transformed ? x->cent_t : x->cent_raw;
+    if (o.coarse_mode == 0) {  // certified fp32 prefilter + exact fp64 rescoring (coarse.cu)
+        launch_coarse_probes_fast(Qs, nq, cent, x->k, D, nprobe, transformed ? x->cc_t : x->cc_raw,
+                                  x->coarse, probes, st);
+        if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[2], st));
+    } else {  // exact fp64 distance to every centroid, then select
+        double* dist = x->dist.get<double>(static_cast<size_t>(nq) * x->k);
+        launch_coarse_dist(Qs, nq, cent, x->k, D, dist, st);
+        if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[2], st));
+        launch_select_probes(dist, nq, x->k, nprobe, probes, st);
+    }
     if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[3], st));
     DevSegPlan& plan = ivf_plan(x, mode, eps0, dd);
     SearchLaunch a{};
@@ -1083,10 +1128,9 @@ int ads_ivf_probe_order(ads_ivf* x, const float* Q, int32_t nq, int32_t nprobe, 
         const size_t qn = static_cast<size_t>(nq) * x->d;
         float* dq = x->qin_t.get<float>(qn);
         ADS_CUDA(cudaMemcpyAsync(dq, Q, qn * sizeof(float), cudaMemcpyHostToDevice, st));
-        double* dist = x->dist.get<double>(static_cast<size_t>(nq) * x->k);
         int32_t* dp = x->probes.get<int32_t>(static_cast<size_t>(nq) * nprobe);
-        launch_coarse_dist(dq, nq, transformed ? x->cent_t : x->cent_raw, x->k, x->d, dist, st);
-        launch_select_probes(dist, nq, x->k, nprobe, dp, st);
+        launch_coarse_probes_fast(dq, nq, transformed ? x->cent_t : x->cent_raw, x->k, x->d, nprobe,
+                                  transformed ? x->cc_t : x->cc_raw, x->coarse, dp, st);
         ADS_CUDA(cudaMemcpyAsync(probes, dp, sizeof(int32_t) * nq * nprobe, cudaMemcpyDeviceToHost, st));
         ADS_CUDA(cudaStreamSynchronize(st));
     });
@@ -1140,6 +1184,7 @@ int ads_ivf_subset(ads_ivf* src, const uint8_t* keep, ads_ivf** out) {
             ADS_CUDA(cudaMemcpyAsync(x->P, src->P, sizeof(double) * D * static_cast<size_t>(D),
                                      cudaMemcpyDeviceToDevice, st));
         }
+        ivf_finish_coarse(x.get(), st);
         // owned lists are contiguous row ranges in every flat array: one copy per run of
         // consecutive owned lists
         for (int c = 0; c < k;) {

@@ -153,6 +153,30 @@ struct ListMajorScratch {
 void launch_listmajor_search(const ListMajorLaunch& a, ListMajorScratch& s, cudaStream_t st);
 size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int qgroup);
 
+// Certified coarse quantizer (coarse.cu): fp32 prefilter + exact fp64 rescoring.
+struct CoarseScratch {
+    DevBuf approx, qc, qn2, qnrm;
+};
+// Per centroid table: mean mu (fp64), centred fp32 copy, |c~|^2 and max |c~|.
+struct CoarseCentroids {
+    double* mu = nullptr;
+    float* cc = nullptr;
+    float* cn2 = nullptr;
+    double cmax = 0.0;
+    void release() {
+        for (void* p : {static_cast<void*>(mu), static_cast<void*>(cc), static_cast<void*>(cn2)})
+            if (p) cudaFree(p);
+        mu = nullptr;
+        cc = nullptr;
+        cn2 = nullptr;
+    }
+};
+void coarse_center(const float* X, int n, int D, const double* mu, float* Xc, float* n2, double* nrm,
+                   cudaStream_t st);
+void launch_coarse_probes_fast(const float* Q, int nq, const float* C, int L, int D, int nprobe,
+                               const CoarseCentroids& cc, CoarseScratch& s, int32_t* probes,
+                               cudaStream_t st);
+
 // Exact fp64 centroid distances (nq x L, l2_sq order) and top-nprobe by (d2, id).
 void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,
                         cudaStream_t st);

@@ -300,3 +300,32 @@ def test_ivf_listmajor_tiles_smaller_than_lists(eng, orc):
             ids, dists, stats = orc.ivf_query(lay, qt[qi], qr[qi], 10, 5, "ad-split", waves=[0, 1, 3])
             np.testing.assert_array_equal(res.ids[qi, :len(ids)], ids)
             assert int(res.dims[qi]) == int(stats[0])
+
+
+def test_coarse_prefilter_adversarial_ties(eng, orc):
+    """Certified prefilter == exact probe_order with exact and near-duplicate centroids."""
+    rng = np.random.default_rng(12)
+    d, L = 96, 300
+    base = rng.normal(0, 1, (L, d)).astype(np.float32)
+    base[1] = base[0]                              # exact duplicate centroid
+    base[2] = base[0] + np.float32(1e-6)           # near duplicates
+    base[3] = np.nextafter(base[0], np.float32(np.inf))
+    base[10:20] = base[9]                          # a block of identical centroids
+    n = L  # one point per list: point i == centroid i
+    P = orc.generate_orthogonal(d, 3)
+    lay = {"n": n, "d": d, "k": L, "d1": 32, "split": True, "centroids_t": base,
+           "centroids_raw": base, "list_off": np.arange(L + 1, dtype=np.int64),
+           "ids_flat": np.arange(n, dtype=np.int32), "vec_t": base, "vec_raw": base,
+           "a1_t": base[:, :32].copy(), "a2_t": base[:, 32:].copy(), "a1_raw": base[:, :32].copy(),
+           "a2_raw": base[:, 32:].copy()}
+    idx = gpu_index(eng, lay, P)
+    Q = np.concatenate([base[:12] + rng.normal(0, 1e-7, (12, d)).astype(np.float32),
+                        rng.normal(0, 1, (20, d)).astype(np.float32)])
+    for nprobe in (1, 2, 3, 5, 13, 64, L):
+        got = idx.probe_order(Q, nprobe)
+        for qi in range(Q.shape[0]):
+            np.testing.assert_array_equal(got[qi], orc.probe_order(base, Q[qi], nprobe))
+    a = eng.ivf_query_batch(idx, Q, Q, 5, 13, eng.IvfMode.kAdSplit, opts=eng.search_opts(coarse_mode=0))
+    b = eng.ivf_query_batch(idx, Q, Q, 5, 13, eng.IvfMode.kAdSplit, opts=eng.search_opts(coarse_mode=1))
+    np.testing.assert_array_equal(a.ids, b.ids)
+    np.testing.assert_array_equal(a.dims, b.dims)
