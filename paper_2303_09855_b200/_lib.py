@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libadsann_b200.so")
+LIB_PATH = os.environ.get("ADS_LIB_PATH") or os.path.join(HERE, "libadsann_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "adsann_b200.h")
 
 if not os.path.exists(LIB_PATH):

@@ -105,6 +105,16 @@ struct PlanKey {
     }
 };
 
+// A1 and A2 of one space share one allocation, A2 starting at the next 128-byte
+// boundary after A1, so the search kernel addresses a line of either array with
+// a single 32-bit offset (16-byte units) from the A1 base.
+static void alloc_split_pair(size_t n, int d1p, int d2p, float** a1, float** a2) {
+    const size_t n1 = (n * static_cast<size_t>(d1p) + 31) / 32 * 32;
+    const size_t n2 = n * static_cast<size_t>(d2p);
+    ADS_CUDA(cudaMalloc(a1, sizeof(float) * (n1 + (n2 > 0 ? n2 : 1))));
+    *a2 = *a1 + n1;
+}
+
 struct ads_ivf {
     ads_ctx* ctx = nullptr;
     int n = 0, d = 0, k = 0, d1 = 0, layout = 0, d1p = 0;
@@ -129,8 +139,7 @@ struct ads_ivf {
     ~ads_ivf() {
         for (void* p : {static_cast<void*>(cent_t), static_cast<void*>(cent_raw),
                         static_cast<void*>(list_off), static_cast<void*>(ids),
-                        static_cast<void*>(a1_t), static_cast<void*>(a2_t),
-                        static_cast<void*>(a1_raw), static_cast<void*>(a2_raw),
+                        static_cast<void*>(a1_t), static_cast<void*>(a1_raw),  // a2_* live inside
                         static_cast<void*>(P), static_cast<void*>(chain_rank)})
             if (p) cudaFree(p);
         cc_t.release();
@@ -747,8 +756,7 @@ int ads_ivf_create(ads_ctx* ctx, const ads_ivf_desc* desc, ads_ivf** out) {
         x->list_off = dev_upload(s.list_off, static_cast<size_t>(s.k_clusters) + 1, st);
         x->ids = dev_upload(s.ids_flat, n, st);
         auto split_up = [&](const float* a1, const float* a2, const float* vec, float** o1, float** o2) {
-            ADS_CUDA(cudaMalloc(o1, sizeof(float) * n * d1p));
-            ADS_CUDA(cudaMalloc(o2, sizeof(float) * (n * d2p > 0 ? n * d2p : 1)));
+            alloc_split_pair(n, d1p, d2p, o1, o2);
             if (a1) {
                 ADS_CUDA(cudaMemcpyAsync(*o1, a1, sizeof(float) * n * d1p, cudaMemcpyHostToDevice, st));
                 if (d2p) ADS_CUDA(cudaMemcpyAsync(*o2, a2, sizeof(float) * n * d2p, cudaMemcpyHostToDevice, st));
@@ -812,13 +820,11 @@ int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int
             ADS_CUDA(cudaMalloc(&x->list_off, sizeof(int64_t) * (k + 1)));
             ADS_CUDA(cudaMalloc(&x->ids, sizeof(int32_t) * N));
             build_lists(asg, n, k, x->list_off, x->ids, st);  // ivf.cpp:213-214, 229-241
-            ADS_CUDA(cudaMalloc(&x->a1_t, sizeof(float) * N * d1p));
-            ADS_CUDA(cudaMalloc(&x->a2_t, sizeof(float) * (N * d2p > 0 ? N * d2p : 1)));
+            alloc_split_pair(N, d1p, d2p, &x->a1_t, &x->a2_t);
             gather_split(dt, x->ids, n, d, d1p, x->a1_t, x->a2_t, st);
             if (dr) {
                 x->has_raw = true;
-                ADS_CUDA(cudaMalloc(&x->a1_raw, sizeof(float) * N * d1p));
-                ADS_CUDA(cudaMalloc(&x->a2_raw, sizeof(float) * (N * d2p > 0 ? N * d2p : 1)));
+                alloc_split_pair(N, d1p, d2p, &x->a1_raw, &x->a2_raw);
                 gather_split(dr, x->ids, n, d, d1p, x->a1_raw, x->a2_raw, st);
                 // centroids_raw = P^T centroids_t (ivf.cpp:216-226)
                 std::vector<double> PT(static_cast<size_t>(d) * d);
@@ -1007,9 +1013,12 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.ntest = plan.ntest;
     a.vec = plan.vec;
     a.full = plan.full;
-    // 16-byte line descriptors address each array in 31 bits of 16-byte units.
-    const int64_t widest = static_cast<int64_t>(x->n) * std::max(x->d1p, D - x->d1p);
-    if (widest / 4 >= (int64_t(1) << 31)) {
+    // 16-byte line descriptors address A1|A2 (one allocation) in 32 bits of
+    // 16-byte units from a1.
+    const int64_t gap = a.a2 - a.a1;
+    const int64_t units = (gap + static_cast<int64_t>(x->n) * (D - x->d1p)) / 4;
+    a.a2_16 = static_cast<uint32_t>(gap / 4);
+    if (gap < 0 || gap % 4 != 0 || units >= int64_t(0xffffffff)) {
         a.vec = 1;
         a.full = 0;
     }
@@ -1166,14 +1175,12 @@ int ads_ivf_subset(ads_ivf* src, const uint8_t* keep, ads_ivf** out) {
                                  cudaMemcpyDeviceToDevice, st));
         x->list_off = dev_upload(noff.data(), noff.size(), st);
         ADS_CUDA(cudaMalloc(&x->ids, sizeof(int32_t) * nn));
-        ADS_CUDA(cudaMalloc(&x->a1_t, sizeof(float) * nn * d1p));
-        ADS_CUDA(cudaMalloc(&x->a2_t, sizeof(float) * (nn * d2p > 0 ? nn * d2p : 1)));
+        alloc_split_pair(nn, d1p, d2p, &x->a1_t, &x->a2_t);
         if (x->has_raw) {
             ADS_CUDA(cudaMalloc(&x->cent_raw, sizeof(float) * k * static_cast<size_t>(D)));
             ADS_CUDA(cudaMemcpyAsync(x->cent_raw, src->cent_raw, sizeof(float) * k * static_cast<size_t>(D),
                                      cudaMemcpyDeviceToDevice, st));
-            ADS_CUDA(cudaMalloc(&x->a1_raw, sizeof(float) * nn * d1p));
-            ADS_CUDA(cudaMalloc(&x->a2_raw, sizeof(float) * (nn * d2p > 0 ? nn * d2p : 1)));
+            alloc_split_pair(nn, d1p, d2p, &x->a1_raw, &x->a2_raw);
         }
         if (src->chain_rank) {
             ADS_CUDA(cudaMalloc(&x->chain_rank, sizeof(int32_t) * k));

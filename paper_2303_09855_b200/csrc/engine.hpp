@@ -72,6 +72,7 @@ void launch_dco_fixed(const DcoLaunch& a, cudaStream_t st);
 struct SearchLaunch {
     const float* a1;
     const float* a2;
+    uint32_t a2_16;    // (a2 - a1) in 16-byte units (VEC=4: A2 follows A1 in one allocation)
     int d1;            // physical split (A1 row stride)
     int D;
     const int32_t* ids;

@@ -249,9 +249,9 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
     double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
     double* pend_d = topd + a.K;
-    int64_t* cpos = reinterpret_cast<int64_t*>(pend_d + chunk_cap);
-    int64_t* lstart = cpos + chunk_cap;
-    Seg* segs = reinterpret_cast<Seg*>(lstart + a.nprobe);
+    int64_t* lstart = reinterpret_cast<int64_t*>(pend_d + chunk_cap);
+    int32_t* cpos = reinterpret_cast<int32_t*>(lstart + a.nprobe);
+    Seg* segs = reinterpret_cast<Seg*>(cpos + ((chunk_cap + 1) & ~1));
     int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
     int32_t* pend_i = topi + a.K;
     int32_t* pre = pend_i + chunk_cap;
@@ -262,6 +262,10 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     float* wbuf = wbuf_all + warp * 1024;
     for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
     for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) tfac[i] = a.tfac[i];
+    // VEC=4 line descriptor = pos * stride + column offset, 16-byte units from a.a1
+    const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
+    const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
+    const char* gbase = lane_base16(a.a1);
 
     for (;;) {
         __syncthreads();
@@ -320,15 +324,14 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                     if (pre[mid] <= i) l = mid;
                     else h = mid - 1;
                 }
-                cpos[sl] = lstart[l] + (i - pre[l]);
+                cpos[sl] = static_cast<int32_t>(lstart[l] + (i - pre[l]));
             }
             if (threadIdx.x == 0) sh.next = lo;
             for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
             __syncthreads();
             const double r = sh.r, r_sq = sh.r_sq;
 
-            int cand = -1, seg = 0;
-            int64_t pos = 0;
+            int cand = -1, seg = 0, pos = 0;
             double s = 0.0;
             for (;;) {
                 const unsigned need = __ballot_sync(kFull, cand < 0);
@@ -350,21 +353,19 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 const Seg sg = segs[seg];
                 if constexpr (VEC == 4) {
                     uint32_t dsc = kNoLine;
-                    if (cand >= 0) {
-                        const int64_t off = sg.arr == 0 ? pos * a.d1 + sg.col
-                                                        : pos * (a.D - a.d1) + (sg.col - a.d1);
-                        dsc = (static_cast<uint32_t>(sg.arr) << 31) | static_cast<uint32_t>(off >> 2);
-                    }
-                    gather_issue16<FULL>(wbuf, a.a1, a.a2, dsc, sg.len >> 2);
+                    if (cand >= 0)
+                        dsc = sg.arr == 0 ? static_cast<uint32_t>(pos) * str1 + (sg.col >> 2)
+                                          : static_cast<uint32_t>(pos) * str2 + a2c + (sg.col >> 2);
+                    gather_issue16<FULL>(wbuf, gbase, dsc, sg.len >> 2);
                 } else {
-                    const float* src = sg.arr == 0 ? a.a1 + pos * a.d1 + sg.col
-                                                   : a.a2 + pos * (a.D - a.d1) + (sg.col - a.d1);
+                    const float* src = sg.arr == 0 ? a.a1 + static_cast<int64_t>(pos) * a.d1 + sg.col
+                                                   : a.a2 + static_cast<int64_t>(pos) * (a.D - a.d1) + (sg.col - a.d1);
                     gather_issue4(wbuf, src, cand >= 0 ? sg.len : 0);
                 }
                 cp_async_wait_group<0>();
                 __syncwarp();
                 if (cand >= 0) {
-                    s = accumulate_line<VEC>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                    s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
                     if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
                         my_dims += static_cast<unsigned long long>(sg.col + sg.len);
                         cand = -1;
@@ -431,7 +432,7 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
     size_t b = sizeof(float) * a.warps * 1024;
     b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + chunk_cap);
-    b += sizeof(int64_t) * (a.nprobe + chunk_cap);
+    b += sizeof(int64_t) * a.nprobe + sizeof(int32_t) * ((chunk_cap + 1) & ~1);
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + chunk_cap + a.nprobe + 1);
     b += sizeof(unsigned) * ((chunk_cap + 31) / 32);

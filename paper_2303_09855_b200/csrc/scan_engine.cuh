@@ -27,8 +27,8 @@ namespace ads {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kQPitch = 34;  // doubles per segment slot of the staged query (16-byte aligned)
 
-// 16-byte-granular line descriptor for the VEC=4 path: bit 31 selects the
-// array (A1 / A2), bits 0..30 the line start in 16-byte units.
+// 16-byte-granular line descriptor for the VEC=4 path: the line start in
+// 16-byte units from one base (A1 and A2 share an allocation, A2 after A1).
 constexpr uint32_t kNoLine = 0xffffffffu;
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
@@ -37,24 +37,31 @@ __device__ __forceinline__ void cp_async_wait_group() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// VEC=4: issue the copies of the warp's 32 lines (packed descriptors), no wait.
+// VEC=4: issue the copies of the warp's 32 lines (descriptors), no wait.
 // full_len: every line is 32 floats (no per-line length shuffle).
+// bc = base + (lane & 7) * 16 bytes (lane_base16), kept in a register by the caller.
+__device__ __forceinline__ const char* lane_base16(const float* base) {
+    const char* p = reinterpret_cast<const char*>(base) + (lane_id() & 7u) * 16u;
+    unsigned long long v;
+    // opaque copy: stops the compiler from re-deriving the pointer from the
+    // kernel-parameter bank inside every predicated copy
+    asm volatile("mov.b64 %0, %1;" : "=l"(v) : "l"(reinterpret_cast<unsigned long long>(p)));
+    return reinterpret_cast<const char*>(v);
+}
+
 template <bool FULL>
-__device__ __forceinline__ void gather_issue16(float* wbuf, const float* base0, const float* base1,
-                                               uint32_t desc, int nchunk) {
+__device__ __forceinline__ void gather_issue16(float* wbuf, const char* bc, uint32_t desc, int nchunk) {
     const unsigned lane = lane_id();
+    const int c = static_cast<int>(lane & 7u);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int L = j * 4 + static_cast<int>(lane >> 3);
-        const int c = static_cast<int>(lane & 7u);
         const uint32_t dsc = __shfl_sync(kFull, desc, L);
         int l = 8;
         if constexpr (!FULL) l = __shfl_sync(kFull, nchunk, L);
-        if (dsc != kNoLine && c < l) {
-            const float* base = (dsc >> 31) ? base1 : base0;
+        if (dsc != kNoLine && c < l)
             cp_async16(wbuf + L * 32 + (((c + L) & 7) << 2),
-                       base + (static_cast<size_t>(dsc & 0x7fffffffu) << 2) + c * 4);
-        }
+                       reinterpret_cast<const float*>(bc + static_cast<uint64_t>(dsc) * 16u));
     }
     cp_async_commit();
 }
@@ -98,16 +105,17 @@ __device__ __forceinline__ void gather_lines(float* wbuf, const float* src, int 
 }
 
 // Adds the lane's gathered segment (len floats) to s, index order, fp64.
-template <int VEC>
+// FULL: len == 32 for every segment (no per-chunk guard).
+template <int VEC, bool FULL = false>
 __device__ __forceinline__ double accumulate_line(const float* wbuf, const double* qq, int len,
                                                   double s) {
     const unsigned lane = lane_id();
     const float* row = wbuf + lane * 32;
     if constexpr (VEC == 4) {
-        const int nc = len >> 2;
+        const int nc = FULL ? 8 : len >> 2;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            if (c < nc) {
+            if (FULL || c < nc) {
                 const float4 v =
                     *reinterpret_cast<const float4*>(row + (((c + static_cast<int>(lane)) & 7) << 2));
                 const double2 q0 = *reinterpret_cast<const double2*>(qq + c * 4);
