@@ -209,8 +209,8 @@ int ads_ivf_export(ads_ivf *idx, float *centroids_t, float *centroids_raw, int64
 typedef struct {
     int64_t first;         /* default K (scheduler 0) / 1 list (scheduler 1) */
     int64_t step;          /* default 256 candidates (scheduler 0) */
-    int32_t warps_per_cta; /* default 8 */
-    int32_t queries_per_cta; /* query slots served concurrently by one CTA, default 4 */
+    int32_t warps_per_cta; /* default 4 */
+    int32_t queries_per_cta; /* reserved: the query-major kernel serves one query per CTA */
     int32_t ctas_per_sm;   /* 0 = occupancy maximum */
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */
     int32_t scheduler;     /* 0 query-major (default), 1 list-major waves (16-byte-aligned layouts) */

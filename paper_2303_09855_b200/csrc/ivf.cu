@@ -233,7 +233,8 @@ __device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double 
 
 struct SearchShared {
     double r, r_sq;
-    int q, stop, total, next, cnt;
+    int q, stop, total, next, cnt, pnext;
+    int pcount[2];
     unsigned long long dims;
 };
 
@@ -249,9 +250,10 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
     double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
     double* pend_d = topd + a.K;
-    int64_t* lstart = reinterpret_cast<int64_t*>(pend_d + chunk_cap);
-    int32_t* cpos = reinterpret_cast<int32_t*>(lstart + a.nprobe);
-    Seg* segs = reinterpret_cast<Seg*>(cpos + ((chunk_cap + 1) & ~1));
+    double* pre_s = pend_d + chunk_cap;  // 2 x chunk_cap: untested-prefix sums, by chunk parity
+    int32_t* lstart = reinterpret_cast<int32_t*>(pre_s + 2 * chunk_cap);
+    int32_t* cpos = lstart + a.nprobe;
+    Seg* segs = reinterpret_cast<Seg*>(cpos + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
     int32_t* pend_i = topi + a.K;
     int32_t* pre = pend_i + chunk_cap;
@@ -266,9 +268,27 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
     const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
     const char* gbase = lane_base16(a.a1);
+    // stream index -> flat position (last probed list with pre[l] <= i)
+    auto locate = [&](int i) {
+        int l = 0, h = a.nprobe - 1;
+        while (l < h) {
+            const int mid = (l + h + 1) >> 1;
+            if (pre[mid] <= i) l = mid;
+            else h = mid - 1;
+        }
+        return lstart[l] + (i - pre[l]);
+    };
+    int nseg0 = -1;  // leading segments no threshold test depends on (set after the first barrier)
 
     for (;;) {
         __syncthreads();
+        if (nseg0 < 0) {
+            // The split layouts' A1 prefix (and FD's whole walk but the last
+            // segment) is tested against nothing (ivf.cpp:366-386): lanes left
+            // idle at a chunk's tail precompute it for the next chunk.
+            nseg0 = 0;
+            while (nseg0 < a.nseg - 1 && segs[nseg0].test < 0) ++nseg0;
+        }
         if (threadIdx.x == 0) {
             const int w = static_cast<int>(atomicAdd(a.counter, 1ull));
             sh.stop = w >= a.nq;
@@ -291,7 +311,7 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 if (i < a.nprobe) {
                     const int p = a.probes[static_cast<int64_t>(qi) * a.nprobe + i];
                     const int64_t s0 = a.list_off[p];
-                    lstart[i] = s0;
+                    lstart[i] = static_cast<int32_t>(s0);
                     len = static_cast<int>(a.list_off[p + 1] - s0);
                 }
                 int incl = len;
@@ -312,29 +332,29 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
         const int total = sh.total;
         unsigned long long my_dims = 0;
 
-        for (int lo = 0; lo < total;) {
+        if (threadIdx.x == 0) sh.pcount[0] = 0;
+        for (int lo = 0, j = 0; lo < total; ++j) {
             const int64_t span = lo == 0 ? a.first : a.step;
             const int hi = static_cast<int>(lo + span < total ? lo + span : total);
-            // stream index -> flat position for every candidate of the chunk
-            for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) {
-                const int i = lo + sl;
-                int l = 0, h = a.nprobe - 1;  // last list with pre[k] <= i
-                while (l < h) {
-                    const int mid = (l + h + 1) >> 1;
-                    if (pre[mid] <= i) l = mid;
-                    else h = mid - 1;
-                }
-                cpos[sl] = static_cast<int32_t>(lstart[l] + (i - pre[l]));
+            const int nhi = static_cast<int>(hi + a.step < total ? hi + a.step : total);  // next chunk [hi, nhi)
+            double* pre_cur = pre_s + (j & 1) * chunk_cap;
+            double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
+            for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) cpos[sl] = locate(lo + sl);
+            if (threadIdx.x == 0) {
+                sh.next = lo;
+                sh.pnext = 0;
             }
-            if (threadIdx.x == 0) sh.next = lo;
             for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
             __syncthreads();
             const double r = sh.r, r_sq = sh.r_sq;
+            const int pc = sh.pcount[j & 1];  // [lo, lo + pc) carry their prefix in pre_cur
+            const bool can_pre = nseg0 > 0 && nhi > hi;
 
             int cand = -1, seg = 0, pos = 0;
+            bool prew = false;  // lane holds a next-chunk candidate's untested prefix
             double s = 0.0;
             for (;;) {
-                const unsigned need = __ballot_sync(kFull, cand < 0);
+                unsigned need = __ballot_sync(kFull, cand < 0);
                 if (need) {
                     int base = 0;
                     if (lane == 0) base = atomicAdd(&sh.next, __popc(need));
@@ -344,8 +364,32 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                         if (i < hi) {
                             cand = i;
                             pos = cpos[i - lo];
-                            seg = 0;
-                            s = 0.0;
+                            prew = false;
+                            if (i - lo < pc) {
+                                seg = nseg0;
+                                s = pre_cur[i - lo];
+                            } else {
+                                seg = 0;
+                                s = 0.0;
+                            }
+                        }
+                    }
+                    if (can_pre) {
+                        need = __ballot_sync(kFull, cand < 0);
+                        if (need) {
+                            int pb = 0;
+                            if (lane == 0) pb = atomicAdd(&sh.pnext, __popc(need));
+                            pb = __shfl_sync(kFull, pb, 0);
+                            if (cand < 0) {
+                                const int rel = pb + __popc(need & ((1u << lane) - 1u));
+                                if (rel < nhi - hi) {
+                                    cand = rel;
+                                    pos = locate(hi + rel);
+                                    prew = true;
+                                    seg = 0;
+                                    s = 0.0;
+                                }
+                            }
                         }
                     }
                 }
@@ -366,7 +410,14 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 __syncwarp();
                 if (cand >= 0) {
                     s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
-                    if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
+                    if (prew) {
+                        if (seg + 1 == nseg0) {
+                            pre_nxt[cand] = s;
+                            cand = -1;
+                        } else {
+                            ++seg;
+                        }
+                    } else if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
                         my_dims += static_cast<unsigned long long>(sg.col + sg.len);
                         cand = -1;
                     } else if (seg == a.nseg - 1) {  // d == D (dco.hpp:145; ivf.cpp:335-338)
@@ -406,6 +457,7 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                         sh.r_sq = rsq;
                     }
                 }
+                if (lane == 0) sh.pcount[(j & 1) ^ 1] = can_pre ? min(sh.pnext, nhi - hi) : 0;
             }
             __syncthreads();
             lo = hi;
@@ -431,8 +483,8 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
 size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
     size_t b = sizeof(float) * a.warps * 1024;
-    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + chunk_cap);
-    b += sizeof(int64_t) * a.nprobe + sizeof(int32_t) * ((chunk_cap + 1) & ~1);
+    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + 3 * chunk_cap);
+    b += sizeof(int32_t) * (a.nprobe + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + chunk_cap + a.nprobe + 1);
     b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
