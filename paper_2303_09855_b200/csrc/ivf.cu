@@ -234,9 +234,210 @@ __device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double 
 struct SearchShared {
     double r, r_sq;
     int q, stop, total, next, cnt, pnext;
+    int wc[64];  // per-(round, warp) counts of the CTA-wide merge compaction
     int pcount[2];
     unsigned long long dims;
 };
+
+// The same rank merge with every thread of the CTA, for chunks with many
+// positives (r still loose early in a query).  Kept positives are compacted
+// in candidate order to pend_d/pend_i[0, m) first.  Returns m on success,
+// -(m + 1) on a tie (the compacted batch is then offered sequentially).
+// Needs n <= 2 * blockDim.x and sh.cnt <= 2 * blockDim.x; call with all threads.
+__device__ __noinline__ int cta_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, int K, double* pend_d,
+                               int32_t* pend_i, const unsigned* pflag, int n) {
+    const int tid = threadIdx.x, nthr = blockDim.x, nwarps = nthr >> 5, warp = tid >> 5;
+    const unsigned lane = lane_id();
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int c = sh.cnt;
+    const bool full = c == K;
+    const double maxd = full ? topd[K - 1] : kInf;
+    double d[2];
+    int32_t id[2];
+    bool keep[2];
+    unsigned kb[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int slot = r * nthr + tid;
+        keep[r] = slot < n && ((pflag[slot >> 5] >> (slot & 31)) & 1u);
+        d[r] = 0.0;
+        id[r] = 0;
+        if (keep[r]) {
+            d[r] = pend_d[slot];
+            id[r] = pend_i[slot];
+            keep[r] = !full || d[r] < maxd;  // the max only decreases
+        }
+        kb[r] = __ballot_sync(kFull, keep[r]);
+        if (lane == 0) sh.wc[r * nwarps + warp] = __popc(kb[r]);
+    }
+    __syncthreads();
+    int m = 0, off[2] = {0, 0};
+    for (int e = 0; e < 2 * nwarps; ++e) {
+        const int v = sh.wc[e];
+        if (e < warp) off[0] += v;
+        if (e < nwarps + warp) off[1] += v;
+        m += v;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (keep[r]) {
+            const int k = off[r] + __popc(kb[r] & lt_mask);
+            pend_d[k] = d[r];
+            pend_i[k] = id[r];
+        }
+    }
+    __syncthreads();
+    bool tie = false;
+    int bnew[2] = {-1, -1}, snew[2] = {-1, -1};
+    double sd[2] = {0.0, 0.0};
+    int32_t si[2] = {0, 0};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int kk = r * nthr + tid;
+        if (kk < m) {  // batch entry: rank in the batch + rank in the top-K
+            d[r] = pend_d[kk];
+            id[r] = pend_i[kk];
+            int less = 0;
+            for (int k = 0; k < m; ++k) {
+                const double od = pend_d[k];
+                less += pair_lt(od, pend_i[k], d[r], id[r]);
+                tie |= od == d[r] && k != kk;
+            }
+            int lo = 0, hi = c;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (pair_lt(topd[mid], topi[mid], d[r], id[r])) lo = mid + 1;
+                else hi = mid;
+            }
+            bnew[r] = lo + less;
+        }
+        const int i = r * nthr + tid;
+        if (i < c) {  // top-K entry: index + batch entries below it
+            sd[r] = topd[i];
+            si[r] = topi[i];
+            int below = 0;
+            for (int k = 0; k < m; ++k) {
+                const double od = pend_d[k];
+                below += pair_lt(od, pend_i[k], sd[r], si[r]);
+                tie |= od == sd[r];
+            }
+            snew[r] = i + below;
+        }
+    }
+    if (__syncthreads_or(tie)) return -(m + 1);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (snew[r] >= 0 && snew[r] < K) {
+            topd[snew[r]] = sd[r];
+            topi[snew[r]] = si[r];
+        }
+        if (bnew[r] >= 0 && bnew[r] < K) {
+            topd[bnew[r]] = d[r];
+            topi[bnew[r]] = id[r];
+        }
+    }
+    if (tid == 0) sh.cnt = c + m < K ? c + m : K;
+    __syncthreads();
+    return m;
+}
+
+// Offers a chunk's positives (pflag bits over pend_d/pend_i, candidate order)
+// to the sorted top-K in one pass of one warp.  When no positive's distance
+// equals another distance of the top-K or the batch, the sequential offers of
+// ivf.cpp:273-280 (insert iff dist < max when full, strictly; pop the max
+// (dist, id) pair) leave exactly the K smallest pairs of top-K ∪ batch, so
+// every entry moves to its rank in the union.  Returns false, with nothing
+// changed, on a tie or more than 32 surviving positives (sequential path).
+__device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, int K, const double* pend_d,
+                                 const int32_t* pend_i, const unsigned* pflag, int n) {
+    const unsigned lane = lane_id();
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int c = sh.cnt;
+    const bool full = c == K;
+    const double maxd = full ? topd[K - 1] : kInf;
+    // batch: up to 32 kept positives, lane t holds the t-th in candidate order
+    double bd = 0.0;
+    int32_t bi = 0;
+    int m = 0;
+    for (int w = 0; w < ((n + 31) >> 5); ++w) {
+        const unsigned bits = pflag[w];
+        if (!bits) continue;
+        double d = 0.0;
+        int32_t id = 0;
+        bool keep = false;
+        if ((bits >> lane) & 1u) {
+            d = pend_d[w * 32 + lane];
+            id = pend_i[w * 32 + lane];
+            keep = !full || d < maxd;  // the max only decreases: rejected whatever comes first
+        }
+        const unsigned kb = __ballot_sync(kFull, keep);
+        if (!kb) continue;
+        const int tot = m + __popc(kb);
+        if (tot > 32) return false;
+        const int t = static_cast<int>(lane) - m;
+        const int src = (t >= 0 && t < tot - m) ? static_cast<int>(__fns(kb, 0, t + 1)) : 0;
+        const double dd = __shfl_sync(kFull, d, src);
+        const int32_t ii = __shfl_sync(kFull, id, src);
+        if (t >= 0 && t < tot - m) {
+            bd = dd;
+            bi = ii;
+        }
+        m = tot;
+    }
+    if (m == 0) return true;
+    const bool mine = static_cast<int>(lane) < m;
+    int rb = 0;  // batch entries below mine
+    bool tie = false;
+    for (int k = 0; k < m; ++k) {
+        const double od = __shfl_sync(kFull, bd, k);
+        const int32_t oi = __shfl_sync(kFull, bi, k);
+        if (mine && k != static_cast<int>(lane)) {
+            rb += pair_lt(od, oi, bd, bi);
+            tie |= od == bd;
+        }
+    }
+    int rs = 0;  // top-K entries below mine
+    if (mine) {
+        int lo = 0, hi = c;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (pair_lt(topd[mid], topi[mid], bd, bi)) lo = mid + 1;
+            else hi = mid;
+        }
+        tie |= (lo > 0 && topd[lo - 1] == bd) || (lo < c && topd[lo] == bd);
+        rs = lo;
+    }
+    if (__any_sync(kFull, tie)) return false;
+    // top-K entries only move up: move 32-entry groups from the top down
+    for (int g = (c - 1) >> 5; g >= 0; --g) {
+        const int i = g * 32 + static_cast<int>(lane);
+        double sd = 0.0;
+        int32_t si = 0;
+        int below = 0;
+        if (i < c) {
+            sd = topd[i];
+            si = topi[i];
+        }
+        for (int k = 0; k < m; ++k) {
+            const double od = __shfl_sync(kFull, bd, k);
+            const int32_t oi = __shfl_sync(kFull, bi, k);
+            below += pair_lt(od, oi, sd, si);
+        }
+        __syncwarp();
+        if (i < c && i + below < K) {
+            topd[i + below] = sd;
+            topi[i + below] = si;
+        }
+        __syncwarp();
+    }
+    if (mine && rs + rb < K) {
+        topd[rs + rb] = bd;
+        topi[rs + rb] = bi;
+    }
+    if (lane == 0) sh.cnt = c + m < K ? c + m : K;
+    __syncwarp();
+    return true;
+}
 
 template <int VEC, bool FULL>
 __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
@@ -437,8 +638,22 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 }
             }
             __syncthreads();
-            if (warp == 0) {  // offer the chunk's positives in candidate order
-                const int nw = (hi - lo + 31) / 32;
+            // offer the chunk's positives in candidate order: few -> one warp,
+            // many -> the whole CTA, ties or oversize -> one by one
+            const int n = hi - lo;
+            int npos = 0;
+            for (int w = 0; w < (n + 31) >> 5; ++w) npos += __popc(pflag[w]);
+            int seq = -1;  // >= 0: offer pend[0, seq) sequentially (compacted batch)
+            if (npos > 32 && n <= 2 * static_cast<int>(blockDim.x) && sh.cnt <= 2 * static_cast<int>(blockDim.x)) {
+                const int rc = cta_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n);
+                if (rc < 0) seq = -rc - 1;
+                npos = 0;
+            }
+            if (warp == 0) {
+                bool merged = npos == 0;
+                if (!merged && npos <= 32) merged = warp_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n);
+                for (int k = 0; k < seq; ++k) warp_offer(topd, topi, &sh.cnt, a.K, pend_d[k], pend_i[k]);
+                const int nw = merged ? 0 : (n + 31) / 32;
                 for (int w = 0; w < nw; ++w) {
                     unsigned bits = pflag[w];
                     while (bits) {

@@ -164,6 +164,28 @@ def test_ivf_batched_schedule_bitexact(eng, orc, first, step):
             assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, 32, f, step)
 
 
+@pytest.mark.parametrize("K,first,step", [(10, 0, 256), (10, 1, 1), (25, 0, 16), (7, 3, 5)])
+def test_ivf_duplicate_vectors_ties(eng, orc, K, first, step):
+    """Exact duplicates (equal distances, distinct ids) drive the top-K's tie
+    rules (strict '<' at the max, (dist, id) pop order) through both the
+    CTA-wide rank merge and its sequential fallback."""
+    raw, t, qr, qt, P = make_fixture(orc, 1200, 64, 8, 30, 401)
+    rng = np.random.default_rng(402)
+    src = rng.integers(0, 1200, 1800)
+    raw = np.concatenate([raw, raw[src], raw[src[:300]]]).astype(np.float32)  # 1-3 copies
+    t = orc.apply_dataset(P, raw)
+    qr = np.concatenate([qr, raw[src[:10]]]).astype(np.float32)  # queries on duplicated points
+    qt = orc.apply_dataset(P, qr)
+    lay = oracle_index(orc, raw, t, P, 24, 403, d1=32)
+    idx = gpu_index(eng, lay, P)
+    for mode in ("ad-split", "fd", "pd"):
+        for nprobe in (2, 9, 24):
+            res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]),
+                                      eng.DcoConfig(), first=first, step=step)
+            f = first if first > 0 else K
+            assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, 32, f, step)
+
+
 def test_ivf_rotation_on_device(eng, orc):
     """Q_t omitted -> queries rotated on the GPU with P; identical results."""
     raw, t, qr, qt, P = make_fixture(orc, 2000, 64, 16, 30, 7)
