@@ -252,9 +252,10 @@ def run_search(args, D: Dist):
                                         C.c_void_p(d_dims.ptr), C.c_void_p(d_cand.ptr)))
 
     if args.tune and D.rank == 0:
-        for st_, w_, g_, sch, qg, qo in ((256, 4, 64, 0, 1, 0), (256, 4, 64, 0, 1, 1),
-                                         (128, 4, 64, 0, 1, 1), (512, 4, 64, 0, 1, 1),
-                                         (256, 8, 64, 0, 1, 1), (16, 16, 64, 1, 16, 1)):
+        for st_, w_, g_, sch, qg, qo in ((256, 4, 64, 0, 1, 0), (128, 4, 64, 0, 1, 0),
+                                         (192, 4, 64, 0, 1, 0), (384, 4, 64, 0, 1, 0),
+                                         (512, 4, 64, 0, 1, 0), (256, 8, 64, 0, 1, 0),
+                                         (512, 8, 64, 0, 1, 0), (256, 2, 64, 0, 1, 0)):
             if True:
                 o2 = ads.search_opts(first=1 if sch else 0, step=st_, warps_per_cta=w_, tile=g_,
                                      scheduler=sch, queries_per_cta=qg, time_stages=True,

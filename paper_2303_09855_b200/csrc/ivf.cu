@@ -351,7 +351,6 @@ __device__ __noinline__ int cta_merge_chunk(double* topd, int32_t* topi, SearchS
 __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, int K, const double* pend_d,
                                  const int32_t* pend_i, const unsigned* pflag, int n) {
     const unsigned lane = lane_id();
-    const unsigned lt_mask = (1u << lane) - 1u;
     const int c = sh.cnt;
     const bool full = c == K;
     const double maxd = full ? topd[K - 1] : kInf;
