@@ -150,6 +150,18 @@ int ads_dco(ads_ctx *ctx, int32_t kind, const float *o, int32_t n_o, const float
             double r, double epsilon0, int32_t delta_d, int32_t *positive, double *distance,
             double *observed, int32_t *dims_used);
 
+/* ------------------------------------------------------------------ verify_theory
+ * The fixed-threshold study of bench.cpp:303-392 (bench.hpp:90-99): for every
+ * query, r_sq = the exact K-th smallest squared distance over all n rows;
+ * every (query, row) pair gets a delta_d = 1 adaptive comparison per grid
+ * epsilon0.  Rows come back sorted by epsilon0 (ascending):
+ * failure_rate = failures / positives, avg_dims = dims / (nq * n).  Any
+ * output pointer may be NULL.  Xt / Qt are transformed host arrays. */
+int ads_verify_theory(ads_ctx *ctx, const float *Xt, int64_t n, int32_t d, const float *Qt,
+                      int32_t nq, int32_t K, const double *grid, int32_t G, double *eps_sorted,
+                      double *failure_rate, double *avg_dims, uint64_t *failures,
+                      uint64_t *positives);
+
 /* ------------------------------------------------------------------ exact k-NN
  * brute_force_knn, bench.hpp:34 / bench.cpp:31-61: the K smallest (d2, id) pairs. */
 int ads_brute_force_knn(ads_ctx *ctx, const float *base, int64_t n, int32_t d,

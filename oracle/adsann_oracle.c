@@ -508,6 +508,7 @@ int orc_ivf_layout(int32_t n, int32_t d, int32_t k, int32_t d1, int split, const
                    float *vec_raw, float *a1_t, float *a2_t, float *a1_raw, float *a2_raw,
                    float *centroids_raw) {
     if (split && (d1 < 1 || d1 >= d)) return fail(1, "build_ivf: split layout needs 1 <= d1 < D");
+    if (k < 1) return fail(1, "layout: k must be >= 1");
     for (int32_t c = 0; c <= k; ++c) list_off[c] = 0;
     for (int32_t i = 0; i < n; ++i) {
         if (assignment[i] < 0 || assignment[i] >= k) return fail(1, "layout: bad assignment");
@@ -728,5 +729,75 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
     free(pending);
     free(prefix);
     free(mark);
+    return 0;
+}
+
+/* bench.cpp:303-392 verify_theory: every (query, object) pair gets one
+ * adaptive comparison with delta_d = 1 against the exact K-th nearest
+ * squared distance r_sq of that query; reject_at[g] = the first d in [1, D)
+ * with s_d > factor_g[d] * r_sq (the grid sorted ascending; a larger
+ * epsilon0 never rejects earlier).  dims adds reject_at or D; a failure is
+ * a positive (d2 <= r_sq) object that some epsilon0 rejects.  Outputs per
+ * sorted grid entry: eps_sorted, dims (sum), failures; plus positives. */
+static int cmp_double(const void *a, const void *b) {
+    const double x = *(const double *)a, y = *(const double *)b;
+    return (x > y) - (x < y);
+}
+
+int orc_verify_theory(const float *X, int32_t n, int32_t d, const float *Q, int32_t nq, int32_t K,
+                      const double *grid, int32_t G, double *eps_sorted, uint64_t *dims,
+                      uint64_t *failures, uint64_t *positives) {
+    if (K < 1 || K > n) return fail(1, "verify_theory: bad K");
+    for (int32_t g = 0; g < G; ++g) eps_sorted[g] = grid[g];
+    qsort(eps_sorted, (size_t)G, sizeof(double), cmp_double);
+    double *factor = malloc(sizeof(double) * (size_t)G * (size_t)(d > 0 ? d : 1));
+    for (int32_t g = 0; g < G; ++g) {
+        const int rc = orc_ad_context(eps_sorted[g], 1, d, factor + (size_t)g * d);
+        if (rc) {
+            free(factor);
+            return rc;
+        }
+        dims[g] = 0;
+        failures[g] = 0;
+    }
+    *positives = 0;
+    double *dist_sq = malloc(sizeof(double) * (size_t)n);
+    double *kth = malloc(sizeof(double) * (size_t)n);
+    int32_t *reject_at = malloc(sizeof(int32_t) * (size_t)(G > 0 ? G : 1));
+    for (int32_t qi = 0; qi < nq; ++qi) {
+        const float *q = Q + (size_t)qi * d;
+        for (int32_t i = 0; i < n; ++i) dist_sq[i] = orc_l2_sq(X + (size_t)i * d, q, d);
+        memcpy(kth, dist_sq, sizeof(double) * (size_t)n);
+        qsort(kth, (size_t)n, sizeof(double), cmp_double);
+        const double r_sq = kth[K - 1];
+        for (int32_t i = 0; i < n; ++i) {
+            const int positive = dist_sq[i] <= r_sq;
+            if (positive) ++*positives;
+            const float *o = X + (size_t)i * d;
+            double s = 0.0;
+            int32_t first_active = 0;
+            for (int32_t g = 0; g < G; ++g) reject_at[g] = 0;
+            for (int32_t dd = 1; dd < d && first_active < G; ++dd) {
+                const double a = (double)o[dd - 1] - (double)q[dd - 1];
+                s += a * a;
+                while (first_active < G && s > factor[(size_t)first_active * d + dd] * r_sq) {
+                    reject_at[first_active] = dd;
+                    ++first_active;
+                }
+            }
+            for (int32_t g = 0; g < G; ++g) {
+                if (reject_at[g] > 0) {
+                    dims[g] += (uint64_t)reject_at[g];
+                    if (positive) ++failures[g];
+                } else {
+                    dims[g] += (uint64_t)d;
+                }
+            }
+        }
+    }
+    free(factor);
+    free(dist_sq);
+    free(kth);
+    free(reject_at);
     return 0;
 }

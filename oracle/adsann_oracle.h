@@ -120,6 +120,14 @@ int orc_ivf_query_waves(const orc_ivf *idx, const float *q_t, const float *q_raw
 int orc_probe_order(const float *centroids, int32_t L, int32_t d, const float *q,
                     int32_t nprobe, int32_t *order);
 
+
+/* bench.cpp:303-392 fixed-threshold study (delta_d = 1, r_sq = exact K-th
+ * nearest squared distance); per ascending grid entry: summed dims and
+ * failures; positives counts objects with d2 <= r_sq over all queries. */
+int orc_verify_theory(const float *X, int32_t n, int32_t d, const float *Q, int32_t nq, int32_t K,
+                      const double *grid, int32_t G, double *eps_sorted, uint64_t *dims,
+                      uint64_t *failures, uint64_t *positives);
+
 #ifdef __cplusplus
 }
 #endif

@@ -194,6 +194,9 @@ class Oracle(_Common):
                                    C.c_int32, C.c_int64, C.c_int64, _i32p, _f64p,
                                    C.POINTER(C.c_int32), _u64p])
         self._fn("orc_probe_order", [_f32p, C.c_int32, C.c_int32, _f32p, C.c_int32, _i32p])
+        self._fn("orc_verify_theory", [_f32p, C.c_int32, C.c_int32, _f32p, C.c_int32, C.c_int32,
+                                       _f64p, C.c_int32, _f64p, _u64p, _u64p,
+                                       C.POINTER(C.c_uint64)])
         self._fn("orc_ivf_query_waves", [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int, C.c_double,
                                          C.c_int32, _i32p, C.c_int32, _i32p, _f64p,
                                          C.POINTER(C.c_int32), _u64p])
@@ -254,6 +257,23 @@ class Oracle(_Common):
             self._check(self._ivf_query(C.addressof(s), _nullable(qt), _nullable(qr), K, nprobe, m,
                                         eps0, delta_d, first, step, ids, dists, C.byref(cnt), stats))
         return ids[:cnt.value].copy(), dists[:cnt.value].copy(), stats
+
+    def verify_theory(self, X, Q, K, grid):
+        """bench.cpp:303-392 -> (eps sorted, failure_rate, avg_dims, failures, positives),
+        the ratios formed exactly as the reference forms them."""
+        X = _f32(X)
+        Q = _f32(Q)
+        G = len(grid)
+        eps = np.empty(G)
+        dims, fails = np.empty(G, np.uint64), np.empty(G, np.uint64)
+        pos = C.c_uint64()
+        self._check(self._verify_theory(X, X.shape[0], X.shape[1], Q, Q.shape[0], K,
+                                        _f64(list(grid)), G, eps, dims, fails, C.byref(pos)))
+        p = int(pos.value)
+        total = float(Q.shape[0]) * float(X.shape[0])
+        fr = np.array([float(f) / p if p > 0 else 0.0 for f in fails])
+        ad = np.array([float(x) / total for x in dims])
+        return eps, fr, ad, fails, np.full(G, p, np.uint64)
 
     def probe_order(self, centroids, q, nprobe):
         centroids = _f32(centroids)

@@ -93,6 +93,7 @@ ads_dco_fixed = _sig("ads_dco_fixed", [vp, C.POINTER(DcoBatch)])
 ads_dco_fixed_device = _sig("ads_dco_fixed_device", [vp, C.POINTER(DcoBatch)])
 ads_dco = _sig("ads_dco", [vp, i32, vp, i32, vp, i32, f64, f64, i32, pi32, pf64, pf64, pi32])
 ads_brute_force_knn = _sig("ads_brute_force_knn", [vp, vp, i64, i32, vp, i32, i32, vp])
+ads_verify_theory = _sig("ads_verify_theory", [vp, vp, i64, i32, vp, i32, i32, vp, i32, vp, vp, vp, vp, vp])
 ads_brute_force_knn_device = _sig("ads_brute_force_knn_device", [vp, vp, i64, i32, vp, i32, i32, vp])
 ads_kmeans = _sig("ads_kmeans", [vp, vp, i64, i32, i32, i32, u64, i32, vp, vp, pf64, pi32])
 ads_ivf_create = _sig("ads_ivf_create", [vp, C.POINTER(IvfDesc), C.POINTER(vp)])

@@ -14,7 +14,7 @@ import enum
 import math
 import threading
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import NamedTuple, Optional, Sequence
 
 import numpy as np
 
@@ -422,6 +422,35 @@ def brute_force_knn(ds: np.ndarray, queries: np.ndarray, K: int,
     check(L.ads_brute_force_knn(ctx.h, ds.ctypes.data, ds.shape[0], ds.shape[1],
                                 queries.ctypes.data, queries.shape[0], K, ids.ctypes.data))
     return ids
+
+
+class TheoryRow(NamedTuple):  # bench.hpp:90-96
+    epsilon0: float
+    failure_rate: float
+    avg_dims: float
+    failures: int
+    positives: int
+
+
+def verify_theory(ds_t: np.ndarray, queries_t: np.ndarray, K: int, epsilon0_grid,
+                  ctx: Optional[Context] = None) -> list:
+    """bench.cpp:303-392 on the GPU: one delta_d = 1 comparison per (query, object)
+    per epsilon0 against the exact K-th neighbour distance; rows sorted by epsilon0."""
+    ctx = ctx or Context.default()
+    ds_t = _f32(ds_t)
+    queries_t = _f32(queries_t)
+    if ds_t.shape[1] != queries_t.shape[1]:
+        raise ValueError("verify_theory: dimensionality mismatch")
+    grid = np.ascontiguousarray(list(epsilon0_grid), np.float64)
+    G = len(grid)
+    eps, fr, ad = np.empty(max(G, 1)), np.empty(max(G, 1)), np.empty(max(G, 1))
+    fails, pos = np.empty(max(G, 1), np.uint64), np.empty(max(G, 1), np.uint64)
+    check(L.ads_verify_theory(ctx.h, ds_t.ctypes.data, ds_t.shape[0], ds_t.shape[1],
+                              queries_t.ctypes.data, queries_t.shape[0], K, grid.ctypes.data, G,
+                              eps.ctypes.data, fr.ctypes.data, ad.ctypes.data, fails.ctypes.data,
+                              pos.ctypes.data))
+    return [TheoryRow(float(eps[g]), float(fr[g]), float(ad[g]), int(fails[g]), int(pos[g]))
+            for g in range(G)]
 
 
 def recall(result_ids, gt_ids, K: int) -> float:  # bench.cpp:63-72 (set arithmetic)

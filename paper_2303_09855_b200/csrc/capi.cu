@@ -660,6 +660,50 @@ int ads_brute_force_knn(ads_ctx* ctx, const float* base, int64_t n, int32_t d,
     });
 }
 
+// ------------------------------------------------------------------ verify_theory
+int ads_verify_theory(ads_ctx* ctx, const float* Xt, int64_t n, int32_t d, const float* Qt, int32_t nq,
+                      int32_t K, const double* grid, int32_t G, double* eps_sorted, double* failure_rate,
+                      double* avg_dims, uint64_t* failures, uint64_t* positives) {
+    return guard([&] {
+        // bench.cpp:305-307
+        require(d >= 1, "verify_theory: dimensionality mismatch");
+        require(K >= 1 && K <= n, "verify_theory: bad K");
+        require(G >= 0, "verify_theory: bad grid");
+        std::vector<double> eps(grid, grid + G);
+        std::sort(eps.begin(), eps.end());
+        std::vector<double> factor(static_cast<size_t>(G) * d);
+        for (int g = 0; g < G; ++g) {  // AdContext(DcoConfig{eps, 1}, dim) (bench.cpp:316)
+            const std::vector<double> f = ad_factor(eps[g], 1, d);
+            std::copy(f.begin(), f.end(), factor.begin() + static_cast<size_t>(g) * d);
+        }
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        DevBuf dx, dq, df, dids, dr, dc;
+        float* xp = dx.get<float>(static_cast<size_t>(n) * d);
+        float* qp = dq.get<float>(static_cast<size_t>(nq) * d);
+        double* fp = df.get<double>(factor.size());
+        ADS_CUDA(cudaMemcpyAsync(xp, Xt, sizeof(float) * n * d, cudaMemcpyHostToDevice, st));
+        if (nq) ADS_CUDA(cudaMemcpyAsync(qp, Qt, sizeof(float) * nq * static_cast<size_t>(d), cudaMemcpyHostToDevice, st));
+        if (G) ADS_CUDA(cudaMemcpyAsync(fp, factor.data(), sizeof(double) * factor.size(), cudaMemcpyHostToDevice, st));
+        auto* cnt = dc.get<unsigned long long>(2 * static_cast<size_t>(G) + 1);
+        launch_verify_theory(xp, n, d, qp, nq, K, fp, G, dids.get<int32_t>(static_cast<size_t>(nq) * K),
+                             dr.get<double>(nq), cnt, st);
+        std::vector<unsigned long long> h(2 * static_cast<size_t>(G) + 1);
+        ADS_CUDA(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        // bench.cpp:376-391
+        const uint64_t pos = h[2 * G];
+        const double total = static_cast<double>(nq) * static_cast<double>(n);
+        for (int g = 0; g < G; ++g) {
+            if (eps_sorted) eps_sorted[g] = eps[g];
+            if (failures) failures[g] = h[G + g];
+            if (positives) positives[g] = pos;
+            if (failure_rate) failure_rate[g] = pos > 0 ? static_cast<double>(h[G + g]) / pos : 0.0;
+            if (avg_dims) avg_dims[g] = static_cast<double>(h[g]) / total;
+        }
+    });
+}
+
 // ------------------------------------------------------------------ k-means
 int ads_kmeans(ads_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k, int32_t max_iters,
                uint64_t seed, int32_t init, float* centroids, int32_t* assignment, double* objective,

@@ -191,6 +191,11 @@ void launch_apply(const double* P, int dim, const float* X, int64_t n, float* Y,
 // brute_force_knn: K smallest (d2, id) pairs per query.
 void launch_brute_knn(const float* base, int64_t n, int D, const float* Q, int nq, int K,
                       int32_t* ids, cudaStream_t st);
+// verify_theory (bench.cpp:303-392): counters[0, G) dims, [G, 2G) failures, [2G] positives
+// over the ascending grid whose factor tables (delta_d = 1) are factor[g*d ..]; theory.cu.
+void launch_verify_theory(const float* X, int64_t n, int d, const float* Q, int nq, int K,
+                          const double* factor, int G, int32_t* ids_scratch, double* r_sq,
+                          unsigned long long* counters, cudaStream_t st);
 
 // k-means pieces (kmeans.cu).
 struct KmeansOut {

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <limits>
@@ -584,6 +585,32 @@ GroundTruth brute_force_knn(const Dataset& ds, const Dataset& queries, std::int3
     check(ads_brute_force_knn(engine(), ds.data.data(), ds.n, ds.d, queries.data.data(), queries.n, K,
                               gt.ids.data()));
     return gt;
+}
+
+std::vector<TheoryRow> verify_theory(const Dataset& ds_t, const Dataset& queries_t, std::int32_t K,
+                                     std::vector<double> epsilon0_grid) {
+    if (ds_t.d != queries_t.d) throw std::invalid_argument("verify_theory: dimensionality mismatch");
+    if (K < 1 || K > ds_t.n) throw std::invalid_argument("verify_theory: bad K");
+    const auto G = static_cast<std::int32_t>(epsilon0_grid.size());
+    std::vector<double> eps(G), fr(G), ad(G);
+    std::vector<std::uint64_t> fails(G), pos(G);
+    check(ads_verify_theory(engine(), ds_t.data.data(), ds_t.n, ds_t.d, queries_t.data.data(), queries_t.n, K,
+                            epsilon0_grid.data(), G, eps.data(), fr.data(), ad.data(), fails.data(), pos.data()));
+    std::vector<TheoryRow> rows(G);
+    for (std::int32_t g = 0; g < G; ++g) rows[g] = TheoryRow{eps[g], fr[g], ad[g], fails[g], pos[g]};
+    return rows;
+}
+
+void write_theory_csv(const std::vector<TheoryRow>& rows, const std::filesystem::path& path) {
+    std::ofstream out(path, std::ios::trunc);
+    if (!out) throw std::runtime_error("cannot open " + path.string() + " for writing");
+    out << "epsilon0,failure_rate,avg_dims,failures,positives\n";
+    char line[256];
+    for (const TheoryRow& r : rows) {
+        std::snprintf(line, sizeof(line), "%.3f,%.8f,%.4f,%llu,%llu\n", r.epsilon0, r.failure_rate, r.avg_dims,
+                      static_cast<unsigned long long>(r.failures), static_cast<unsigned long long>(r.positives));
+        out << line;
+    }
 }
 
 double recall(std::span<const std::int32_t> result_ids, std::span<const std::int32_t> gt_ids, std::int32_t K) {

@@ -351,3 +351,27 @@ def test_coarse_prefilter_adversarial_ties(eng, orc):
     b = eng.ivf_query_batch(idx, Q, Q, 5, 13, eng.IvfMode.kAdSplit, opts=eng.search_opts(coarse_mode=1))
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dims, b.dims)
+
+
+@pytest.mark.parametrize("n,d,nq,K,grid", [(1500, 48, 12, 20, [1e6]),
+                                           (2000, 64, 10, 50, [2.5, 0.5, 1.0, 2.0, 1.5, 3.0]),
+                                           (800, 30, 7, 1, [2.1, 2.1, 0.2]),
+                                           (3000, 128, 20, 100, [0.3, 1.0, 2.1, 4.0])])
+def test_verify_theory_bitexact(eng, orc, n, d, nq, K, grid):
+    """verify_theory (bench.cpp:303-392) on the GPU == the oracle: counts exact,
+    ratios bit-identical (formed like the reference)."""
+    _, t, _, qt, _ = make_fixture(orc, n, d, 8, nq, 31 + d)
+    if n == 3000:  # duplicated rows: ties at the K-th distance
+        t = np.concatenate([t, t[:400]]).astype(np.float32)
+    rows = eng.verify_theory(t, qt, K, grid)
+    eps, fr, ad, fails, pos = orc.verify_theory(t, qt, K, grid)
+    assert len(rows) == len(grid)
+    for g, r in enumerate(rows):
+        assert (r.epsilon0, r.failures, r.positives) == (eps[g], int(fails[g]), int(pos[g])), g
+        assert r.failure_rate == fr[g] and r.avg_dims == ad[g], g
+    with pytest.raises(ValueError):
+        eng.verify_theory(t, qt, 0, grid)
+    with pytest.raises(ValueError):
+        eng.verify_theory(t, qt, t.shape[0] + 1, grid)
+    with pytest.raises(ValueError):
+        eng.verify_theory(t, qt, K, [0.0])

@@ -191,3 +191,21 @@ def test_oracle_batched_schedule_semantics(orc):
         np.testing.assert_array_equal(np.sort(c[0]), np.sort(gt[qi]))
         assert int(b[2][0]) >= int(a[2][0]) * 0.95
         assert len(set(a[0]) & set(gt[qi])) <= 10
+
+
+@pytest.mark.parametrize("n,d,nq,K,grid", [(1500, 48, 12, 20, [1e6]),
+                                           (2000, 64, 10, 50, [2.5, 0.5, 1.0, 2.0, 1.5, 3.0]),
+                                           (800, 30, 7, 1, [2.1, 2.1, 0.2])])
+def test_ref_verify_theory(orc, ref, n, d, nq, K, grid):
+    """orc_verify_theory == adsann::verify_theory (bench.cpp:303-392), every field exact."""
+    from helpers import make_fixture
+
+    _, t, _, qt, _ = make_fixture(orc, n, d, 8, nq, 31 + d)
+    a = orc.verify_theory(t, qt, K, grid)
+    b = ref.verify_theory(t, qt, K, grid)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    with pytest.raises(ValueError):
+        orc.verify_theory(t, qt, 0, grid)
+    with pytest.raises(ValueError):
+        orc.verify_theory(t, qt, n + 1, grid)
