@@ -252,23 +252,20 @@ def run_search(args, D: Dist):
                                         C.c_void_p(d_dims.ptr), C.c_void_p(d_cand.ptr)))
 
     if args.tune and D.rank == 0:
-        for st_, w_, g_, sch, qg, qo in ((256, 4, 64, 0, 1, 0), (128, 4, 64, 0, 1, 0),
-                                         (192, 4, 64, 0, 1, 0), (384, 4, 64, 0, 1, 0),
-                                         (512, 4, 64, 0, 1, 0), (256, 8, 64, 0, 1, 0),
-                                         (512, 8, 64, 0, 1, 0), (256, 2, 64, 0, 1, 0)):
-            if True:
-                o2 = ads.search_opts(first=1 if sch else 0, step=st_, warps_per_cta=w_, tile=g_,
-                                     scheduler=sch, queries_per_cta=qg, time_stages=True,
-                                     query_order=qo)
-                ts, dm = [], 0
-                for rep in range(4):
-                    ctx.flush_l2()
-                    r_ = ads.ivf_query_batch(idx, None, q, K, nprobe, mode, opts=o2)
-                    ts.append(float(idx.last_timings()[3]))
-                    dm = float(r_.dims.mean())
-                scan = float(np.min(ts))
-                log(f"tune sched={sch} order={qo} step={st_} warps={w_} tile={g_} qgroup={qg}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
-                    f"recall {ads.recall_batch(r_.ids, gt, K):.5f}")
+        grid = [(256, 4), (384, 6), (512, 8), (192, 3), (128, 2), (320, 5), (640, 10)]
+        if args.tune_grid:
+            grid = [tuple(int(v) for v in t.split("x")) for t in args.tune_grid.split(",")]
+        for st_, w_ in grid:
+            o2 = ads.search_opts(first=0, step=st_, warps_per_cta=w_, time_stages=True)
+            ts, dm = [], 0
+            for rep in range(4):
+                ctx.flush_l2()
+                r_ = ads.ivf_query_batch(idx, None, q, K, nprobe, mode, opts=o2)
+                ts.append(float(idx.last_timings()[3]))
+                dm = float(r_.dims.mean())
+            scan = float(np.min(ts))
+            log(f"tune step={st_} warps={w_}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
+                f"recall {ads.recall_batch(r_.ids, gt, K):.5f}")
     for _ in range(args.warmup):
         ctx.flush_l2()
         step()
@@ -334,8 +331,9 @@ def run_search(args, D: Dist):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(cfg.describe(), nprobe=nprobe, recall_at_k=recall,
                        parallelism=f"replicas{D.world}" if D.world > 1 else "single-gpu",
-                       l2="flushed between timed steps (and index 512 MB > 126 MB L2)",
-                       threshold_refresh={"first": K, "step": args.step}),
+                       l2=f"flushed between timed steps (and index {cfg.n * d * 4 / 1e6:.0f} MB vs 126 MB L2)",
+                       threshold_refresh={"first": K, "step": ads.search_shape(d, args.step, args.warps)[0]},
+                       warps_per_cta=ads.search_shape(d, args.step, args.warps)[1]),
         "e2e": {"value": world_q / e2e_total, "unit": "queries/s",
                 "h2d_bytes_per_step": nq * d * 4,
                 "d2h_bytes_per_step": nq * K * (4 + 8) + nq * (4 + 8 + 8)},
@@ -568,11 +566,12 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nprobe", type=int, default=0)
     ap.add_argument("--nq", type=int, default=0)
-    ap.add_argument("--step", type=int, default=256, help="threshold refresh interval")
-    ap.add_argument("--warps", type=int, default=4)
+    ap.add_argument("--step", type=int, default=0, help="threshold refresh interval (0: 64 x warps)")
+    ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0: 4 for D <= 256, else 10)")
     ap.add_argument("--slots", type=int, default=4, help="queries served concurrently per CTA")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true", help="time (step, warps) variants after setup")
+    ap.add_argument("--tune-grid", default="", help="comma list of STEPxWARPS for --tune")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--kmeans-init", type=int, default=-1, help="override (profiling runs: 1)")

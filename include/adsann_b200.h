@@ -220,8 +220,8 @@ int ads_ivf_export(ads_ivf *idx, float *centroids_t, float *centroids_raw, int64
  *   step as given); each list is read once per wave for all its queries. */
 typedef struct {
     int64_t first;         /* default K (scheduler 0) / 1 list (scheduler 1) */
-    int64_t step;          /* default 256 candidates (scheduler 0) */
-    int32_t warps_per_cta; /* default 4 */
+    int64_t step;          /* 0 (default): 64 * warps_per_cta candidates (scheduler 0), 1 list (scheduler 1) */
+    int32_t warps_per_cta; /* 0 (default): 4 for D <= 256, else 10 (scheduler 0); 8 (scheduler 1) */
     int32_t queries_per_cta; /* reserved: the query-major kernel serves one query per CTA */
     int32_t ctas_per_sm;   /* 0 = occupancy maximum */
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */

@@ -472,7 +472,14 @@ def recall_batch(ids: np.ndarray, gt: np.ndarray, K: int) -> float:
 # ---------------------------------------------------------------- IVF (GPU)
 
 
-def search_opts(first: int = 0, step: int = 256, warps_per_cta: int = 4, queries_per_cta: int = 1,
+def search_shape(d: int, step: int = 0, warps_per_cta: int = 0) -> tuple:
+    """The (step, warps_per_cta) the engine uses for scheduler 0 at dimension d
+    (0 = auto, as ads_search_opts documents)."""
+    w = warps_per_cta if warps_per_cta > 0 else (4 if d <= 256 else 10)
+    return (step if step > 0 else 64 * w), w
+
+
+def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
                 tile: int = 64, query_order: int = 0, coarse_mode: int = 0) -> L.SearchOpts:
     """scheduler 0: query-major, first/step in candidates; scheduler 1: list-major
@@ -594,8 +601,8 @@ class BatchResult:
 
 
 def ivf_query_batch(idx: IvfIndex, Q_t, Q_raw, K: int, n_probe: int, mode: IvfMode,
-                    cfg: DcoConfig = DcoConfig(), first: int = 0, step: int = 256,
-                    warps_per_cta: int = 4, opts: Optional[L.SearchOpts] = None) -> BatchResult:
+                    cfg: DcoConfig = DcoConfig(), first: int = 0, step: int = 0,
+                    warps_per_cta: int = 0, opts: Optional[L.SearchOpts] = None) -> BatchResult:
     """Batched ivf_query (ivf.hpp:87-89).  first/step set the threshold refresh
     schedule; first=step=1 reproduces the reference's per-candidate refresh."""
     Qt = None if Q_t is None else _f32(np.atleast_2d(Q_t))

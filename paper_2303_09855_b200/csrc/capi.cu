@@ -944,9 +944,9 @@ int ads_ivf_export(ads_ivf* x, float* centroids_t, float* centroids_raw, int64_t
 }
 
 void ads_search_opts_default(ads_search_opts* o) {
-    o->first = 0;  // 0 -> K
-    o->step = 256;
-    o->warps_per_cta = 4;
+    o->first = 0;          // 0 -> K
+    o->step = 0;           // 0 -> 64 * warps_per_cta
+    o->warps_per_cta = 0;  // 0 -> 4 for D <= 256, else 10
     o->queries_per_cta = 4;
     o->ctas_per_sm = 0;
     o->time_stages = 0;
@@ -1010,6 +1010,11 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     ads_search_opts_default(&o);
     if (opts) o = *opts;
     if (o.first <= 0) o.first = K;
+    // auto launch shape: CTAs of 4 warps for D <= 256; wider CTAs amortise the
+    // larger per-query shared state (staged query, chunk slots) at high D.
+    // The refresh interval follows the CTA: 64 candidates per warp.
+    if (o.warps_per_cta <= 0) o.warps_per_cta = o.scheduler == 1 ? 8 : (x->d <= 256 ? 4 : 10);
+    if (o.step <= 0) o.step = o.scheduler == 1 ? 1 : 64 * static_cast<int64_t>(o.warps_per_cta);
     require(o.warps_per_cta >= 1 && o.warps_per_cta <= 32, "search: warps_per_cta in [1, 32]");
     require(o.queries_per_cta >= 1 && o.queries_per_cta <= 16, "search: queries_per_cta in [1, 16]");
     cudaStream_t st = x->ctx->stream;
