@@ -270,6 +270,9 @@ def run_search(args, D: Dist):
         ctx.flush_l2()
         step()
     ctx.sync()
+    cst = idx.coarse_stats()
+    log(f"coarse prefilter: {cst['rescored'] / max(1, cst['queries']):.1f} centroids rescored per query "
+        f"(nprobe {nprobe}), {cst['fallbacks']} exhaustive fallbacks")
     clocks = ClockSampler(dev)
     step_ms, scan_ms, stage_ms = [], [], []
     D.barrier()

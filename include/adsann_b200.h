@@ -230,9 +230,12 @@ typedef struct {
     int32_t query_order;   /* 1: run the batch's queries in an L2-friendly order (by the
                               nearest list's position in a nearest-neighbour chain of centroids);
                               results do not depend on it */
-    int32_t coarse_mode;   /* 0 (default): certified fp32 prefilter + exact fp64 rescoring of the
-                              centroids that can reach the top-nprobe; 1: exact fp64 distance to
-                              every centroid.  Both give probe_order's exact (d2, id) order. */
+    int32_t coarse_mode;   /* 0 (default): certified prefilter — approximate distances from a
+                              tcgen05 TF32 GEMM (fp32 FMA when D % 4 != 0) with a rigorous error
+                              bound — plus exact fp64 rescoring of every centroid that can reach the
+                              top-nprobe; 2: the same with the fp32-FMA GEMM; 1: exact fp64
+                              distance to every centroid.  All give probe_order's exact (d2, id)
+                              order. */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 
@@ -256,6 +259,11 @@ int ads_ivf_probe_order(ads_ivf *idx, const float *Q, int32_t nq, int32_t nprobe
                         int32_t transformed, int32_t *probes);
 /* Stage times (ms) of the last search with opts.time_stages: [rotate, coarse, select, scan]. */
 int ads_ivf_last_timings(ads_ivf *idx, float *ms4);
+
+/* Coarse prefilter counters of the index's last search / probe_order call:
+ * out[0] queries, out[1] centroids rescored exactly (>= queries * nprobe),
+ * out[2] queries that fell back to scoring every centroid exactly. */
+int ads_ivf_coarse_stats(ads_ivf *idx, uint64_t *out);
 
 /* ------------------------------------------------------------------ list sharding (multi-GPU)
  * Shard of an index for one GPU: same k_clusters, centroids and P (probe order is

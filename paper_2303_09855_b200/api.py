@@ -565,6 +565,12 @@ class IvfIndex:
         check(L.ads_ivf_last_timings(self.h, ms.ctypes.data))
         return ms
 
+    def coarse_stats(self) -> dict:
+        """Certified coarse prefilter counters of the last search / probe_order call."""
+        v = np.zeros(3, np.uint64)
+        check(L.ads_ivf_coarse_stats(self.h, v.ctypes.data))
+        return {"queries": int(v[0]), "rescored": int(v[1]), "fallbacks": int(v[2])}
+
 
 def build_ivf(ds_raw: np.ndarray, ds_transformed: np.ndarray, m: TransformMatrix, k_clusters: int,
               seed: int, layout: IvfLayout = IvfLayout.kContiguous, d1: int = 32,

@@ -759,6 +759,10 @@ static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& o
     double* nrm = nullptr;
     ADS_CUDA(cudaMalloc(&nrm, sizeof(double) * k));
     coarse_center(dC, k, D, out.mu, out.cc, out.cn2, nrm, st);
+    if (tc_coarse_supported(D)) {
+        ADS_CUDA(cudaMalloc(&out.cc_tf, sizeof(float) * h.size()));
+        coarse_center(dC, k, D, out.mu, out.cc_tf, out.cn2, nrm, st, true);
+    }
     std::vector<double> hn(static_cast<size_t>(k));
     ADS_CUDA(cudaMemcpyAsync(hn.data(), nrm, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
     ADS_CUDA(cudaStreamSynchronize(st));
@@ -1031,9 +1035,9 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[1], st));
     int32_t* probes = x->probes.get<int32_t>(static_cast<size_t>(nq) * nprobe);
     const float* cent = transformed ? x->cent_t : x->cent_raw;
-    if (o.coarse_mode == 0) {  // certified fp32 prefilter + exact fp64 rescoring (coarse.cu)
+    if (o.coarse_mode == 0 || o.coarse_mode == 2) {  // certified prefilter + exact fp64 rescoring (coarse.cu)
         launch_coarse_probes_fast(Qs, nq, cent, x->k, D, nprobe, transformed ? x->cc_t : x->cc_raw,
-                                  x->coarse, probes, st);
+                                  x->coarse, probes, o.coarse_mode == 2 ? 1 : 0, st);
         if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[2], st));
     } else {  // exact fp64 distance to every centroid, then select
         double* dist = x->dist.get<double>(static_cast<size_t>(nq) * x->k);
@@ -1188,9 +1192,24 @@ int ads_ivf_probe_order(ads_ivf* x, const float* Q, int32_t nq, int32_t nprobe, 
         ADS_CUDA(cudaMemcpyAsync(dq, Q, qn * sizeof(float), cudaMemcpyHostToDevice, st));
         int32_t* dp = x->probes.get<int32_t>(static_cast<size_t>(nq) * nprobe);
         launch_coarse_probes_fast(dq, nq, transformed ? x->cent_t : x->cent_raw, x->k, x->d, nprobe,
-                                  transformed ? x->cc_t : x->cc_raw, x->coarse, dp, st);
+                                  transformed ? x->cc_t : x->cc_raw, x->coarse, dp, 0, st);
         ADS_CUDA(cudaMemcpyAsync(probes, dp, sizeof(int32_t) * nq * nprobe, cudaMemcpyDeviceToHost, st));
         ADS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ads_ivf_coarse_stats(ads_ivf* idx, uint64_t* out) {
+    return guard([&] {
+        idx->ctx->use();
+        std::lock_guard<std::mutex> lk(idx->ctx->mu);
+        unsigned long long h[2] = {0, 0};
+        if (idx->coarse.stats.p) {
+            ADS_CUDA(cudaStreamSynchronize(idx->ctx->stream));
+            ADS_CUDA(cudaMemcpy(h, idx->coarse.stats.p, sizeof(h), cudaMemcpyDeviceToHost));
+        }
+        out[0] = static_cast<uint64_t>(idx->coarse.last_nq);
+        out[1] = h[0];
+        out[2] = h[1];
     });
 }
 

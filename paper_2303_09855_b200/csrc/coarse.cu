@@ -2,7 +2,9 @@
 // (ivf.cpp:283-292: fp64 l2_sq per centroid, partial_sort by (d2, id)) at a
 // fraction of the exact cost.
 //
-//  1. approx_gemm_kernel — fp32 FMA tiles on mean-centred vectors
+//  1. the approximate distance matrix: tcgen05 TF32 tiles (tc_gemm.cu, the
+//     default; its bound is documented there) or approx_gemm_kernel — fp32
+//     FMA tiles on mean-centred vectors
 //     q~ = fl32(q - mu), c~ = fl32(c - mu) (centring in fp64, mu = centroid
 //     mean): a(q,c) = |q~|^2 + |c~|^2 - 2 q~.c~.  Rigorous bound, with
 //     s = |q~| + cmax~ (u = 2^-24, gamma_D = D u / (1 - D u)):
@@ -82,16 +84,24 @@ __global__ void __launch_bounds__(256) approx_gemm_kernel(const float* __restric
 }
 
 // X~ = fl32(X - mu) (fp64 subtraction), |X~|^2 (fp64 -> fp32) and |X~| (fp64).
+// tf32: store X~ rounded to TF32 (cvt.rna) for the tensor-core GEMM; the norms
+// stay those of X~ (tc_gemm.cu's bound accounts for the rounding).
 __global__ void center_norms_kernel(const float* __restrict__ X, int n, int D,
                                     const double* __restrict__ mu, float* __restrict__ Xc,
-                                    float* __restrict__ n2, double* __restrict__ nrm) {
+                                    float* __restrict__ n2, double* __restrict__ nrm, int tf32) {
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const unsigned lane = threadIdx.x & 31u;
     if (i >= n) return;
     double s = 0.0;
     for (int j = static_cast<int>(lane); j < D; j += 32) {
         const float c = static_cast<float>(static_cast<double>(X[static_cast<int64_t>(i) * D + j]) - mu[j]);
-        Xc[static_cast<int64_t>(i) * D + j] = c;
+        float cs = c;
+        if (tf32) {
+            uint32_t r;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(c));
+            cs = __uint_as_float(r);
+        }
+        if (Xc) Xc[static_cast<int64_t>(i) * D + j] = cs;
         const double v = c;
         s += v * v;
     }
@@ -148,7 +158,8 @@ __global__ void __launch_bounds__(kPT) prefilter_kernel(const float* __restrict_
                                                         const float* __restrict__ C, int D, int nprobe,
                                                         const double* __restrict__ qnrm, double cmax,
                                                         double gamma, int cap, int P2,
-                                                        int32_t* __restrict__ probes) {
+                                                        int32_t* __restrict__ probes,
+                                                        unsigned long long* __restrict__ stats) {
     extern __shared__ __align__(16) unsigned char sm[];
     double* cd = reinterpret_cast<double*>(sm);          // P2 exact distances
     double* qd = cd + P2;                                // the query as doubles
@@ -214,6 +225,10 @@ __global__ void __launch_bounds__(kPT) prefilter_kernel(const float* __restrict_
     if (tid == 0 && (q < 6 || n > cap))
         printf("PREFILTER q=%d n=%d cap=%d T=%.9g e=%.6g qn=%.6g cmax=%.6g\n", q, n, cap, (double)T, e, qnrm[q], cmax);
 #endif
+    if (tid == 0) {
+        atomicAdd(&stats[0], static_cast<unsigned long long>(n));
+        if (n > cap) atomicAdd(&stats[1], 1ull);
+    }
     if (n > cap) {  // fallback: exact scoring of every centroid (keep the nprobe best)
         n = L;
         if (tid == 0) s_full = 1;
@@ -273,27 +288,37 @@ __global__ void __launch_bounds__(kPT) prefilter_kernel(const float* __restrict_
 }  // namespace
 
 void coarse_center(const float* X, int n, int D, const double* mu, float* Xc, float* n2, double* nrm,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool tf32) {
     if (n <= 0) return;
-    center_norms_kernel<<<(n + 7) / 8, 256, 0, st>>>(X, n, D, mu, Xc, n2, nrm);
+    center_norms_kernel<<<(n + 7) / 8, 256, 0, st>>>(X, n, D, mu, Xc, n2, nrm, tf32 ? 1 : 0);
     ADS_LAUNCH_CHECK();
 }
 
 void launch_coarse_probes_fast(const float* Q, int nq, const float* C, int L, int D, int nprobe,
-                               const CoarseCentroids& cc, CoarseScratch& s, int32_t* probes,
+                               const CoarseCentroids& cc, CoarseScratch& s, int32_t* probes, int gemm,
                                cudaStream_t st) {
     if (nq <= 0) return;
     float* approx = s.approx.get<float>(static_cast<size_t>(nq) * L);
     float* qc = s.qc.get<float>(static_cast<size_t>(nq) * D);
     float* qn2 = s.qn2.get<float>(nq);
     double* qnrm = s.qnrm.get<double>(nq);
-    coarse_center(Q, nq, D, cc.mu, qc, qn2, qnrm, st);
+    const bool tc = gemm == 0 && tc_coarse_supported(D) && cc.cc_tf;
+    coarse_center(Q, nq, D, cc.mu, qc, qn2, qnrm, st, tc);
     const double cmax = cc.cmax;
-    dim3 grid((L + kGC - 1) / kGC, (nq + kGT - 1) / kGT);
-    approx_gemm_kernel<<<grid, 256, 0, st>>>(qc, nq, cc.cc, L, D, qn2, cc.cn2, approx);
-    ADS_LAUNCH_CHECK();
-    const double u = 0x1.0p-24;
-    const double gamma = (static_cast<double>(D) * u) / (1.0 - static_cast<double>(D) * u) + 4.0 * u;
+    double gamma;
+    if (tc) {  // tcgen05 TF32 (tc_gemm.cu) on TF32-rounded operands
+        launch_tc_coarse_gemm(qc, nq, cc.cc_tf, L, D, qn2, cc.cn2, approx, st);
+        gamma = tc_coarse_gamma(D);
+    } else {  // fp32 FMA tiles
+        dim3 grid((L + kGC - 1) / kGC, (nq + kGT - 1) / kGT);
+        approx_gemm_kernel<<<grid, 256, 0, st>>>(qc, nq, cc.cc, L, D, qn2, cc.cn2, approx);
+        ADS_LAUNCH_CHECK();
+        const double u = 0x1.0p-24;
+        gamma = (static_cast<double>(D) * u) / (1.0 - static_cast<double>(D) * u) + 4.0 * u;
+    }
+    unsigned long long* stats = s.stats.get<unsigned long long>(2);
+    ADS_CUDA(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st));
+    s.last_nq = nq;
     if (nprobe > 2 * kPT) throw std::invalid_argument("coarse prefilter: nprobe > 512 (use coarse_mode 1)");
     int cap = 4 * nprobe + 256;
     if (cap > L) cap = L;
@@ -303,7 +328,8 @@ void launch_coarse_probes_fast(const float* Q, int nq, const float* C, int L, in
     if (smem > 200 * 1024) throw std::invalid_argument("coarse: nprobe too large for the prefilter");
     ADS_CUDA(cudaFuncSetAttribute(prefilter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    prefilter_kernel<<<nq, kPT, smem, st>>>(approx, L, Q, C, D, nprobe, qnrm, cmax, gamma, cap, P2, probes);
+    prefilter_kernel<<<nq, kPT, smem, st>>>(approx, L, Q, C, D, nprobe, qnrm, cmax, gamma, cap, P2, probes,
+                                            stats);
     ADS_LAUNCH_CHECK();
 }
 

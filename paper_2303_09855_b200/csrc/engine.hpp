@@ -157,25 +157,36 @@ size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int qgr
 // Certified coarse quantizer (coarse.cu): fp32 prefilter + exact fp64 rescoring.
 struct CoarseScratch {
     DevBuf approx, qc, qn2, qnrm;
+    DevBuf stats;     // [rescored centroids, fallback queries] of the last launch
+    int last_nq = 0;
 };
 // Per centroid table: mean mu (fp64), centred fp32 copy, |c~|^2 and max |c~|.
 struct CoarseCentroids {
     double* mu = nullptr;
-    float* cc = nullptr;
+    float* cc = nullptr;     // fl32(c - mu)
+    float* cc_tf = nullptr;  // the same rounded to TF32 (tensor-core GEMM operand)
     float* cn2 = nullptr;
     double cmax = 0.0;
     void release() {
-        for (void* p : {static_cast<void*>(mu), static_cast<void*>(cc), static_cast<void*>(cn2)})
+        for (void* p : {static_cast<void*>(mu), static_cast<void*>(cc), static_cast<void*>(cc_tf),
+                        static_cast<void*>(cn2)})
             if (p) cudaFree(p);
         mu = nullptr;
         cc = nullptr;
+        cc_tf = nullptr;
         cn2 = nullptr;
     }
 };
 void coarse_center(const float* X, int n, int D, const double* mu, float* Xc, float* n2, double* nrm,
-                   cudaStream_t st);
+                   cudaStream_t st, bool tf32 = false);
+// tc_gemm.cu: the approximate distance matrix on tcgen05 (kind::tf32) and its error factor.
+bool tc_coarse_supported(int D);
+double tc_coarse_gamma(int D);
+void launch_tc_coarse_gemm(const float* Qc, int nq, const float* Cc, int L, int D, const float* qn2,
+                           const float* cn2, float* out, cudaStream_t st);
+// gemm: 0 = tensor cores when supported (D % 4 == 0), 1 = fp32 FMA on the CUDA cores.
 void launch_coarse_probes_fast(const float* Q, int nq, const float* C, int L, int D, int nprobe,
-                               const CoarseCentroids& cc, CoarseScratch& s, int32_t* probes,
+                               const CoarseCentroids& cc, CoarseScratch& s, int32_t* probes, int gemm,
                                cudaStream_t st);
 
 // Exact fp64 centroid distances (nq x L, l2_sq order) and top-nprobe by (d2, id).

@@ -353,6 +353,32 @@ def test_coarse_prefilter_adversarial_ties(eng, orc):
     np.testing.assert_array_equal(a.dims, b.dims)
 
 
+@pytest.mark.parametrize("d,L,nprobe", [(128, 512, 16), (96, 300, 64), (960, 256, 32), (30, 200, 8)])
+def test_coarse_prefilter_gemm_paths(eng, orc, d, L, nprobe):
+    """The tcgen05 TF32 prefilter (default; fp32 FMA when d % 4 != 0), the fp32-FMA
+    prefilter (coarse_mode 2) and exact scoring (coarse_mode 1) give the same probes;
+    the certified window stays tight (a wrong GEMM would show up here as many
+    rescored centroids or fallbacks, which the exact fallback would otherwise hide)."""
+    raw, t, qr, qt, P = make_fixture(orc, 6 * L, d, 64, 300, 5 + d, center_scale=3.0)
+    lay = oracle_index(orc, raw, t, P, L, 7, d1=32 if d > 32 else 16, iters=4)
+    idx = gpu_index(eng, lay, P)
+    res = {}
+    for mode in (0, 2, 1):
+        r = eng.ivf_query_batch(idx, qt, qr, 10, nprobe, eng.IvfMode.kAdSplit,
+                                eng.DcoConfig(2.1, min(32, d)), opts=eng.search_opts(coarse_mode=mode))
+        res[mode] = r
+        if mode != 1:
+            st = idx.coarse_stats()
+            assert st["queries"] == qt.shape[0] and st["fallbacks"] == 0, (mode, st)
+            assert st["rescored"] <= qt.shape[0] * (3 * nprobe + 16), (mode, st)
+    for mode in (0, 2):
+        np.testing.assert_array_equal(res[mode].ids, res[1].ids)
+        np.testing.assert_array_equal(res[mode].dims, res[1].dims)
+    got = idx.probe_order(qt, nprobe)
+    for qi in range(0, qt.shape[0], 37):
+        np.testing.assert_array_equal(got[qi], orc.probe_order(lay["centroids_t"], qt[qi], nprobe))
+
+
 @pytest.mark.parametrize("n,d,nq,K,grid", [(1500, 48, 12, 20, [1e6]),
                                            (2000, 64, 10, 50, [2.5, 0.5, 1.0, 2.0, 1.5, 3.0]),
                                            (800, 30, 7, 1, [2.1, 2.1, 0.2]),
