@@ -565,7 +565,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="search", choices=["search", "dco"])
+    ap.add_argument("--mode", default="search", choices=["search", "dco", "transform"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nprobe", type=int, default=0)
     ap.add_argument("--nq", type=int, default=0)
@@ -596,6 +596,10 @@ def main():
             from bench_dco import run_dco
 
             res = run_dco(args, D)
+        elif args.mode == "transform":
+            from bench_transform import run_transform
+
+            res = run_transform(args, D)
         elif sharded and (D.world > 1 or args.force_shard):
             res = run_search_sharded(args, D)
         else:

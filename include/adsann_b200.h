@@ -111,6 +111,13 @@ int ads_transform_destroy(ads_transform *t);
 int ads_apply_dataset(ads_transform *t, const float *X, int64_t n, float *Y);
 int ads_apply_dataset_device(ads_transform *t, const float *dX, int64_t n, float *dY);
 int ads_apply_transpose(ads_transform *t, const float *X, int64_t n, float *Y);
+/* The same rotation on the tensor cores (tcgen05 kind::tf32, 3xTF32 split:
+ * X P^T ~= Xh Ph^T + Xh Pl^T + Xl Ph^T, fp32 accumulation): not bit-identical
+ * to apply_dataset's fp64 result (|error| ~1e-7 |x| typical, measured by the
+ * parity tests); dim must be a multiple of 4 and >= 32.  The engine's own search and
+ * build paths keep the exact fp64 transform. */
+int ads_apply_dataset_tc(ads_transform *t, const float *X, int64_t n, float *Y);
+int ads_apply_dataset_tc_device(ads_transform *t, const float *dX, int64_t n, float *dY);
 int ads_apply_transpose_device(ads_transform *t, const float *dX, int64_t n, float *dY);
 
 /* ------------------------------------------------------------------ fixed-threshold DCOs

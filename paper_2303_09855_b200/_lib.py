@@ -87,6 +87,8 @@ ads_transform_create = _sig("ads_transform_create", [vp, vp, i32, C.POINTER(vp)]
 ads_transform_destroy = _sig("ads_transform_destroy", [vp])
 ads_apply_dataset = _sig("ads_apply_dataset", [vp, vp, i64, vp])
 ads_apply_dataset_device = _sig("ads_apply_dataset_device", [vp, vp, i64, vp])
+ads_apply_dataset_tc = _sig("ads_apply_dataset_tc", [vp, vp, i64, vp])
+ads_apply_dataset_tc_device = _sig("ads_apply_dataset_tc_device", [vp, vp, i64, vp])
 ads_apply_transpose = _sig("ads_apply_transpose", [vp, vp, i64, vp])
 ads_apply_transpose_device = _sig("ads_apply_transpose_device", [vp, vp, i64, vp])
 ads_dco_fixed = _sig("ads_dco_fixed", [vp, C.POINTER(DcoBatch)])

@@ -288,6 +288,21 @@ class Transform:
         check(L.ads_apply_transpose(self.h, X.ctypes.data, X.shape[0], Y.ctypes.data))
         return Y
 
+    def apply_dataset_tc(self, X: np.ndarray) -> np.ndarray:
+        """The rotation on the tensor cores (3xTF32); not bit-identical to apply_dataset."""
+        X = _f32(X)
+        if X.ndim != 2 or X.shape[1] != self.m.dim:
+            raise ValueError("apply_dataset: dataset dimension does not match matrix")
+        Y = np.empty_like(X)
+        check(L.ads_apply_dataset_tc(self.h, X.ctypes.data, X.shape[0], Y.ctypes.data))
+        return Y
+
+    def apply_dataset_tc_device(self, dX: "DeviceArray", dY: "DeviceArray") -> None:
+        check(L.ads_apply_dataset_tc_device(self.h, C.c_void_p(dX.ptr), dX.shape[0], C.c_void_p(dY.ptr)))
+
+    def apply_dataset_device(self, dX: "DeviceArray", dY: "DeviceArray") -> None:
+        check(L.ads_apply_dataset_device(self.h, C.c_void_p(dX.ptr), dX.shape[0], C.c_void_p(dY.ptr)))
+
 
 _TCACHE: dict = {}
 
@@ -307,6 +322,11 @@ def apply_dataset(m: TransformMatrix, ds: np.ndarray) -> np.ndarray:  # transfor
     if ds.ndim != 2 or ds.shape[1] != m.dim:
         raise ValueError("apply_dataset: dataset dimension does not match matrix")
     return _transform_for(m).apply_dataset(ds)
+
+
+def apply_dataset_tc(m: TransformMatrix, ds: np.ndarray) -> np.ndarray:
+    """apply_dataset on the tensor cores (tcgen05 3xTF32); fp32-accurate, not bit-exact."""
+    return _transform_for(m).apply_dataset_tc(ds)
 
 
 def apply(m: TransformMatrix, x) -> np.ndarray:  # transform.hpp:48

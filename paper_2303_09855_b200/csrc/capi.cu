@@ -94,6 +94,8 @@ struct ads_transform {
     double* P = nullptr;
     double* PT = nullptr;
     DevBuf xin, yout;
+    DevBuf ph, pl, xh, xl;  // 3xTF32 tensor-core path: P and X as TF32 hi/lo pairs
+    bool split_ready = false;
 };
 
 struct PlanKey {
@@ -360,6 +362,53 @@ static void apply_host(ads_transform* t, const double* M, const float* X, int64_
 
 int ads_apply_dataset(ads_transform* t, const float* X, int64_t n, float* Y) {
     return guard([&] { apply_host(t, t->P, X, n, Y); });
+}
+
+// 3xTF32 tensor-core transform (tc_gemm.cu): dX, dY device arrays of n x dim.
+static void apply_tc(ads_transform* t, const float* dX, int64_t n, float* dY) {
+    require(n >= 0, "apply: n must be >= 0");
+    require(t->dim % 4 == 0 && t->dim >= 32, "apply (tensor cores): dimension must be a multiple of 4 and >= 32");
+    cudaStream_t st = t->ctx->stream;
+    const size_t dd = static_cast<size_t>(t->dim) * t->dim;
+    if (!t->split_ready) {  // P (fp64) -> fp32 -> TF32 hi/lo, once
+        std::vector<double> hp(dd);
+        ADS_CUDA(cudaMemcpyAsync(hp.data(), t->P, sizeof(double) * dd, cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        std::vector<float> pf(hp.begin(), hp.end());
+        float* p32 = t->xin.get<float>(dd);
+        ADS_CUDA(cudaMemcpyAsync(p32, pf.data(), sizeof(float) * dd, cudaMemcpyHostToDevice, st));
+        launch_split_tf32(p32, static_cast<int64_t>(dd), t->ph.get<float>(dd), t->pl.get<float>(dd), st);
+        ADS_CUDA(cudaStreamSynchronize(st));
+        t->split_ready = true;
+    }
+    const size_t cnt = static_cast<size_t>(n) * t->dim;
+    float* xh = t->xh.get<float>(cnt);
+    float* xl = t->xl.get<float>(cnt);
+    launch_split_tf32(dX, static_cast<int64_t>(cnt), xh, xl, st);
+    launch_tc_transform(xh, xl, n, t->ph.get<float>(dd), t->pl.get<float>(dd), t->dim, dY, st);
+}
+
+int ads_apply_dataset_tc(ads_transform* t, const float* X, int64_t n, float* Y) {
+    return guard([&] {
+        ads_ctx* c = t->ctx;
+        c->use();
+        std::lock_guard<std::mutex> lk(c->mu);
+        const size_t cnt = static_cast<size_t>(n) * t->dim;
+        float* dx = t->yout.get<float>(cnt);  // input staging
+        DevBuf dyb;
+        float* dy = dyb.get<float>(cnt);
+        ADS_CUDA(cudaMemcpyAsync(dx, X, cnt * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        apply_tc(t, dx, n, dy);
+        ADS_CUDA(cudaMemcpyAsync(Y, dy, cnt * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        ADS_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ads_apply_dataset_tc_device(ads_transform* t, const float* dX, int64_t n, float* dY) {
+    return guard([&] {
+        t->ctx->use();
+        apply_tc(t, dX, n, dY);
+    });
 }
 int ads_apply_transpose(ads_transform* t, const float* X, int64_t n, float* Y) {
     return guard([&] { apply_host(t, t->PT, X, n, Y); });

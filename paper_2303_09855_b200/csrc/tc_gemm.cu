@@ -1,49 +1,54 @@
-// Coarse-quantizer GEMM on the 5th-generation tensor cores (tcgen05, kind::tf32).
+// GEMMs on the 5th-generation tensor cores (tcgen05, kind::tf32): the coarse
+// quantizer's approximate distances and the 3xTF32 dataset rotation.
 //
-// approx(q, c) = |q~|^2 + |c~|^2 - 2 q^.c^ for mean-centred queries q~ and
-// centroids c~, with q^ / c^ their TF32 roundings (cvt.rna, done once by the
-// centring kernel, coarse.cu).  The products of TF32 values are exact in fp32; the tensor core
-// accumulates in fp32.  The prefilter (coarse.cu) certifies the probe order
-// with the bound
+// Pipeline (one CTA per 128 x BN output tile, 128 threads): thread 0 is the
+// producer and the MMA issuer.  TMA loads each 32-wide K block of the operand
+// tiles (boxes of 32 fp32 x rows, SWIZZLE_128B, which lands them directly in
+// the canonical K-major UMMA layout: 8-row 1024-byte atoms, 16-byte chunk
+// index XOR row-in-atom; rows outside the matrix are zero-filled) into one of
+// STAGES shared-memory stages and arms the stage's `full` mbarrier with the
+// byte count; the MMAs of a block (K = 8 per instruction) accumulate in TMEM
+// and commit to the stage's `empty` mbarrier, which frees it for the block
+// STAGES ahead.  After the last block a commit on `done` releases the four
+// warps to the epilogue: TMEM -> registers (tcgen05.ld, warp w owns lanes
+// 32w..32w+31 = rows) -> shared memory -> global with lane = column, so
+// every store writes a contiguous 128-byte row segment.
+//
+// Coarse quantizer (NPROD = 1): approx(q, c) = |q~|^2 + |c~|^2 - 2 q^.c^ for
+// mean-centred queries q~ / centroids c~ and their TF32 roundings q^ / c^
+// (cvt.rna, coarse.cu).  TF32 products are exact in fp32; accumulation is
+// fp32.  The prefilter certifies the probe order with
 //     |approx - d| <= 1.01 ((2^-10 + 2^-22 + gamma'_D + 4u) s^2 + 2 s Delta + Delta^2)
-// where gamma'_D = D u' / (1 - D u') with u' = 2^-22 (one unit of 2^-23 per
-// accumulation, doubled to cover truncating / aligned accumulation), 2^-10
-// the two operand roundings, s = |q~| + max |c~| and Delta the centring
-// round-off (see coarse.cu).  Every centroid that can reach the exact
-// top-nprobe is then rescored in fp64, so the probe order stays exact.
+// with gamma'_D = D u' / (1 - D u'), u' = 2^-22 (one unit of 2^-23 per
+// accumulation, doubled to cover truncating or aligned accumulation), 2^-10
+// for the two operand roundings, s = |q~| + max |c~| and Delta the centring
+// round-off (coarse.cu); every centroid that can reach the exact top-nprobe is
+// rescored in fp64, so the probe order stays exact.
 //
-// Tile: 128 queries (M) x 256 centroids (N) per CTA, K in blocks of 32 fp32
-// (one 128-byte swizzle row).  Operands are staged into shared memory in the
-// canonical K-major SWIZZLE_128B layout (8-row, 1024-byte atoms; 16-byte chunk
-// index XOR row-in-atom) with cp.async by all 128 threads, two stages (the
-// next block loads while the tensor core works on this one); one thread issues
-// the 4 MMAs (K = 8 each) of a block and commits them to the stage's mbarrier;
-// the accumulator (128 lanes x 256 fp32 columns) lives in TMEM and is read
-// back by the four warps (each owns 32 lanes = 32 queries) with tcgen05.ld.
+// Rotation (NPROD = 3): Y = X P^T (y_i = sum_j P[i][j] x_j, transform.cpp:99-117)
+// with X = Xh + Xl, P = Ph + Pl split into TF32 pairs and
+// Y ~= Xh Ph^T + Xh Pl^T + Xl Ph^T (the Xl Pl term, ~2^-22 relative, dropped).
+#include <cuda.h>
+
 #include <cstdint>
+#include <string>
 
 #include "engine.hpp"
 
 namespace ads {
 namespace {
 
-constexpr int kTM = 128;          // queries per tile (MMA M)
-constexpr int kTN = 256;          // centroids per tile (MMA N)
-constexpr int kTK = 32;           // fp32 per k-block (128 bytes)
-constexpr int kAStage = kTM * 128;  // bytes
-constexpr int kBStage = kTN * 128;
-constexpr int kStage = kAStage + kBStage;
+constexpr int kTM = 128;  // rows per tile (MMA M)
+constexpr int kTK = 32;   // fp32 per K block (one 128-byte swizzle row)
 constexpr int kThreads = 128;
-constexpr uint32_t kTmemCols = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 format):
-// start >> 4 [0,14), LBO >> 4 [16,30) (unused by swizzled K-major: 1),
-// SBO >> 4 [32,46) = 1024 B between 8-row atoms, version 1 [46,48),
-// layout SWIZZLE_128B = 2 [61,64).
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100): start >> 4
+// [0,14), LBO >> 4 [16,30) (unused by swizzled K-major: 1), SBO >> 4 [32,46)
+// = 1024 B between 8-row atoms, version 1 [46,48), SWIZZLE_128B = 2 [61,64).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
     d |= static_cast<uint64_t>(1) << 16;
@@ -53,14 +58,19 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     return d;
 }
 
-// Instruction descriptor: D fp32, A/B TF32, both K-major, N = 256, M = 128.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kTN >> 3) << 17) |
-                            (static_cast<uint32_t>(kTM >> 4) << 24);
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+// Instruction descriptor: D fp32, A/B TF32, both K-major, N = BN, M = 128.
+template <int BN>
+constexpr uint32_t idesc_tf32() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+           (static_cast<uint32_t>(kTM >> 4) << 24);
 }
 
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
@@ -70,53 +80,78 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
-
-// Stage rows [r0, r0 + rows) x k-block kb of a row-major matrix X (n x D) of
-// TF32-rounded values into a SWIZZLE_128B K-major tile at dst with cp.async
-// (zeros outside the matrix); the caller commits and waits.
-__device__ __forceinline__ void stage_rows(unsigned char* dst, const float* __restrict__ X, int n, int D, int r0,
-                                           int rows, int kb) {
-    const int k0 = kb * kTK;
-#pragma unroll 4
-    for (int e = threadIdx.x; e < rows * 8; e += kThreads) {
-        const int r = e >> 3, ch = e & 7;  // row, 16-byte chunk
-        const int row = r0 + r, col = k0 + ch * 4;
-        unsigned char* p = dst + (r >> 3) * 1024 + (r & 7) * 128 + ((ch ^ (r & 7)) << 4);
-        if (row < n && col < D) {
-            const uint32_t sa = smem_u32(p);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
-                         "l"(X + static_cast<int64_t>(row) * D + col)
-                         : "memory");
-        } else {
-            *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
-        }
-    }
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads) tc_coarse_gemm_kernel(const float* __restrict__ Qc, int nq,
-                                                                  const float* __restrict__ Cc, int L, int D,
-                                                                  const float* __restrict__ qn2,
-                                                                  const float* __restrict__ cn2,
-                                                                  float* __restrict__ out) {
+// Epilogues: called with (row, col, accumulator) for in-range elements.
+struct CoarseEpi {
+    const float* qn2;
+    const float* cn2;
+    float* out;
+    int ld;
+    __device__ __forceinline__ void operator()(int r, int c, float v) const {
+        out[static_cast<int64_t>(r) * ld + c] = (qn2[r] + cn2[c]) - 2.f * v;
+    }
+};
+struct StoreEpi {
+    float* out;
+    int ld;
+    __device__ __forceinline__ void operator()(int r, int c, float v) const {
+        out[static_cast<int64_t>(r) * ld + c] = v;
+    }
+};
+
+// NPROD 1: C = A0 B0^T.  NPROD 3: C = A0 B0^T + A0 B1^T + A1 B0^T.
+template <int NPROD, int BN, int STAGES, class Epi>
+__global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const __grid_constant__ CUtensorMap tA0,
+                                                           const __grid_constant__ CUtensorMap tA1,
+                                                           const __grid_constant__ CUtensorMap tB0,
+                                                           const __grid_constant__ CUtensorMap tB1, int M,
+                                                           int N, int K, Epi epi) {
+    constexpr int NA = NPROD == 3 ? 2 : 1, NB = NPROD == 3 ? 2 : 1;
+    constexpr int ATILE = kTM * 128, BTILE = BN * 128;
+    constexpr int STAGE = NA * ATILE + NB * BTILE;
+    constexpr uint32_t IDESC = idesc_tf32<BN>();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the swizzle atoms
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    __shared__ uint64_t bars[2];
+    __shared__ uint64_t full[STAGES], empty[STAGES], done;
     __shared__ uint32_t tmem_holder;
     const int warp = threadIdx.x >> 5;
     const unsigned lane = threadIdx.x & 31u;
-    const int q0 = blockIdx.y * kTM, c0 = blockIdx.x * kTN;
-    const int nkb = (D + kTK - 1) / kTK;
+    const int m0 = blockIdx.y * kTM, n0 = blockIdx.x * BN;
+    const int nkb = (K + kTK - 1) / kTK;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s]);
+            mbar_init(&empty[s]);
+        }
+        mbar_init(&done);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tA0)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tB0)) : "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
-                     "r"(kTmemCols)
+                     "r"(static_cast<uint32_t>(BN))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -125,64 +160,49 @@ __global__ void __launch_bounds__(kThreads) tc_coarse_gemm_kernel(const float* _
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_holder;
 
-    uint32_t phase[2] = {0u, 0u};
-    auto load = [&](int kb) {
-        unsigned char* a = smem + (kb & 1) * kStage;
-        stage_rows(a, Qc, nq, D, q0, kTM, kb);
-        stage_rows(a + kAStage, Cc, L, D, c0, kTN, kb);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    load(0);
-    for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb & 1;
-        if (kb + 1 < nkb) {  // prefetch the next block into the other stage
-            const int sn = st ^ 1;
-            if (kb + 1 >= 2) {  // once the MMAs that read it (block kb - 1) are done
-                mbar_wait(&bars[sn], phase[sn]);
-                phase[sn] ^= 1u;
-            }
-            load(kb + 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        unsigned char* a = smem + st * kStage;
-        unsigned char* b = a + kAStage;
-        if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
+        auto issue = [&](int kb) {
+            const int s = kb % STAGES;
+            unsigned char* t = smem + s * STAGE;
+            mbar_expect(&full[s], STAGE);
+            tma_load(t, &tA0, &full[s], kb * kTK, m0);
+            if constexpr (NA == 2) tma_load(t + ATILE, &tA1, &full[s], kb * kTK, m0);
+            tma_load(t + NA * ATILE, &tB0, &full[s], kb * kTK, n0);
+            if constexpr (NB == 2) tma_load(t + NA * ATILE + BTILE, &tB1, &full[s], kb * kTK, n0);
+        };
+        for (int kb = 0; kb < STAGES && kb < nkb; ++kb) issue(kb);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % STAGES;
+            const uint32_t ph = static_cast<uint32_t>(kb / STAGES) & 1u;
+            mbar_wait(&full[s], ph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t da = sw128_desc(smem_u32(a)), db = sw128_desc(smem_u32(b));
+            unsigned char* t = smem + s * STAGE;
+            const uint64_t a0 = sw128_desc(smem_u32(t));
+            const uint64_t a1 = sw128_desc(smem_u32(t + (NA - 1) * ATILE));
+            const uint64_t b0 = sw128_desc(smem_u32(t + NA * ATILE));
+            const uint64_t b1 = sw128_desc(smem_u32(t + NA * ATILE + (NB - 1) * BTILE));
 #pragma unroll
             for (int k = 0; k < kTK / 8; ++k) {  // K = 8 tf32 = 32 bytes per MMA
-                const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\t"
-                    "setp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                    "l"(da + static_cast<uint64_t>(k * 2)), "l"(db + static_cast<uint64_t>(k * 2)), "r"(kIdesc),
-                    "r"(acc)
-                    : "memory");
+                const uint64_t dk = static_cast<uint64_t>(k * 2);
+                umma_tf32(tmem, a0 + dk, b0 + dk, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+                if constexpr (NPROD == 3) {
+                    umma_tf32(tmem, a0 + dk, b1 + dk, IDESC, 1u);
+                    umma_tf32(tmem, a1 + dk, b0 + dk, IDESC, 1u);
+                }
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(&bars[st]))
-                         : "memory");
+            umma_commit(&empty[s]);
+            if (kb + STAGES < nkb) {
+                mbar_wait(&empty[s], ph);  // the MMAs reading this stage are done
+                issue(kb + STAGES);
+            }
         }
+        umma_commit(&done);
     }
-    // the last commit covers every earlier MMA of this thread
-    {
-        const int st = (nkb - 1) & 1;
-        mbar_wait(&bars[st], phase[st]);
-    }
+    mbar_wait(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-    // epilogue: warp w owns TMEM lanes (queries) 32w .. 32w + 31.  A 32 x 32
-    // block goes TMEM -> registers (thread = query) -> shared memory (the
-    // operand stages are free now) -> global with lane = centroid, so every
-    // store writes one contiguous 128-byte row segment.
     float* tr = reinterpret_cast<float*>(smem) + warp * (32 * 33);
-    const int qb = q0 + warp * 32;
-    for (int cb = 0; cb < kTN; cb += 32) {
+    for (int cb = 0; cb < BN; cb += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(cb);
         asm volatile(
@@ -197,23 +217,77 @@ __global__ void __launch_bounds__(kThreads) tc_coarse_gemm_kernel(const float* _
 #pragma unroll
         for (int j = 0; j < 32; ++j) tr[lane * 33 + j] = __uint_as_float(v[j]);
         __syncwarp();
-        const int c = c0 + cb + static_cast<int>(lane);
-        const float cn = c < L ? cn2[c] : 0.f;
+        const int c = n0 + cb + static_cast<int>(lane);
         for (int r = 0; r < 32; ++r) {
-            const int q = qb + r;
-            if (q < nq && c < L) out[static_cast<int64_t>(q) * L + c] = (qn2[q] + cn) - 2.f * tr[r * 33 + lane];
+            const int row = m0 + warp * 32 + r;
+            if (row < M && c < N) epi(row, c, tr[r * 33 + lane]);
         }
         __syncwarp();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(static_cast<uint32_t>(BN))
+                     : "memory");
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t h, l;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x[i]));
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x[i] - __uint_as_float(h)));
+        hi[i] = __uint_as_float(h);
+        lo[i] = __uint_as_float(l);
+    }
+}
+
+// ---- host: tensor maps through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        ADS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// rows x width row-major fp32 (width % 4 == 0); box = 32 columns x box_rows rows, SWIZZLE_128B.
+CUtensorMap tile_map(const float* base, int width, int64_t rows, int box_rows) {
+    CUtensorMap m{};
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * sizeof(float)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return m;
+}
+
+template <int NPROD, int BN, int STAGES, class Epi>
+void launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1, int M,
+               int N, int K, Epi epi, cudaStream_t st) {
+    constexpr int NA = NPROD == 3 ? 2 : 1, NB = NPROD == 3 ? 2 : 1;
+    constexpr int smem = STAGES * (NA * kTM * 128 + NB * BN * 128) + 1024;
+    auto kern = tc_gemm_kernel<NPROD, BN, STAGES, Epi>;
+    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid((N + BN - 1) / BN, (M + kTM - 1) / kTM);
+    kern<<<grid, kThreads, smem, st>>>(a0, a1, b0, b1, M, N, K, epi);
+    ADS_LAUNCH_CHECK();
 }
 
 }  // namespace
 
-bool tc_coarse_supported(int D) { return D % 4 == 0; }
+bool tc_coarse_supported(int D) { return D % 4 == 0 && D >= kTK; }
 
 double tc_coarse_gamma(int D) {
     const double up = 0x1.0p-22;
@@ -224,11 +298,30 @@ double tc_coarse_gamma(int D) {
 void launch_tc_coarse_gemm(const float* Qc, int nq, const float* Cc, int L, int D, const float* qn2,
                            const float* cn2, float* out, cudaStream_t st) {
     if (nq <= 0 || L <= 0) return;
-    const int smem = 2 * kStage + 1024;
-    ADS_CUDA(cudaFuncSetAttribute(tc_coarse_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid((L + kTN - 1) / kTN, (nq + kTM - 1) / kTM);
-    tc_coarse_gemm_kernel<<<grid, kThreads, smem, st>>>(Qc, nq, Cc, L, D, qn2, cn2, out);
+    const CUtensorMap a = tile_map(Qc, D, nq, kTM);
+    const CUtensorMap b = tile_map(Cc, D, L, 256);
+    launch_tc<1, 256, 4>(a, a, b, b, nq, L, D, CoarseEpi{qn2, cn2, out, L}, st);
+}
+
+void launch_split_tf32(const float* x, int64_t n, float* hi, float* lo, cudaStream_t st) {
+    if (n <= 0) return;
+    const int64_t blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+    split_tf32_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, n, hi, lo);
     ADS_LAUNCH_CHECK();
+}
+
+void launch_tc_transform(const float* Xh, const float* Xl, int64_t n, const float* Ph, const float* Pl, int D,
+                         float* Y, cudaStream_t st) {
+    if (n <= 0) return;
+    if (D % 4 != 0 || D < kTK)
+        throw std::invalid_argument("apply (tensor cores): dimension must be a multiple of 4 and >= 32");
+    const CUtensorMap ph = tile_map(Ph, D, D, 128), pl = tile_map(Pl, D, D, 128);
+    const int64_t chunk = static_cast<int64_t>(65535) * kTM;
+    for (int64_t r = 0; r < n; r += chunk) {
+        const int64_t rows = n - r < chunk ? n - r : chunk;
+        const CUtensorMap xh = tile_map(Xh + r * D, D, rows, kTM), xl = tile_map(Xl + r * D, D, rows, kTM);
+        launch_tc<3, 128, 3>(xh, xl, ph, pl, static_cast<int>(rows), D, D, StoreEpi{Y + r * D, D}, st);
+    }
 }
 
 }  // namespace ads

