@@ -243,6 +243,9 @@ typedef struct {
                               top-nprobe; 2: the same with the fp32-FMA GEMM; 1: exact fp64
                               distance to every centroid.  All give probe_order's exact (d2, id)
                               order. */
+    int32_t rotate_mode;   /* when the queries come untransformed (Q_t == NULL): 0 (default) exact
+                              fp64 rotation, bit-identical to apply(); 1 the 3xTF32 tensor-core
+                              rotation of ads_apply_dataset_tc (~1e-6 |q|; D % 4 == 0, D >= 32) */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 

@@ -501,7 +501,8 @@ def search_shape(d: int, step: int = 0, warps_per_cta: int = 0) -> tuple:
 
 def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
-                tile: int = 64, query_order: int = 0, coarse_mode: int = 0) -> L.SearchOpts:
+                tile: int = 64, query_order: int = 0, coarse_mode: int = 0,
+                rotate_mode: int = 0) -> L.SearchOpts:
     """scheduler 0: query-major, first/step in candidates; scheduler 1: list-major
     waves, first/step in probed lists (see include/adsann_b200.h)."""
     o = L.SearchOpts()
@@ -509,6 +510,7 @@ def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_p
     o.first, o.step, o.warps_per_cta, o.queries_per_cta, o.ctas_per_sm, o.time_stages = (
         first, step, warps_per_cta, queries_per_cta, ctas_per_sm, int(time_stages))
     o.scheduler, o.tile, o.query_order, o.coarse_mode = scheduler, tile, query_order, coarse_mode
+    o.rotate_mode = rotate_mode
     return o
 
 

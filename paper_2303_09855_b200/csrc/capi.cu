@@ -129,6 +129,8 @@ struct ads_ivf {
     double* P = nullptr;
     std::map<PlanKey, std::unique_ptr<DevSegPlan>> plans;
     DevBuf dist, probes, qrot, qin_t, qin_raw, o_ids, o_dists, o_cnt, o_dims, o_cand;
+    DevBuf ph, pl, qh, ql;  // rotate_mode 1: P and the queries as TF32 hi/lo pairs
+    bool p_split = false;
     ListMajorScratch lm;
     int32_t* chain_rank = nullptr;  // L2-locality rank of each list (host chain over centroids)
     DevBuf order, order_tmp;
@@ -1007,6 +1009,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->tile = 64;
     o->query_order = 0;
     o->coarse_mode = 0;
+    o->rotate_mode = 0;
 }
 
 namespace {
@@ -1078,7 +1081,28 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     const float* Qs = transformed ? dQt : dQraw;
     if (transformed && !dQt) {  // rotate on device (apply, transform.cpp:99-117)
         float* qr = x->qrot.get<float>(static_cast<size_t>(nq) * D);
-        launch_apply(x->P, D, dQraw, nq, qr, st);
+        if (o.rotate_mode == 1) {  // 3xTF32 tensor cores (tc_gemm.cu)
+            require(D % 4 == 0 && D >= 32, "rotate_mode 1: dimension must be a multiple of 4 and >= 32");
+            const size_t dd = static_cast<size_t>(D) * D;
+            if (!x->p_split) {
+                std::vector<double> hp(dd);
+                ADS_CUDA(cudaMemcpyAsync(hp.data(), x->P, sizeof(double) * dd, cudaMemcpyDeviceToHost, st));
+                ADS_CUDA(cudaStreamSynchronize(st));
+                std::vector<float> pf(hp.begin(), hp.end());
+                float* p32 = x->qh.get<float>(dd);
+                ADS_CUDA(cudaMemcpyAsync(p32, pf.data(), sizeof(float) * dd, cudaMemcpyHostToDevice, st));
+                launch_split_tf32(p32, static_cast<int64_t>(dd), x->ph.get<float>(dd), x->pl.get<float>(dd), st);
+                ADS_CUDA(cudaStreamSynchronize(st));
+                x->p_split = true;
+            }
+            const size_t cnt = static_cast<size_t>(nq) * D;
+            float* qh = x->qh.get<float>(cnt);
+            float* ql = x->ql.get<float>(cnt);
+            launch_split_tf32(dQraw, static_cast<int64_t>(cnt), qh, ql, st);
+            launch_tc_transform(qh, ql, nq, x->ph.get<float>(dd), x->pl.get<float>(dd), D, qr, st);
+        } else {
+            launch_apply(x->P, D, dQraw, nq, qr, st);
+        }
         Qs = qr;
     }
     if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[1], st));

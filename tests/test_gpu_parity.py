@@ -398,6 +398,21 @@ def test_transform_tensor_cores(eng, orc, n, d):
         eng.apply_dataset_tc(eng.generate_orthogonal(6, 1), rng.normal(size=(3, 6)).astype(np.float32))
 
 
+def test_ivf_tensor_core_query_rotation(eng, orc):
+    """rotate_mode 1 (queries rotated by the 3xTF32 tensor-core transform on the GPU)
+    == the oracle run on the same TC-rotated queries, bit for bit."""
+    raw, t, qr, qt, P = make_fixture(orc, 3000, 128, 16, 40, 77)
+    lay = oracle_index(orc, raw, t, P, 40, 78, d1=32)
+    idx = gpu_index(eng, lay, P)
+    m = eng.TransformMatrix(128, 0, np.asarray(P, np.float64))
+    qt_tc = eng.apply_dataset_tc(m, qr)
+    assert not np.array_equal(qt_tc, qt)  # a different (fp32-accurate) rotation
+    for mode in ("ad-split", "ad"):
+        res = eng.ivf_query_batch(idx, None, qr, 10, 7, eng.IvfMode(MODE_ID[mode]),
+                                  opts=eng.search_opts(rotate_mode=1))
+        assert_same_results(res, orc, lay, qt_tc, qr, 10, 7, mode, 2.1, 32, 10, 256)
+
+
 @pytest.mark.parametrize("n,d,nq,K,grid", [(1500, 48, 12, 20, [1e6]),
                                            (2000, 64, 10, 50, [2.5, 0.5, 1.0, 2.0, 1.5, 3.0]),
                                            (800, 30, 7, 1, [2.1, 2.1, 0.2]),
