@@ -210,6 +210,15 @@ int ads_ivf_create(ads_ctx *ctx, const ads_ivf_desc *desc, ads_ivf **out);
 int ads_ivf_build(ads_ctx *ctx, const float *raw, const float *t, int32_t n, int32_t d,
                   const double *P, int32_t k, uint64_t seed, int32_t layout, int32_t d1,
                   int32_t max_iters, int32_t init, ads_ivf **out);
+/* build_ivf for data that does not fit the reference's flow (config 5,
+ * 1e8 rows): dT is the transformed dataset on the device (n x d); k-means
+ * (seeded sample init, max_iters Lloyd iterations) runs on every
+ * (n / sample)-th row, then every row goes to its nearest centroid through the
+ * certified coarse prefilter at nprobe = 1 (the exact fp64 argmin, lowest id
+ * on ties); split layout at d1, transformed space only (AD / AD-split modes). */
+int ads_ivf_build_sampled_device(ads_ctx *ctx, const float *dT, int64_t n, int32_t d, const double *P,
+                                 int32_t k, uint64_t seed, int32_t d1, int32_t max_iters, int64_t sample,
+                                 ads_ivf **out);
 int ads_ivf_destroy(ads_ivf *idx);
 /* meta[0..6] = n, d, k_clusters, d1, layout, seed, has_raw */
 int ads_ivf_meta(ads_ivf *idx, int64_t *meta);

@@ -112,6 +112,7 @@ ads_ivf_search_device = _sig("ads_ivf_search_device", [vp, vp, vp, i32, i32, i32
 ads_ivf_probe_order = _sig("ads_ivf_probe_order", [vp, vp, i32, i32, i32, vp])
 ads_ivf_last_timings = _sig("ads_ivf_last_timings", [vp, vp])
 ads_ivf_coarse_stats = _sig("ads_ivf_coarse_stats", [vp, vp])
+ads_ivf_build_sampled_device = _sig("ads_ivf_build_sampled_device", [vp, vp, i64, i32, vp, i32, u64, i32, i32, i64, C.POINTER(vp)])
 ads_ivf_subset = _sig("ads_ivf_subset", [vp, vp, C.POINTER(vp)])
 ads_merge_topk = _sig("ads_merge_topk", [vp, vp, vp, i32, i32, i32, vp, vp, vp])
 ads_merge_topk_device = _sig("ads_merge_topk_device", [vp, vp, vp, i32, i32, i32, vp, vp, vp])

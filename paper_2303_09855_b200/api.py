@@ -613,6 +613,23 @@ def build_ivf(ds_raw: np.ndarray, ds_transformed: np.ndarray, m: TransformMatrix
     return IvfIndex(h, ctx)
 
 
+def build_ivf_sampled_device(dT: "DeviceArray", m: TransformMatrix, k_clusters: int, seed: int, d1: int = 32,
+                             max_iters: int = 10, sample: int = 2_000_000,
+                             ctx: Optional[Context] = None) -> IvfIndex:
+    """build_ivf for device-resident data too large for the reference flow (config 5):
+    k-means on every (n / sample)-th row, every row assigned by the certified
+    coarse prefilter (exact argmin), split layout, transformed space only."""
+    ctx = ctx or Context.default()
+    n, d = dT.shape
+    if m.dim != d:
+        raise ValueError("build_ivf: matrix dimension does not match the data")
+    P = np.ascontiguousarray(m.entries, np.float64)
+    h = C.c_void_p()
+    check(L.ads_ivf_build_sampled_device(ctx.h, C.c_void_p(dT.ptr), n, d, P.ctypes.data, k_clusters, seed, d1,
+                                         max_iters, min(sample, n), C.byref(h)))
+    return IvfIndex(h, ctx)
+
+
 @dataclass
 class BatchResult:
     ids: np.ndarray      # nq x K int32 (-1 padded)

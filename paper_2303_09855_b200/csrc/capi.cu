@@ -956,6 +956,56 @@ int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int
     });
 }
 
+int ads_ivf_build_sampled_device(ads_ctx* ctx, const float* dT, int64_t n, int32_t d, const double* P, int32_t k,
+                                 uint64_t seed, int32_t d1, int32_t max_iters, int64_t sample, ads_ivf** out) {
+    return guard([&] {
+        require(n >= 1 && n <= 0x7fffffff && d >= 1, "build_ivf: bad shape");
+        require(P != nullptr, "build_ivf: matrix dimension does not match the data");
+        require(d1 >= 1 && d1 < d, "build_ivf: split layout needs 1 <= d1 < D");
+        require(k >= 1 && sample >= k && sample <= n, "build_ivf: need 1 <= k <= sample <= n");
+        ctx->use();
+        cudaStream_t st = ctx->stream;
+        auto x = std::make_unique<ads_ivf>();
+        x->ctx = ctx;
+        x->n = static_cast<int>(n);
+        x->d = d;
+        x->k = k;
+        x->d1 = d1;
+        x->layout = 1;
+        x->seed = seed;
+        ivf_alloc_common(x.get());
+        x->d1p = d1;
+        const size_t N = static_cast<size_t>(n);
+        x->P = dev_upload(P, static_cast<size_t>(d) * d, st);
+        ADS_CUDA(cudaMalloc(&x->cent_t, sizeof(float) * k * static_cast<size_t>(d)));
+        // k-means on every (n / sample)-th row (seeded sample init, Lloyd iterations)
+        const int64_t stride = n / sample;
+        DevBuf ds, dsa, dasg;
+        float* S = ds.get<float>(static_cast<size_t>(sample) * d);
+        ADS_CUDA(cudaMemcpy2DAsync(S, sizeof(float) * d, dT, sizeof(float) * d * stride, sizeof(float) * d,
+                                   static_cast<size_t>(sample), cudaMemcpyDeviceToDevice, st));
+        (void)run_kmeans(S, sample, d, k, max_iters, seed, 1, x->cent_t, dsa.get<int32_t>(sample), st);
+        ds.release();
+        // every row to its nearest centroid: the certified coarse prefilter at
+        // nprobe = 1 (exact fp64 argmin, lowest id on ties, as kmeans assigns)
+        centroid_prefilter(x->cent_t, k, d, x->cc_t, st);
+        int32_t* asg = dasg.get<int32_t>(N);
+        const int64_t chunk = 65536;
+        for (int64_t r = 0; r < n; r += chunk) {
+            const int rows = static_cast<int>(n - r < chunk ? n - r : chunk);
+            launch_coarse_probes_fast(dT + r * d, rows, x->cent_t, k, d, 1, x->cc_t, x->coarse, asg + r, 0, st);
+        }
+        ADS_CUDA(cudaMalloc(&x->list_off, sizeof(int64_t) * (k + 1)));
+        ADS_CUDA(cudaMalloc(&x->ids, sizeof(int32_t) * N));
+        build_lists(asg, n, k, x->list_off, x->ids, st);
+        alloc_split_pair(N, d1, d - d1, &x->a1_t, &x->a2_t);
+        gather_split(dT, x->ids, n, d, d1, x->a1_t, x->a2_t, st);
+        x->coarse.release();  // the assignment-sized scratch
+        ADS_CUDA(cudaStreamSynchronize(st));
+        *out = x.release();
+    });
+}
+
 int ads_ivf_destroy(ads_ivf* idx) {
     return guard([&] {
         if (!idx) return;

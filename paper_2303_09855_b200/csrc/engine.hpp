@@ -116,6 +116,11 @@ struct DevBuf {
         }
         return static_cast<T*>(p);
     }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -159,6 +164,9 @@ struct CoarseScratch {
     DevBuf approx, qc, qn2, qnrm;
     DevBuf stats;     // [rescored centroids, fallback queries] of the last launch
     int last_nq = 0;
+    void release() {
+        for (DevBuf* b : {&approx, &qc, &qn2, &qnrm, &stats}) b->release();
+    }
 };
 // Per centroid table: mean mu (fp64), centred fp32 copy, |c~|^2 and max |c~|.
 struct CoarseCentroids {
