@@ -142,6 +142,25 @@ def measured_peaks() -> dict:
 
 
 # ---------------------------------------------------------------- workload setup
+def config_for(args):
+    """BASELINE config args.config, with --cfg-override applied (calibration runs only)."""
+    import copy
+    import dataclasses
+
+    from paper_2303_09855_b200 import configs
+
+    cfg = copy.deepcopy(configs.CONFIGS[args.config])
+    for kv in filter(None, getattr(args, "cfg_override", "").split(",")):
+        k, v = kv.split("=")
+        if k in {f.name for f in dataclasses.fields(cfg)}:
+            cur = getattr(cfg, k)
+            setattr(cfg, k, type(cur)(float(v)) if not isinstance(cur, bool) else v in ("1", "true"))
+        else:
+            cfg.extra[k] = int(float(v))
+        cfg.key += f"-{k}{v}"
+    return cfg
+
+
 def setup_large(cfg, dev, rank, log):
     """Config 5 (1e8 rows): generate on the host, rotate and build on the device
     (ads_ivf_build_sampled_device), ground truth for the first gt_queries queries
@@ -259,7 +278,7 @@ def run_search(args, D: Dist):
     from paper_2303_09855_b200 import configs
 
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
-    cfg = configs.CONFIGS[args.config]
+    cfg = config_for(args)
     if args.nq:
         cfg.nq = args.nq
     if args.kmeans_init >= 0:
@@ -437,7 +456,7 @@ def run_search_sharded(args, D: Dist):
     from paper_2303_09855_b200.shard import merge_topk_device, partition_lists, shard_index
 
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
-    cfg = configs.CONFIGS[args.config]
+    cfg = config_for(args)
     if args.nq:
         cfg.nq = args.nq
     if args.kmeans_init >= 0:
@@ -559,7 +578,7 @@ def run_reference(args, D: Dist):
     log = lambda *a: print(*a, file=sys.stderr, flush=True)  # noqa: E731
     from oracle import ref_available
 
-    cfg = configs.CONFIGS[args.config]
+    cfg = config_for(args)
     if args.nq:
         cfg.nq = args.nq
     nprobe = args.nprobe or cfg.nprobe
@@ -631,6 +650,8 @@ def main():
     ap.add_argument("--force-shard", action="store_true",
                     help="run the list-sharded path even at N=1 (exercises NCCL + merge)")
     ap.add_argument("--kmeans-iters", type=int, default=0)
+    ap.add_argument("--cfg-override", default="",
+                    help="calibration runs: comma list of Config fields / extra keys, e.g. sigma=0.5,gt_queries=30")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
