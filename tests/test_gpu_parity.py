@@ -435,3 +435,36 @@ def test_verify_theory_bitexact(eng, orc, n, d, nq, K, grid):
         eng.verify_theory(t, qt, t.shape[0] + 1, grid)
     with pytest.raises(ValueError):
         eng.verify_theory(t, qt, K, [0.0])
+
+
+@pytest.mark.parametrize("K", [200, 256, 300, 1000])
+def test_ivf_large_k_merge_paths(eng, orc, K):
+    """K = 200 / 256 fit the CTA rank merge (heap <= 2 x blockDim), 300 / 1000 take
+    the one-warp sequential offers; all bit-exact, including partial (count < K) results."""
+    raw, t, qr, qt, P = make_fixture(orc, 4000, 64, 16, 12, 91 + K)
+    lay = oracle_index(orc, raw, t, P, 30, 93, d1=32)
+    idx = gpu_index(eng, lay, P)
+    for mode in ("ad-split", "fd"):
+        for nprobe in (2, 11, 30):
+            res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]), first=0, step=128)
+            assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, 32, K, 128)
+
+
+def test_ivf_empty_lists_and_empty_streams(eng, orc):
+    """Many empty lists (k close to n): queries whose probed lists hold nothing
+    return count 0 (ids -1, NaN dists); the rest stay bit-exact."""
+    raw, t, qr, qt, P = make_fixture(orc, 150, 32, 4, 20, 5)
+    k = 120
+    cent = t[:k].copy()
+    asg = np.zeros(150, np.int32)  # everything in 3 lists, 117 lists empty
+    asg[50:100] = 1
+    asg[100:] = 2
+    lay = orc.ivf_layout(raw, t, P, cent, asg, k, 16, True)
+    idx = gpu_index(eng, lay, P)
+    for nprobe in (1, 3, 40, k):
+        res = eng.ivf_query_batch(idx, qt, qr, 5, nprobe, eng.IvfMode.kAdSplit, eng.DcoConfig(2.1, 16))
+        assert_same_results(res, orc, lay, qt, qr, 5, nprobe, "ad-split", 2.1, 16, 5, 256)
+        empty = res.counts == 0
+        if nprobe == 1:
+            assert empty.any()
+        assert (res.ids[empty] == -1).all() and np.isnan(res.dists[empty]).all()
