@@ -71,6 +71,13 @@ T* dev_upload(const T* h, size_t count, cudaStream_t st) {
     if (count) ADS_CUDA(cudaMemcpyAsync(d, h, sizeof(T) * count, cudaMemcpyHostToDevice, st));
     return d;
 }
+// Upload into a scratch DevBuf (freed with it, also when a later step throws).
+template <typename T>
+T* buf_upload(DevBuf& b, const T* h, size_t count, cudaStream_t st) {
+    T* d = b.get<T>(count);
+    if (count) ADS_CUDA(cudaMemcpyAsync(d, h, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    return d;
+}
 }  // namespace
 
 struct ads_ctx {
@@ -96,6 +103,10 @@ struct ads_transform {
     DevBuf xin, yout;
     DevBuf ph, pl, xh, xl;  // 3xTF32 tensor-core path: P and X as TF32 hi/lo pairs
     bool split_ready = false;
+    ~ads_transform() {
+        if (P) cudaFree(P);
+        if (PT) cudaFree(PT);
+    }
 };
 
 struct PlanKey {
@@ -342,8 +353,6 @@ int ads_transform_destroy(ads_transform* t) {
     return guard([&] {
         if (!t) return;
         t->ctx->use();
-        cudaFree(t->P);
-        cudaFree(t->PT);
         delete t;
     });
 }
@@ -473,7 +482,7 @@ void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int6
     a.counter = ctx->counter;
     constexpr int64_t kTile = 2048;
     a.tile = kTile;
-    int64_t* dt = nullptr;
+    DevBuf tiles;
     if (b.cand_rows) {
         require(host_off != nullptr, "dco: candidate offsets missing");
         std::vector<int64_t> tq, tl, th;
@@ -492,7 +501,7 @@ void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int6
         all.insert(all.end(), tq.begin(), tq.end());
         all.insert(all.end(), tl.begin(), tl.end());
         all.insert(all.end(), th.begin(), th.end());
-        dt = dev_upload(all.data(), all.size(), st);
+        const int64_t* dt = buf_upload(tiles, all.data(), all.size(), st);
         a.tile_q = dt;
         a.tile_lo = dt + a.ntiles;
         a.tile_hi = dt + 2 * a.ntiles;
@@ -505,7 +514,6 @@ void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int6
     if (b.dims_per_query) ADS_CUDA(cudaMemsetAsync(b.dims_per_query, 0, sizeof(uint64_t) * b.nq, st));
     if (a.ntiles > 0) launch_dco_fixed(a, st);
     ADS_CUDA(cudaStreamSynchronize(st));  // dp / tile table are freed below
-    if (dt) cudaFree(dt);
     dp.release();
 }
 
@@ -698,16 +706,13 @@ int ads_brute_force_knn(ads_ctx* ctx, const float* base, int64_t n, int32_t d,
         require(K <= n, "brute_force_knn: K exceeds dataset size");
         ctx->use();
         cudaStream_t st = ctx->stream;
-        float* db = dev_upload(base, static_cast<size_t>(n) * d, st);
-        float* dq = dev_upload(queries, static_cast<size_t>(nq) * d, st);
-        int32_t* di = nullptr;
-        ADS_CUDA(cudaMalloc(&di, sizeof(int32_t) * (static_cast<size_t>(nq) * K + 1)));
+        DevBuf bb, bq, bi;
+        const float* db = buf_upload(bb, base, static_cast<size_t>(n) * d, st);
+        const float* dq = buf_upload(bq, queries, static_cast<size_t>(nq) * d, st);
+        int32_t* di = bi.get<int32_t>(static_cast<size_t>(nq) * K);
         launch_brute_knn(db, n, d, dq, nq, K, di, st);
         ADS_CUDA(cudaMemcpyAsync(ids, di, sizeof(int32_t) * nq * K, cudaMemcpyDeviceToHost, st));
         ADS_CUDA(cudaStreamSynchronize(st));
-        cudaFree(db);
-        cudaFree(dq);
-        cudaFree(di);
     });
 }
 
@@ -807,8 +812,8 @@ static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& o
     out.mu = dev_upload(mu.data(), mu.size(), st);
     ADS_CUDA(cudaMalloc(&out.cc, sizeof(float) * h.size()));
     ADS_CUDA(cudaMalloc(&out.cn2, sizeof(float) * k));
-    double* nrm = nullptr;
-    ADS_CUDA(cudaMalloc(&nrm, sizeof(double) * k));
+    DevBuf bn;
+    double* nrm = bn.get<double>(k);
     coarse_center(dC, k, D, out.mu, out.cc, out.cn2, nrm, st);
     if (tc_coarse_supported(D)) {
         ADS_CUDA(cudaMalloc(&out.cc_tf, sizeof(float) * h.size()));
@@ -817,7 +822,6 @@ static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& o
     std::vector<double> hn(static_cast<size_t>(k));
     ADS_CUDA(cudaMemcpyAsync(hn.data(), nrm, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
     ADS_CUDA(cudaStreamSynchronize(st));
-    cudaFree(nrm);
     double m = 0.0;
     for (double v : hn) m = std::max(m, v);
     out.cmax = m * (1.0 + 1e-12) + 1e-300;
@@ -929,11 +933,11 @@ int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int
                 std::vector<double> PT(static_cast<size_t>(d) * d);
                 for (int i = 0; i < d; ++i)
                     for (int j = 0; j < d; ++j) PT[static_cast<size_t>(j) * d + i] = P[static_cast<size_t>(i) * d + j];
-                double* dPT = dev_upload(PT.data(), PT.size(), st);
+                DevBuf bpt;
+                const double* dPT = buf_upload(bpt, PT.data(), PT.size(), st);
                 ADS_CUDA(cudaMalloc(&x->cent_raw, sizeof(float) * k * static_cast<size_t>(d)));
                 launch_apply(dPT, d, x->cent_t, k, x->cent_raw, st);
                 ADS_CUDA(cudaStreamSynchronize(st));
-                cudaFree(dPT);
             }
             std::vector<float> hc(static_cast<size_t>(k) * d);
             ADS_CUDA(cudaMemcpyAsync(hc.data(), x->cent_t, sizeof(float) * hc.size(), cudaMemcpyDeviceToHost, st));
@@ -1431,21 +1435,17 @@ int ads_merge_topk(ads_ctx* ctx, const double* dists, const int32_t* ids, int32_
         ctx->use();
         cudaStream_t st = ctx->stream;
         const size_t in = static_cast<size_t>(G) * nq * K, o = static_cast<size_t>(nq) * K;
-        double* dd = dev_upload(dists, in, st);
-        int32_t* di = dev_upload(ids, in, st);
-        int32_t *oi = nullptr, *oc = nullptr;
-        double* od = nullptr;
-        ADS_CUDA(cudaMalloc(&oi, sizeof(int32_t) * (o + 1)));
-        ADS_CUDA(cudaMalloc(&od, sizeof(double) * (o + 1)));
-        ADS_CUDA(cudaMalloc(&oc, sizeof(int32_t) * (nq + 1)));
+        DevBuf bd, bi, boi, bod, boc;
+        const double* dd = buf_upload(bd, dists, in, st);
+        const int32_t* di = buf_upload(bi, ids, in, st);
+        int32_t* oi = boi.get<int32_t>(o);
+        double* od = bod.get<double>(o);
+        int32_t* oc = boc.get<int32_t>(nq);
         launch_merge_topk(dd, di, G, nq, K, oi, od, oc, st);
         ADS_CUDA(cudaMemcpyAsync(out_ids, oi, sizeof(int32_t) * o, cudaMemcpyDeviceToHost, st));
         ADS_CUDA(cudaMemcpyAsync(out_dists, od, sizeof(double) * o, cudaMemcpyDeviceToHost, st));
         if (out_counts) ADS_CUDA(cudaMemcpyAsync(out_counts, oc, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st));
         ADS_CUDA(cudaStreamSynchronize(st));
-        for (void* p : {static_cast<void*>(dd), static_cast<void*>(di), static_cast<void*>(oi),
-                        static_cast<void*>(od), static_cast<void*>(oc)})
-            cudaFree(p);
     });
 }
 
