@@ -133,6 +133,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def ncu_traffic(workload: str):
+    """roofline.traffic: DRAM bytes per launch of the dominant kernel from the committed
+    ncu capture of the same command (profiles/traffic.json), in GB; None if not captured."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    e = json.load(open(p)).get(workload)
+    return None if e is None else round(e["dram_read_gb"] + e["dram_write_gb"], 3)
+
+
 def measured_peaks() -> dict:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -402,7 +412,8 @@ def run_search(args, D: Dist):
                 "d2h_bytes_per_step": nq * K * (4 + 8) + nq * (4 + 8 + 8)},
         "gpu_launches": 4 * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(cfg.key),
+                     "traffic_unit": "GB per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
                      "kernel": "ivf_search_kernel<4>", "peak_source": peaks["source"] + ", copy (burst)",
                      "algorithmic_bytes_per_launch": scanned,
                      "scanned_gbs_whole_step": scanned / (float(np.mean(step_ms)) / 1e3) / 1e9},

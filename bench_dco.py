@@ -21,7 +21,7 @@ def run_dco(args, D):
 
     import paper_2303_09855_b200 as ads
     from paper_2303_09855_b200 import _lib as L
-    from bench import ClockSampler, measured_peaks
+    from bench import ClockSampler, measured_peaks, ncu_traffic
 
     log = (lambda *a: print(*a, file=__import__("sys").stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
     n = args.dco_n
@@ -117,7 +117,9 @@ def run_dco(args, D):
         "roofline": {"bound": "hbm", "achieved": scanned / (float(np.mean(ms)) / 1e3) / 1e9,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": scanned / (float(np.mean(ms)) / 1e3) / 1e9 / peaks["hbm_gbs"],
-                     "traffic": None, "kernel": "dco_fixed_kernel<4>",
+                     "traffic": ncu_traffic("cfg4-dco-10M-d256") if n >= 10_000_000 else None,
+                     "traffic_unit": "GB per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
+                     "kernel": "dco_fixed_kernel<4>",
                      "algorithmic_bytes_per_launch": scanned},
         "parity_sample": {"dcos": sample, "mismatched_decisions_or_dims": mism,
                           "checker": "oracle/_ref ad_scan" if sample else None},
