@@ -180,44 +180,98 @@ __global__ void __launch_bounds__(kPT) prefilter_kernel(const float* __restrict_
     // (>= the true nprobe-th smallest; slightly looser, far cheaper than a
     // full selection).
     float m1 = __builtin_huge_valf(), m2 = __builtin_huge_valf();
-    for (int c = tid; c < L; c += kPT) {
-        const float v = row[c];
+    auto keep2 = [&](float v) {
         if (v < m1) {
             m2 = m1;
             m1 = v;
         } else if (v < m2) {
             m2 = v;
         }
-    }
-    float* tk = reinterpret_cast<float*>(ci);  // scratch: 2*kPT floats (ci has >= 512 slots)
-    tk[2 * tid] = m1;
-    tk[2 * tid + 1] = m2;
-    __syncthreads();
-    for (int size = 2; size <= 2 * kPT; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const int i = tid;  // 2*kPT/2 pairs, one per thread
-            const int lo = 2 * i - (i & (stride - 1));
-            const int hi = lo + stride;
-            const bool up = (lo & size) == 0;
-            const float a = tk[lo], b = tk[hi];
-            if ((a > b) == up) {
-                tk[lo] = b;
-                tk[hi] = a;
-            }
-            __syncthreads();
+    };
+    const bool vec = (L & 3) == 0;  // rows are 16-byte aligned: float4 loads, 4 in flight
+    if (vec) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 4
+        for (int c = tid; c < (L >> 2); c += kPT) {
+            const float4 v = __ldg(r4 + c);
+            keep2(v.x);
+            keep2(v.y);
+            keep2(v.z);
+            keep2(v.w);
         }
+    } else {
+        for (int c = tid; c < L; c += kPT) keep2(row[c]);
     }
-    const float T = tk[nprobe - 1 < 2 * kPT - 1 ? nprobe - 1 : 2 * kPT - 1];
+    // T = the nprobe-th smallest of those 2*kPT values: 8-bit radix select on
+    // order-preserving keys (4 passes of a 256-bin histogram)
+    unsigned* hist = reinterpret_cast<unsigned*>(ci);  // scratch: 256 bins (ci has >= 512 slots)
+    __shared__ unsigned s_prefix, s_rank;
+    const unsigned k1 = fkey(m1), k2 = fkey(m2);
+    if (tid == 0) {
+        s_prefix = 0u;
+        s_rank = static_cast<unsigned>(nprobe - 1 < 2 * kPT - 1 ? nprobe - 1 : 2 * kPT - 1);
+    }
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        hist[tid] = 0u;  // kPT == 256 bins
+        __syncthreads();
+        const unsigned pre = s_prefix;
+        const unsigned hmask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
+        if ((k1 & hmask) == (pre & hmask)) atomicAdd(&hist[(k1 >> shift) & 255u], 1u);
+        if ((k2 & hmask) == (pre & hmask)) atomicAdd(&hist[(k2 >> shift) & 255u], 1u);
+        __syncthreads();
+        if (tid < 32) {  // find the bin holding rank s_rank
+            unsigned carry = 0, want = s_rank;
+            int found = -1;
+            unsigned below = 0;
+            for (int b0 = 0; b0 < 256 && found < 0; b0 += 32) {
+                const unsigned c = hist[b0 + tid];
+                unsigned incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += v;
+                }
+                const unsigned excl = carry + incl - c;
+                const unsigned hit = __ballot_sync(0xffffffffu, excl <= want && want < excl + c);
+                if (hit) {
+                    const int l = __ffs(hit) - 1;
+                    found = b0 + l;
+                    below = __shfl_sync(0xffffffffu, excl, l);
+                }
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (tid == 0) {
+                s_prefix = pre | (static_cast<unsigned>(found) << shift);
+                s_rank = want - below;
+            }
+        }
+        __syncthreads();
+    }
+    const unsigned tkey = s_prefix;
+    const float T = __uint_as_float((tkey & 0x80000000u) ? (tkey & 0x7fffffffu) : ~tkey);
     __syncthreads();
     const double sn = qnrm[q] + cmax;
     const double delta = 2.0 * 0x1.0p-24 * sn;
     const double e = 1.01 * (gamma * sn * sn + 2.0 * sn * delta + delta * delta);
     const double lim = static_cast<double>(T) + 2.0 * e;
-    for (int c = tid; c < L; c += kPT) {
-        if (static_cast<double>(row[c]) <= lim) {
+    auto take = [&](float v, int c) {
+        if (static_cast<double>(v) <= lim) {
             const int slot = atomicAdd(&s_n, 1);
             if (slot < cap) ci[slot] = c;
         }
+    };
+    if (vec) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 4
+        for (int c = tid; c < (L >> 2); c += kPT) {
+            const float4 v = __ldg(r4 + c);
+            take(v.x, 4 * c);
+            take(v.y, 4 * c + 1);
+            take(v.z, 4 * c + 2);
+            take(v.w, 4 * c + 3);
+        }
+    } else {
+        for (int c = tid; c < L; c += kPT) take(row[c], c);
     }
     __syncthreads();
     int n = s_n;
@@ -234,7 +288,27 @@ __global__ void __launch_bounds__(kPT) prefilter_kernel(const float* __restrict_
         if (tid == 0) s_full = 1;
     }
     __syncthreads();
-    if (!s_full) {
+    if (!s_full && n <= kPT) {
+        // one candidate per thread: exact distance, then its rank among the
+        // candidates by (d2, id) (ids are distinct) is its slot in the order
+        double di = 0.0;
+        int32_t ii = 0;
+        if (tid < n) {
+            ii = ci[tid];
+            di = exact_d2(C + static_cast<int64_t>(ii) * D, qd, D);
+            cd[tid] = di;
+        }
+        __syncthreads();
+        if (tid < n) {
+            int rank = 0;
+            for (int j = 0; j < n; ++j) {
+                const double dj = cd[j];
+                const int32_t ij = ci[j];
+                rank += dj < di || (dj == di && ij < ii);
+            }
+            if (rank < nprobe) probes[static_cast<int64_t>(q) * nprobe + rank] = ii;
+        }
+    } else if (!s_full) {
         int P = 2;
         while (P < n) P <<= 1;
         for (int i = tid; i < n; i += kPT) cd[i] = exact_d2(C + static_cast<int64_t>(ci[i]) * D, qd, D);

@@ -300,7 +300,10 @@ void launch_tc_coarse_gemm(const float* Qc, int nq, const float* Cc, int L, int 
     if (nq <= 0 || L <= 0) return;
     const CUtensorMap a = tile_map(Qc, D, nq, kTM);
     const CUtensorMap b = tile_map(Cc, D, L, 256);
-    launch_tc<1, 256, 4>(a, a, b, b, nq, L, D, CoarseEpi{qn2, cn2, out, L}, st);
+    // short K: two stages (96 KB, two CTAs per SM overlap one's epilogue with the
+    // other's MMAs); long K: four stages of prefetch (one CTA per SM)
+    if (D <= 256) launch_tc<1, 256, 2>(a, a, b, b, nq, L, D, CoarseEpi{qn2, cn2, out, L}, st);
+    else launch_tc<1, 256, 4>(a, a, b, b, nq, L, D, CoarseEpi{qn2, cn2, out, L}, st);
 }
 
 void launch_split_tf32(const float* x, int64_t n, float* hi, float* lo, cudaStream_t st) {
