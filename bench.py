@@ -35,13 +35,17 @@ sys.path.insert(0, ROOT)
 
 # ---------------------------------------------------------------- distributed plumbing
 class Dist:
-    def __init__(self, backend="gloo"):
+    def __init__(self, backend="gloo", force=False):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
         self.nccl = None
-        if self.world > 1 or os.environ.get("ADS_FORCE_DIST") == "1":
+        if self.world > 1 or force or os.environ.get("ADS_FORCE_DIST") == "1":
+            # a one-rank group needs the rendezvous variables torchrun would set
+            for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"),
+                         ("WORLD_SIZE", "1")):
+                os.environ.setdefault(k, v)
             import torch
             import torch.distributed as dist
 
@@ -667,7 +671,7 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     sharded = args.impl == "ours" and args.mode == "search" and args.shard == "lists"
-    D = Dist("nccl" if sharded else "gloo")
+    D = Dist("nccl" if sharded else "gloo", force=sharded and args.force_shard)
     try:
         if args.impl == "reference":
             res = run_reference(args, D)
