@@ -302,10 +302,13 @@ def run_search(args, D: Dist):
     nprobe = args.nprobe or cfg.nprobe
     dev = D.local
     ads, ctx, base, t, q, m, idx, gt = setup(cfg, dev, D.rank, log)
+    if args.same_query:  # locality experiment: every query = query 0 (perfect L2 reuse)
+        q = np.ascontiguousarray(np.repeat(q[:1], q.shape[0], axis=0))
+        gt = np.repeat(gt[:1], gt.shape[0], axis=0)
     K, nq, d = cfg.K, cfg.nq, cfg.d
     mode = ads.IvfMode.kAdSplit
     opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps,
-                           queries_per_cta=args.slots, time_stages=True)
+                           queries_per_cta=args.slots, time_stages=True, query_order=args.query_order)
 
     # HBM-resident inputs / outputs
     dq = ads.DeviceArray.from_host(ctx, q)
@@ -653,6 +656,8 @@ def main():
     ap.add_argument("--step", type=int, default=0, help="threshold refresh interval (0: 64 x warps)")
     ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0: 4 for D <= 256, else 10)")
     ap.add_argument("--slots", type=int, default=4, help="queries served concurrently per CTA")
+    ap.add_argument("--query-order", type=int, default=0, help="1: L2-locality query order (experiments)")
+    ap.add_argument("--same-query", action="store_true", help="experiment: all queries = query 0")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true", help="time (step, warps) variants after setup")
     ap.add_argument("--tune-grid", default="", help="comma list of STEPxWARPS for --tune")
