@@ -627,6 +627,8 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
     const float *q = transformed ? q_t : q_raw;
     if (!q) return fail(1, "ivf_query: missing query vector");
     if (first < 1 || step < 1) return fail(1, "ivf_query: bad threshold schedule");
+    if (split_mode ? !(transformed ? idx->a1_t : idx->a1_raw) : !(transformed ? idx->vec_t : idx->vec_raw))
+        return fail(1, "ivf_query: the layout lacks the arrays this mode reads");
     const int32_t d = idx->d, d1 = idx->d1;
 
     double *factor = NULL;

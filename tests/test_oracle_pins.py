@@ -209,3 +209,15 @@ def test_ref_verify_theory(orc, ref, n, d, nq, K, grid):
         orc.verify_theory(t, qt, 0, grid)
     with pytest.raises(ValueError):
         orc.verify_theory(t, qt, n + 1, grid)
+
+
+def test_oracle_rejects_layouts_missing_mode_arrays(orc):
+    """A layout without the arrays a mode reads is an error, not a crash."""
+    from helpers import make_fixture, oracle_index
+
+    raw, t, qr, qt, P = make_fixture(orc, 500, 32, 4, 2, 3)
+    lay = oracle_index(orc, raw, t, P, 8, 4, d1=16)
+    lay = dict(lay, vec_raw=None, vec_t=None)
+    orc.ivf_query(lay, qt[0], qr[0], 5, 2, "ad-split", 2.1, 16)  # split arrays present
+    with pytest.raises(ValueError):
+        orc.ivf_query(lay, qt[0], qr[0], 5, 2, "fd")
