@@ -649,7 +649,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="search", choices=["search", "dco", "transform"])
+    ap.add_argument("--mode", default="search", choices=["search", "dco", "transform", "theory"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--nprobe", type=int, default=0)
     ap.add_argument("--nq", type=int, default=0)
@@ -688,6 +688,10 @@ def main():
             from bench_transform import run_transform
 
             res = run_transform(args, D)
+        elif args.mode == "theory":
+            from bench_theory import run_theory
+
+            res = run_theory(args, D)
         elif sharded and (D.world > 1 or args.force_shard):
             res = run_search_sharded(args, D)
         else:
