@@ -417,7 +417,8 @@ def run_search(args, D: Dist):
         "e2e": {"value": world_q / e2e_total, "unit": "queries/s",
                 "h2d_bytes_per_step": nq * d * 4,
                 "d2h_bytes_per_step": nq * K * (4 + 8) + nq * (4 + 8 + 8)},
-        "gpu_launches": 4 * args.steps,
+        # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, scan
+        "gpu_launches": 5 * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(cfg.key),
                      "traffic_unit": "GB per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
@@ -555,7 +556,8 @@ def run_search_sharded(args, D: Dist):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(cfg.describe(), nprobe=nprobe, nq_total=nq,
                        parallelism=f"list-sharded x{W} + NCCL all-gather + merge"),
-        "gpu_launches": 5 * args.steps + 2 * args.steps,
+        # per step: the 5 search kernels + merge_topk (the two NCCL all-gathers are library kernels)
+        "gpu_launches": 6 * args.steps,
         "scanned_gb_per_step_all_ranks": 4.0 * dims / 1e9,
         "clocks": clk,
     }

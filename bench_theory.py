@@ -48,7 +48,8 @@ def run_theory(args, D):
         "rows": [r._asdict() for r in rows],
         "e2e": {"value": pairs / sec, "unit": "pairs/s", "h2d_bytes_per_step": int(t.nbytes + qt.nbytes),
                 "d2h_bytes_per_step": 0},
-        "gpu_launches": None,
+        # per call: brute-force distances + select (one batch), kth distance, theory kernel
+        "gpu_launches": 4 * args.steps,
     }
     from oracle import load_ref, ref_available
 
