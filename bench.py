@@ -175,6 +175,38 @@ def config_for(args):
     return cfg
 
 
+def large_rotated_dataset(cfg, m, ctx):
+    """Config 5's 1e8 rows, generated on the host, rotated on the device (exact fp64);
+    the host copy and the unrotated device copy are released."""
+    import paper_2303_09855_b200 as ads
+    from paper_2303_09855_b200 import api
+
+    kw = dict(kind=cfg.kind, center_scale=cfg.center_scale, center_lo=cfg.center_lo,
+              center_hi=cfg.center_hi, sigma=cfg.sigma, decay=cfg.decay, assign_mode=cfg.assign_mode)
+    base = api.synth(cfg.n, cfg.d, cfg.components, cfg.seed, 1, **kw)
+    dX = ads.DeviceArray.from_host(ctx, base)
+    del base
+    dT = ads.DeviceArray(ctx, (cfg.n, cfg.d), np.float32)
+    ads.Transform(m, ctx).apply_dataset_device(dX, dT)
+    ctx.sync()
+    dX.free()
+    return dT
+
+
+def device_ground_truth(ads, ctx, dT, qt, K):
+    """Exact top-K of the rotated queries qt over the device-resident rotated rows dT
+    (P is orthogonal, so this is the raw-space neighbour set up to rounding)."""
+    import ctypes as C
+
+    from paper_2303_09855_b200 import _lib as L
+
+    dq = ads.DeviceArray.from_host(ctx, np.ascontiguousarray(qt, np.float32))
+    dg = ads.DeviceArray(ctx, (qt.shape[0], K), np.int32)
+    L.check(L.ads_brute_force_knn_device(ctx.h, C.c_void_p(dT.ptr), dT.shape[0], dT.shape[1],
+                                         C.c_void_p(dq.ptr), qt.shape[0], K, C.c_void_p(dg.ptr)))
+    return dg.to_host()
+
+
 def setup_large(cfg, dev, rank, log):
     """Config 5 (1e8 rows): generate on the host, rotate and build on the device
     (ads_ivf_build_sampled_device), ground truth for the first gt_queries queries
@@ -183,29 +215,16 @@ def setup_large(cfg, dev, rank, log):
     from paper_2303_09855_b200 import configs
 
     t0 = time.time()
-    base, q = configs.generate(cfg, role_base=rank)
+    q = configs.generate_queries(cfg, role_base=rank)
     m = ads.generate_orthogonal(cfg.d, cfg.seed)
     ctx = ads.Context.default(dev)
-    dX = ads.DeviceArray.from_host(ctx, base)
-    del base
-    tr = ads.Transform(m, ctx)
-    dT = ads.DeviceArray(ctx, (cfg.n, cfg.d), np.float32)
-    tr.apply_dataset_device(dX, dT)
-    ctx.sync()
-    dX.free()
+    dT = large_rotated_dataset(cfg, m, ctx)
     t1 = time.time()
     idx = ads.build_ivf_sampled_device(dT, m, cfg.nlist, cfg.seed, 32, cfg.kmeans_iters,
                                        cfg.extra.get("sample", 2_000_000), ctx=ctx)
     t2 = time.time()
     ng = min(cfg.extra.get("gt_queries", 100), q.shape[0])
-    qt = tr.apply_dataset(q[:ng])
-    dq = ads.DeviceArray.from_host(ctx, qt)
-    dg = ads.DeviceArray(ctx, (ng, cfg.K), np.int32)
-    from paper_2303_09855_b200 import _lib as L
-    import ctypes as C
-    L.check(L.ads_brute_force_knn_device(ctx.h, C.c_void_p(dT.ptr), cfg.n, cfg.d, C.c_void_p(dq.ptr), ng, cfg.K,
-                                         C.c_void_p(dg.ptr)))
-    gt = dg.to_host()
+    gt = device_ground_truth(ads, ctx, dT, ads.Transform(m, ctx).apply_dataset(q[:ng]), cfg.K)
     dT.free()
     t3 = time.time()
     log(f"setup: data+rotate {t1 - t0:.1f}s, build_ivf (sampled k-means + certified assignment) "
@@ -486,19 +505,35 @@ def run_search_sharded(args, D: Dist):
     W, K, d = D.world, cfg.K, cfg.d
     torch.cuda.set_device(D.local)
     t0 = time.time()
-    base, _ = configs.generate(cfg, nq=1)
-    qs = np.concatenate([configs.generate(cfg, role_base=r, nq=cfg.nq)[1] for r in range(W)])
+    qs = np.concatenate([configs.generate_queries(cfg, role_base=r, nq=cfg.nq) for r in range(W)])
     nq = qs.shape[0]
     m = ads.generate_orthogonal(d, cfg.seed)
     ctx = ads.Context.default(D.local)
-    t = ads.Transform(m, ctx).apply_dataset(base)
-    full = ads.build_ivf(base, t, m, cfg.nlist, cfg.seed, ads.IvfLayout.kSplit, 32,
-                         max_iters=cfg.kmeans_iters, init=cfg.kmeans_init, ctx=ctx)
-    sizes = np.diff(full.export()["list_off"])
-    owner = partition_lists(sizes, W)
-    local = shard_index(full, owner, D.rank)
-    del full
-    gt = ads.brute_force_knn(base, qs, K, ctx=ctx) if D.rank == 0 else None
+    if cfg.n > 20_000_000:
+        # config 5: every rank builds the same index on its device (seeded, deterministic),
+        # keeps its own lists and drops the rest; ground truth for the first gt_queries
+        dT = large_rotated_dataset(cfg, m, ctx)
+        full = ads.build_ivf_sampled_device(dT, m, cfg.nlist, cfg.seed, 32, cfg.kmeans_iters,
+                                            cfg.extra.get("sample", 2_000_000), ctx=ctx)
+        sizes = np.diff(full.list_offsets())
+        owner = partition_lists(sizes, W)
+        local = shard_index(full, owner, D.rank)
+        del full
+        gt = None
+        if D.rank == 0:
+            ng = min(cfg.extra.get("gt_queries", 100), nq)
+            gt = device_ground_truth(ads, ctx, dT, ads.Transform(m, ctx).apply_dataset(qs[:ng]), K)
+        dT.free()
+    else:
+        base, _ = configs.generate(cfg, nq=1)
+        t = ads.Transform(m, ctx).apply_dataset(base)
+        full = ads.build_ivf(base, t, m, cfg.nlist, cfg.seed, ads.IvfLayout.kSplit, 32,
+                             max_iters=cfg.kmeans_iters, init=cfg.kmeans_init, ctx=ctx)
+        sizes = np.diff(full.list_offsets())
+        owner = partition_lists(sizes, W)
+        local = shard_index(full, owner, D.rank)
+        del full
+        gt = ads.brute_force_knn(base, qs, K, ctx=ctx) if D.rank == 0 else None
     log(f"sharded setup {time.time() - t0:.1f}s: {W} ranks, local rows {local.n} "
         f"(max/min shard rows {np.bincount(owner, weights=sizes).max():.0f}/"
         f"{np.bincount(owner, weights=sizes).min():.0f})")
@@ -563,8 +598,11 @@ def run_search_sharded(args, D: Dist):
     }
     if D.rank == 0:
         ids = oi.cpu().numpy()
+        ngt = min(nq, len(gt))
         res["config"]["recall_at_k"] = float(np.mean([len(np.intersect1d(ids[i][ids[i] >= 0], gt[i]))
-                                                      for i in range(nq)]) / K)
+                                                      for i in range(ngt)]) / K)
+        if ngt < nq:
+            res["config"]["recall_queries"] = ngt
     # e2e: host queries in, merged results out (pinned buffers), same collective path
     qh = ads.PinnedArray((nq, d), np.float32)
     qh.array[:] = qs

@@ -575,6 +575,12 @@ class IvfIndex:
                                g("ids_flat"), g("a1_t"), g("a2_t"), g("a1_raw"), g("a2_raw")))
         return out
 
+    def list_offsets(self) -> np.ndarray:
+        """list_off (k + 1) only, without copying the vectors back."""
+        off = np.empty(self.k_clusters + 1, np.int64)
+        check(L.ads_ivf_export(self.h, None, None, off.ctypes.data, None, None, None, None, None))
+        return off
+
     def probe_order(self, Q: np.ndarray, nprobe: int, transformed: bool = True) -> np.ndarray:
         Q = _f32(Q)
         out = np.empty((Q.shape[0], nprobe), np.int32)
