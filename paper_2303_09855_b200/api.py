@@ -305,16 +305,20 @@ class Transform:
 
 
 _TCACHE: dict = {}
+_TCACHE_LOCK = threading.Lock()
 
 
 def _transform_for(m: TransformMatrix, ctx=None) -> Transform:
+    """The device transform of the most recently used matrix (uploading P once); the
+    cache keeps a reference to m.entries, so its id cannot be reused while cached."""
     key = (id(m.entries), m.dim, (ctx or Context.default()).device)
-    t = _TCACHE.get(key)
-    if t is None or t.m.entries is not m.entries:
-        t = Transform(m, ctx)
-        _TCACHE.clear()
-        _TCACHE[key] = t
-    return t
+    with _TCACHE_LOCK:
+        t = _TCACHE.get(key)
+        if t is None or t.m.entries is not m.entries:
+            t = Transform(m, ctx)
+            _TCACHE.clear()
+            _TCACHE[key] = t
+        return t
 
 
 def apply_dataset(m: TransformMatrix, ds: np.ndarray) -> np.ndarray:  # transform.hpp:58
