@@ -704,8 +704,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--kmeans-init", type=int, default=-1, help="override (profiling runs: 1)")
-    ap.add_argument("--shard", default="lists", choices=["lists", "replicas"],
-                    help="N>1: IVF lists partitioned across GPUs + NCCL all-gather merge, or replicas")
+    ap.add_argument("--shard", default="auto", choices=["auto", "lists", "replicas"],
+                    help="N>1: IVF lists partitioned across GPUs + NCCL all-gather merge, or query-sharded "
+                         "replicas; auto = lists for config 5 (the sharded config), replicas for configs that "
+                         "fit one GPU (SURVEY §8e)")
     ap.add_argument("--dco-n", type=int, default=10_000_000)
     ap.add_argument("--force-shard", action="store_true",
                     help="run the list-sharded path even at N=1 (exercises NCCL + merge)")
@@ -715,6 +717,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.shard == "auto":
+        from paper_2303_09855_b200 import configs as _cf
+
+        args.shard = "lists" if _cf.CONFIGS[args.config].n > 20_000_000 else "replicas"
     sharded = args.impl == "ours" and args.mode == "search" and args.shard == "lists"
     D = Dist("nccl" if sharded else "gloo", force=sharded and args.force_shard)
     try:
