@@ -1,0 +1,66 @@
+"""What list sharding costs at N ranks, measured on one GPU: the index is cut into
+N list shards (LPT on list sizes, as bench.py's sharded path does) and each shard's
+search, the work one rank would do, is run in turn on the same queries.  Reports
+the scanned dims summed over shards (looser local thresholds inflate them) and the
+slowest shard's scan time (the step's critical path), next to the unsharded search.
+No rank waits on another, so one GPU measures each shard's work exactly.
+
+    python tools/shard_inflation.py [config] [N ...]
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import bench
+    import paper_2303_09855_b200 as ads
+    from paper_2303_09855_b200 import configs
+    from paper_2303_09855_b200.shard import partition_lists, shard_index
+
+    cfgid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    ns = [int(v) for v in sys.argv[2:]] or [2, 4, 8]
+    cfg = configs.CONFIGS[cfgid]
+    log = lambda *a: print(*a, file=sys.stderr, flush=True)  # noqa: E731
+    ads_, ctx, base, t, q, m, idx, gt = bench.setup(cfg, 0, 0, log)
+    K, nprobe = cfg.K, cfg.nprobe
+    opts = ads.search_opts(time_stages=True)
+
+    def run(index, reps=3):
+        best, dims = None, None
+        for _ in range(reps):
+            ctx.flush_l2()
+            r = ads.ivf_query_batch(index, None, q, K, nprobe, ads.IvfMode.kAdSplit, opts=opts)
+            ms = float(index.last_timings()[3])
+            best = ms if best is None else min(best, ms)
+            dims = float(r.dims.astype(np.float64).sum())
+        return best, dims
+
+    base_ms, base_dims = run(idx)
+    print(f"config {cfgid}: unsharded scan {base_ms:.2f} ms, dims {base_dims:.4g}")
+    sizes = np.diff(idx.list_offsets())
+    rows = []
+    for n in ns:
+        owner = partition_lists(sizes, n)
+        shard_ms, shard_dims = [], []
+        for rank in range(n):
+            local = shard_index(idx, owner, rank)
+            ms, dims = run(local)
+            shard_ms.append(ms)
+            shard_dims.append(dims)
+            del local
+        infl = sum(shard_dims) / base_dims
+        crit = max(shard_ms)
+        rows.append((n, infl, crit, base_ms / crit / n))
+        print(f"N={n}: dims summed over shards x{infl:.3f} of unsharded; slowest shard scan {crit:.2f} ms "
+              f"(unsharded {base_ms:.2f}); list-sharded weak-scaling efficiency on the scan "
+              f"{base_ms / crit:.2f}/{n} = {base_ms / crit / n:.2f} of ideal")
+    return rows
+
+
+if __name__ == "__main__":
+    main()
