@@ -255,6 +255,14 @@ typedef struct {
     int32_t rotate_mode;   /* when the queries come untransformed (Q_t == NULL): 0 (default) exact
                               fp64 rotation, bit-identical to apply(); 1 the 3xTF32 tensor-core
                               rotation of ads_apply_dataset_tc (~1e-6 |q|; D % 4 == 0, D >= 32) */
+    int32_t probe_lo;      /* scheduler 0: scan only the lists at probe ranks probe_lo .. n_probe-1
+                              (default 0) */
+    const double *r0;      /* scheduler 0, nullable: per-query initial radius (a distance); r starts
+                              at r0[q] and is min(r0[q], heap threshold) at every refresh.  Host
+                              memory for ads_ivf_search, device memory for ads_ivf_search_device.
+                              With probe_lo this is the second wave of the sharded search: probe
+                              ranks [0, w) first, all-reduce (min) of the K-th distances, then
+                              [w, n_probe) from the global bound. */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 

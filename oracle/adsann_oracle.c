@@ -595,28 +595,44 @@ static void heap_offer(heap_t *h, double dist, int32_t id) {
  * position of the first candidate of probe rank waves[j] (j < nwaves). */
 static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                           int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
-                          int64_t step, const int32_t *waves, int32_t nwaves, int32_t *ids,
-                          double *dists, int32_t *count, uint64_t *stats);
+                          int64_t step, int32_t probe_lo, double r0, const int32_t *waves,
+                          int32_t nwaves, int32_t *ids, double *dists, int32_t *count,
+                          uint64_t *stats);
 
 int orc_ivf_query(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                   int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                   int64_t step, int32_t *ids, double *dists, int32_t *count, uint64_t *stats) {
-    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, NULL, 0,
-                          ids, dists, count, stats);
+    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, 0, INFINITY,
+                          NULL, 0, ids, dists, count, stats);
 }
 
 int orc_ivf_query_waves(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                         int32_t nprobe, int mode, double eps0, int32_t delta_d,
                         const int32_t *wave_ranks, int32_t nwaves, int32_t *ids, double *dists,
                         int32_t *count, uint64_t *stats) {
-    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, 1, 1, wave_ranks,
-                          nwaves, ids, dists, count, stats);
+    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, 1, 1, 0, INFINITY,
+                          wave_ranks, nwaves, ids, dists, count, stats);
 }
 
+int orc_ivf_query_ext(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                      int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
+                      int64_t step, int32_t probe_lo, double r0, int32_t *ids, double *dists,
+                      int32_t *count, uint64_t *stats) {
+    if (probe_lo < 0 || probe_lo > nprobe) return fail(1, "ivf_query: probe_lo must be in [0, n_probe]");
+    if (!(r0 >= 0.0)) return fail(1, "ivf_query: the initial radius must be >= 0");
+    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, probe_lo, r0,
+                          NULL, 0, ids, dists, count, stats);
+}
+
+/* probe_lo / r0 (the sharded search's second wave): only the lists at probe
+ * ranks probe_lo .. n_probe-1 are scanned, and r starts at the bound r0 and
+ * is min(r0, heap threshold) at every refresh (the heap's max never exceeds
+ * r0 once full, since every positive satisfied dist <= r). */
 static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                           int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
-                          int64_t step, const int32_t *waves, int32_t nwaves, int32_t *ids,
-                          double *dists, int32_t *count, uint64_t *stats) {
+                          int64_t step, int32_t probe_lo, double r0, const int32_t *waves,
+                          int32_t nwaves, int32_t *ids, double *dists, int32_t *count,
+                          uint64_t *stats) {
     /* ivf.cpp:299-307 */
     if (K < 1) return fail(1, "ivf_query: K must be >= 1");
     if (nprobe < 1 || nprobe > idx->k_clusters)
@@ -646,11 +662,11 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
 
     heap_t heap = {malloc(sizeof(pair_t) * (size_t)K), 0, K};
     int64_t total = 0;
-    for (int32_t i = 0; i < nprobe; ++i) total += idx->list_off[probes[i] + 1] - idx->list_off[probes[i]];
+    for (int32_t i = probe_lo; i < nprobe; ++i) total += idx->list_off[probes[i] + 1] - idx->list_off[probes[i]];
     pair_t *pending = malloc(sizeof(pair_t) * (size_t)(total > 0 ? total : 1));
     int64_t npend = 0;
     uint64_t dims = 0;
-    double r = INFINITY;
+    double r = r0;
 
     /* Split modes precompute the A1 prefix of every candidate first
      * (ivf.cpp:366-386); contiguous modes scan in one pass. */
@@ -659,7 +675,7 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
         prefix = malloc(sizeof(double) * (size_t)(total > 0 ? total : 1));
         const float *a1 = mode == 3 ? idx->a1_t : idx->a1_raw;
         int64_t i = 0;
-        for (int32_t pi = 0; pi < nprobe; ++pi)
+        for (int32_t pi = probe_lo; pi < nprobe; ++pi)
             for (int64_t p = idx->list_off[probes[pi]]; p < idx->list_off[probes[pi] + 1]; ++p, ++i) {
                 double s = 0.0;
                 for (int32_t j = 0; j < d1; ++j) {
@@ -677,20 +693,21 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
         mark = calloc((size_t)(total + 1), 1);
         int64_t pos = 0;
         int32_t wj = 0;
-        for (int32_t pi = 0; pi < nprobe; ++pi) {
+        for (int32_t pi = probe_lo; pi < nprobe; ++pi) {
             while (wj < nwaves && waves[wj] < pi) ++wj;
             if (wj < nwaves && waves[wj] == pi) mark[pos] = 1;
             pos += idx->list_off[probes[pi] + 1] - idx->list_off[probes[pi]];
         }
     }
     int64_t i = 0;
-    for (int32_t pi = 0; pi < nprobe; ++pi) {
+    for (int32_t pi = probe_lo; pi < nprobe; ++pi) {
         const int32_t c = probes[pi];
         for (int64_t p = idx->list_off[c]; p < idx->list_off[c + 1]; ++p, ++i) {
             if (i == 0 || (waves ? mark[i] : (i >= first && (i - first) % step == 0))) {
                 for (int64_t j = 0; j < npend; ++j) heap_offer(&heap, pending[j].dist, pending[j].id);
                 npend = 0;
-                r = heap_threshold(&heap); /* ivf.cpp:331, 391 */
+                const double ht = heap_threshold(&heap); /* ivf.cpp:331, 391 */
+                r = ht < r0 ? ht : r0;
             }
             const int32_t id = idx->ids_flat[p];
             if (!split_mode) {

@@ -117,6 +117,12 @@ int orc_ivf_query_waves(const orc_ivf *idx, const float *q_t, const float *q_raw
                         int32_t *count, uint64_t *stats);
 
 /* probe_order, ivf.cpp:283-292 */
+/* ivf_query restricted to probe ranks [probe_lo, n_probe) with the radius
+ * starting at r0 (+inf: the plain query); the sharded search's second wave. */
+int orc_ivf_query_ext(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                      int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
+                      int64_t step, int32_t probe_lo, double r0, int32_t *ids, double *dists,
+                      int32_t *count, uint64_t *stats);
 int orc_probe_order(const float *centroids, int32_t L, int32_t d, const float *q,
                     int32_t nprobe, int32_t *order);
 

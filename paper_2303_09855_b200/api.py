@@ -506,7 +506,7 @@ def search_shape(d: int, step: int = 0, warps_per_cta: int = 0) -> tuple:
 def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
                 tile: int = 64, query_order: int = 0, coarse_mode: int = 0,
-                rotate_mode: int = 0) -> L.SearchOpts:
+                rotate_mode: int = 0, probe_lo: int = 0, r0=None) -> L.SearchOpts:
     """scheduler 0: query-major, first/step in candidates; scheduler 1: list-major
     waves, first/step in probed lists (see include/adsann_b200.h)."""
     o = L.SearchOpts()
@@ -515,6 +515,14 @@ def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_p
         first, step, warps_per_cta, queries_per_cta, ctas_per_sm, int(time_stages))
     o.scheduler, o.tile, o.query_order, o.coarse_mode = scheduler, tile, query_order, coarse_mode
     o.rotate_mode = rotate_mode
+    o.probe_lo = probe_lo
+    if r0 is not None:  # per-query initial radii (host array for the host API)
+        if isinstance(r0, DeviceArray):
+            o.r0 = r0.ptr
+        else:
+            r0 = np.ascontiguousarray(r0, np.float64)
+            o.r0 = r0.ctypes.data
+        o._r0_keep = r0  # keep the buffer alive with the options
     return o
 
 

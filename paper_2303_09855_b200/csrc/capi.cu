@@ -141,6 +141,7 @@ struct ads_ivf {
     std::map<PlanKey, std::unique_ptr<DevSegPlan>> plans;
     DevBuf dist, probes, qrot, qin_t, qin_raw, o_ids, o_dists, o_cnt, o_dims, o_cand;
     DevBuf ph, pl, qh, ql;  // rotate_mode 1: P and the queries as TF32 hi/lo pairs
+    DevBuf r0buf;           // host-API copy of opts.r0
     bool p_split = false;
     ListMajorScratch lm;
     int32_t* chain_rank = nullptr;  // L2-locality rank of each list (host chain over centroids)
@@ -1064,6 +1065,8 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->query_order = 0;
     o->coarse_mode = 0;
     o->rotate_mode = 0;
+    o->probe_lo = 0;
+    o->r0 = nullptr;
 }
 
 namespace {
@@ -1126,6 +1129,8 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     if (o.warps_per_cta <= 0) o.warps_per_cta = o.scheduler == 1 ? 8 : (x->d <= 256 ? 4 : 10);
     if (o.step <= 0) o.step = o.scheduler == 1 ? 1 : 64 * static_cast<int64_t>(o.warps_per_cta);
     require(o.warps_per_cta >= 1 && o.warps_per_cta <= 32, "search: warps_per_cta in [1, 32]");
+    require(o.probe_lo >= 0 && o.probe_lo <= nprobe, "ivf_query: probe_lo must be in [0, n_probe]");
+    require(o.scheduler == 0 || (o.probe_lo == 0 && !o.r0), "search: probe_lo / r0 need scheduler 0");
     require(o.queries_per_cta >= 1 && o.queries_per_cta <= 16, "search: queries_per_cta in [1, 16]");
     cudaStream_t st = x->ctx->stream;
     const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
@@ -1185,6 +1190,8 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.nq = nq;
     a.probes = probes;
     a.nprobe = nprobe;
+    a.probe_lo = o.probe_lo;
+    a.r0 = o.r0;
     a.K = K;
     a.final_fd = mode == ADS_MODE_FD;
     a.segs = plan.segs;
@@ -1292,8 +1299,16 @@ int ads_ivf_search(ads_ivf* x, const float* Qt, const float* Qraw, int32_t nq, i
         int32_t* dc = x->o_cnt.get<int32_t>(nq);
         uint64_t* dm = x->o_dims.get<uint64_t>(nq);
         uint64_t* dn = x->o_cand.get<uint64_t>(nq);
+        ads_search_opts o;
+        ads_search_opts_default(&o);
+        if (opts) o = *opts;
+        if (o.r0 && nq > 0) {  // host radii -> device
+            double* dr = x->r0buf.get<double>(nq);
+            ADS_CUDA(cudaMemcpyAsync(dr, o.r0, sizeof(double) * nq, cudaMemcpyHostToDevice, st));
+            o.r0 = dr;
+        }
         if (nq > 0)
-            search_device(x, dqt, dqr, nq, K, nprobe, mode, eps0, dd, opts, di, dd_, dc, dm, dn);
+            search_device(x, dqt, dqr, nq, K, nprobe, mode, eps0, dd, &o, di, dd_, dc, dm, dn);
         auto down = [&](void* h, const void* d, size_t bytes) {
             if (h && bytes) ADS_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
         };

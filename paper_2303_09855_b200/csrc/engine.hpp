@@ -81,6 +81,8 @@ struct SearchLaunch {
     int nq;
     const int32_t* probes;  // nq x nprobe
     int nprobe;
+    int probe_lo;           // scan probe ranks probe_lo .. nprobe-1
+    const double* r0;       // nullable: per-query initial radius (device)
     int K;
     int final_fd;      // 1: sqrt(s) <= r (kFd), 0: s <= r^2
     const Seg* segs;

@@ -469,8 +469,9 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
     const char* gbase = lane_base16(a.a1);
     // stream index -> flat position (last probed list with pre[l] <= i)
+    const int nl = a.nprobe - a.probe_lo;  // lists scanned per query
     auto locate = [&](int i) {
-        int l = 0, h = a.nprobe - 1;
+        int l = 0, h = nl - 1;
         while (l < h) {
             const int mid = (l + h + 1) >> 1;
             if (pre[mid] <= i) l = mid;
@@ -494,22 +495,25 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
             sh.stop = w >= a.nq;
             sh.q = sh.stop ? w : (a.order ? a.order[w] : w);
             sh.cnt = 0;
-            sh.r = kInf;
-            sh.r_sq = kInf;
+            // the radius starts at the caller's bound (the sharded search's second
+            // wave) or +inf; thresholds follow it until the heap is full
+            const double r0 = (!sh.stop && a.r0) ? a.r0[sh.q] : kInf;
+            sh.r = r0;
+            sh.r_sq = __dmul_rn(r0, r0);
             sh.dims = 0;
         }
         __syncthreads();
         if (sh.stop) break;
         const int qi = sh.q;
         stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
-        for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = kInf;
+        for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = __dmul_rn(tfac[i], sh.r_sq);
         if (warp == 0) {  // probed lists -> stream prefix offsets
             int carry = 0;
-            for (int base = 0; base < a.nprobe; base += 32) {
+            for (int base = 0; base < nl; base += 32) {  // probe ranks probe_lo .. nprobe-1
                 const int i = base + static_cast<int>(lane);
                 int len = 0;
-                if (i < a.nprobe) {
-                    const int p = a.probes[static_cast<int64_t>(qi) * a.nprobe + i];
+                if (i < nl) {
+                    const int p = a.probes[static_cast<int64_t>(qi) * a.nprobe + a.probe_lo + i];
                     const int64_t s0 = a.list_off[p];
                     lstart[i] = static_cast<int32_t>(s0);
                     len = static_cast<int>(a.list_off[p + 1] - s0);
@@ -520,7 +524,7 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                     const int v = __shfl_up_sync(kFull, incl, o);
                     if (static_cast<int>(lane) >= o) incl += v;
                 }
-                if (i < a.nprobe) pre[i + 1] = carry + incl;
+                if (i < nl) pre[i + 1] = carry + incl;
                 carry += __shfl_sync(kFull, incl, 31);
             }
             if (lane == 0) {

@@ -468,3 +468,29 @@ def test_ivf_empty_lists_and_empty_streams(eng, orc):
         if nprobe == 1:
             assert empty.any()
         assert (res.ids[empty] == -1).all() and np.isnan(res.dists[empty]).all()
+
+
+@pytest.mark.parametrize("probe_lo,rscale", [(0, 1.0), (3, 1.0), (3, 0.5), (5, 2.0), (17, 1.3), (0, 0.0)])
+def test_ivf_probe_range_and_initial_radius(eng, orc, probe_lo, rscale):
+    """probe_lo / r0 (the sharded search's second wave): only probe ranks
+    [probe_lo, nprobe) are scanned and r starts at r0[q] == the oracle, bit for bit."""
+    raw, t, qr, qt, P = make_fixture(orc, 4000, 64, 16, 30, 191)
+    lay = oracle_index(orc, raw, t, P, 40, 193, d1=32)
+    idx = gpu_index(eng, lay, P)
+    K, nprobe = 10, 17
+    full = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, first=0, step=64)
+    r0 = np.where(full.counts == K, full.dists[:, K - 1], np.inf) * rscale
+    r0 = np.where(np.isnan(r0), np.inf, r0)
+    for mode in ("ad-split", "ad", "fd", "pd-split"):
+        res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]),
+                                  opts=eng.search_opts(first=0, step=64, probe_lo=probe_lo, r0=r0))
+        for i in range(qt.shape[0]):
+            ids, dists, stats = orc.ivf_query(lay, qt[i], qr[i], K, nprobe, mode, 2.1, 32, K, 64,
+                                              probe_lo=probe_lo, r0=float(r0[i]))
+            c = int(res.counts[i])
+            assert c == len(ids), (mode, i)
+            np.testing.assert_array_equal(res.ids[i, :c], ids, err_msg=f"{mode} q={i}")
+            np.testing.assert_array_equal(res.dists[i, :c], dists)
+            assert int(res.dims[i]) == int(stats[0]), (mode, i)
+    with pytest.raises(ValueError):
+        eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, opts=eng.search_opts(probe_lo=nprobe + 1))
