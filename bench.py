@@ -541,29 +541,50 @@ def run_search_sharded(args, D: Dist):
     dev = torch.device("cuda", D.local)
     stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
     dq = torch.from_numpy(qs).to(dev)
-    li = torch.empty((nq, K), dtype=torch.int32, device=dev)
-    ld = torch.empty((nq, K), dtype=torch.float64, device=dev)
-    lc = torch.empty((nq,), dtype=torch.int32, device=dev)
-    lm = torch.empty((nq,), dtype=torch.int64, device=dev)
-    ln = torch.empty((nq,), dtype=torch.int64, device=dev)
-    gi = torch.empty((W, nq, K), dtype=torch.int32, device=dev)
-    gd = torch.empty((W, nq, K), dtype=torch.float64, device=dev)
+    # two waves with the threshold exchange of SURVEY §8e (--waves 0 disables it): probe ranks
+    # [0, w) on every rank, an all-reduce (min) of the per-query K-th distances (an upper bound on
+    # the global K-th distance), then ranks [w, nprobe) starting from that bound; the merge keeps
+    # the K smallest (dist, id) pairs of the 2 x N local results
+    w = args.waves if args.waves >= 0 else (max(1, nprobe // 8) if W > 1 else 0)
+    w = w if 0 < w < nprobe else 0
+    G = 2 * W if w else W
+    li = torch.empty((G // W, nq, K), dtype=torch.int32, device=dev)
+    ld = torch.empty((G // W, nq, K), dtype=torch.float64, device=dev)
+    lc = torch.empty((G // W, nq), dtype=torch.int32, device=dev)
+    lm = torch.empty((G // W, nq), dtype=torch.int64, device=dev)
+    ln = torch.empty((G // W, nq), dtype=torch.int64, device=dev)
+    gi = torch.empty((W, G // W, nq, K), dtype=torch.int32, device=dev)
+    gd = torch.empty((W, G // W, nq, K), dtype=torch.float64, device=dev)
     oi = torch.empty((nq, K), dtype=torch.int32, device=dev)
     od = torch.empty((nq, K), dtype=torch.float64, device=dev)
     oc = torch.empty((nq,), dtype=torch.int32, device=dev)
+    rb = torch.empty((nq,), dtype=torch.float64, device=dev)
     opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True)
+    opts2 = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True,
+                            probe_lo=w)
+    opts2.r0 = rb.data_ptr()
     mode = ads.IvfMode.kAdSplit
     torch.cuda.synchronize()
 
+    def search(o, np_, k):
+        L.check(L.ads_ivf_search_device(local.h, None, C.c_void_p(dq.data_ptr()), nq, K, np_,
+                                        int(mode), 2.1, 32, C.byref(o), C.c_void_p(li[k].data_ptr()),
+                                        C.c_void_p(ld[k].data_ptr()), C.c_void_p(lc[k].data_ptr()),
+                                        C.c_void_p(lm[k].data_ptr()), C.c_void_p(ln[k].data_ptr())))
+
     def step():
-        L.check(L.ads_ivf_search_device(local.h, None, C.c_void_p(dq.data_ptr()), nq, K, nprobe,
-                                        int(mode), 2.1, 32, C.byref(opts), C.c_void_p(li.data_ptr()),
-                                        C.c_void_p(ld.data_ptr()), C.c_void_p(lc.data_ptr()),
-                                        C.c_void_p(lm.data_ptr()), C.c_void_p(ln.data_ptr())))
+        if w:
+            search(opts, w, 0)
+            with torch.cuda.stream(stream):
+                torch.where(lc[0] == K, ld[0][:, K - 1], torch.full_like(rb, float("inf")), out=rb)
+                D.pg.all_reduce(rb, op=D.pg.ReduceOp.MIN, group=D.nccl)
+            search(opts2, nprobe, 1)
+        else:
+            search(opts, nprobe, 0)
         with torch.cuda.stream(stream):
             D.pg.all_gather_into_tensor(gi, li, group=D.nccl)
             D.pg.all_gather_into_tensor(gd, ld, group=D.nccl)
-        merge_topk_device(ctx, gd.data_ptr(), gi.data_ptr(), W, nq, K, oi.data_ptr(),
+        merge_topk_device(ctx, gd.data_ptr(), gi.data_ptr(), G, nq, K, oi.data_ptr(),
                           od.data_ptr(), oc.data_ptr())
 
     for _ in range(args.warmup):
@@ -590,9 +611,11 @@ def run_search_sharded(args, D: Dist):
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(cfg.describe(), nprobe=nprobe, nq_total=nq,
-                       parallelism=f"list-sharded x{W} + NCCL all-gather + merge"),
-        # per step: the 5 search kernels + merge_topk (the two NCCL all-gathers are library kernels)
-        "gpu_launches": 6 * args.steps,
+                       parallelism=f"list-sharded x{W} + NCCL all-gather + merge",
+                       threshold_exchange={"first_wave_probes": w} if w else None),
+        # per step: 5 search kernels per wave + merge_topk (NCCL collectives and the torch.where
+        # of the exchange are library kernels)
+        "gpu_launches": (11 if w else 6) * args.steps,
         "scanned_gb_per_step_all_ranks": 4.0 * dims / 1e9,
         "clocks": clk,
     }
@@ -709,6 +732,9 @@ def main():
                          "replicas; auto = lists for config 5 (the sharded config), replicas for configs that "
                          "fit one GPU (SURVEY §8e)")
     ap.add_argument("--dco-n", type=int, default=10_000_000)
+    ap.add_argument("--waves", type=int, default=-1,
+                    help="list-sharded search: probe ranks of the first wave before the threshold "
+                         "all-reduce (-1: nprobe/8 when N > 1, else one wave; 0: one wave, no exchange)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the list-sharded path even at N=1 (exercises NCCL + merge)")
     ap.add_argument("--kmeans-iters", type=int, default=0)
@@ -720,7 +746,7 @@ def main():
     if args.shard == "auto":
         from paper_2303_09855_b200 import configs as _cf
 
-        args.shard = "lists" if _cf.CONFIGS[args.config].n > 20_000_000 else "replicas"
+        args.shard = "lists" if (args.force_shard or _cf.CONFIGS[args.config].n > 20_000_000) else "replicas"
     sharded = args.impl == "ours" and args.mode == "search" and args.shard == "lists"
     D = Dist("nccl" if sharded else "gloo", force=sharded and args.force_shard)
     try:
