@@ -36,8 +36,23 @@ def run(rank, world, port, outdir):
     dist.all_gather(gd, torch.from_numpy(dists))
     all_ids = np.stack([x.numpy() for x in gi])
     all_d = np.stack([x.numpy() for x in gd])
+    # the threshold exchange (bench.py's list-sharded step for N > 1): wave 1 over probe
+    # ranks [0, w), all-reduce (min) of the K-th distances, wave 2 over [w, nprobe) from it
+    from shard_helpers import kth_distance
+
+    w = 3
+    i1, d1, m1 = shard_search_oracle(orc, sub, qt, qr, K, w, "ad-split", K, 64)
+    R = torch.from_numpy(kth_distance(d1, K))
+    dist.all_reduce(R, op=dist.ReduceOp.MIN)
+    i2, d2, m2 = shard_search_oracle(orc, sub, qt, qr, K, nprobe, "ad-split", K, 64, probe_lo=w, r0=R.numpy())
+    wi = [torch.zeros((2,) + ids.shape, dtype=torch.int32) for _ in range(world)]
+    wd = [torch.zeros((2,) + dists.shape, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(wi, torch.from_numpy(np.stack([i1, i2])))
+    dist.all_gather(wd, torch.from_numpy(np.stack([d1, d2])))
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), ids=all_ids, dists=all_d, owner=owner,
-             dims=dims)
+             dims=dims, R=R.numpy(), wave_ids=np.stack([x.numpy() for x in wi]).reshape(-1, *ids.shape),
+             wave_dists=np.stack([x.numpy() for x in wd]).reshape(-1, *dists.shape),
+             wave_dims=m1 + m2)
     dist.barrier()
     dist.destroy_process_group()
 

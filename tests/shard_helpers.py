@@ -34,12 +34,19 @@ def merge_ref(dists, ids, K):
     return out_i, out_d
 
 
-def shard_search_oracle(orc, lay, qt, qr, K, nprobe, mode, first, step):
+def shard_search_oracle(orc, lay, qt, qr, K, nprobe, mode, first, step, probe_lo=0, r0=None):
     nq = qt.shape[0]
     ids = np.full((nq, K), -1, np.int32)
     dists = np.full((nq, K), np.nan)
     dims = np.zeros(nq, np.uint64)
     for i in range(nq):
-        a, b, s = orc.ivf_query(lay, qt[i], qr[i], K, nprobe, mode, 2.1, 32, first, step)
+        a, b, s = orc.ivf_query(lay, qt[i], qr[i], K, nprobe, mode, 2.1, 32, first, step,
+                                probe_lo=probe_lo, r0=float("inf") if r0 is None else float(r0[i]))
         ids[i, :len(a)], dists[i, :len(b)], dims[i] = a, b, s[0]
     return ids, dists, dims
+
+
+def kth_distance(dists, K):
+    """Per-query K-th distance of a local top-K (+inf when fewer than K were found)."""
+    d = dists[:, K - 1]
+    return np.where(np.isnan(d), np.inf, d)

@@ -64,3 +64,13 @@ def test_two_rank_gloo_sharded_search(tmp_path, orc):
                 exact = np.sqrt(orc.scan_kernel(1, t[merged_i[q, j]], qt[q], 32, 0, 0.0, np.inf,
                                                 2.1, 32, False)[1])
                 assert merged_d[q, j] == exact
+
+    # threshold exchange: every rank holds the same bound R, which bounds the merged
+    # K-th distance from above; the merged result keeps the one-wave recall
+    np.testing.assert_array_equal(r0["R"], r1["R"])
+    np.testing.assert_array_equal(r0["wave_ids"], r1["wave_ids"])
+    ex_i, ex_d = merge_ref(r0["wave_dists"], r0["wave_ids"], 10)
+    full = ~np.isnan(ex_d[:, -1])
+    assert (ex_d[full, -1] <= r0["R"][full]).all()
+    assert rec(ex_i) >= rec(merged_i) - 0.02
+    assert r0["wave_dims"].sum() + r1["wave_dims"].sum() <= r0["dims"].sum() + r1["dims"].sum()
