@@ -439,7 +439,8 @@ def run_search(args, D: Dist):
         # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, scan
         "gpu_launches": 5 * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(cfg.key),
+                     "frac": achieved / peaks["hbm_gbs"], "frac_vs_nominal_8000": achieved / 8000.0,
+                     "traffic": ncu_traffic(cfg.key),
                      "traffic_unit": "GB per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
                      "kernel": "ivf_search_kernel<4>", "peak_source": peaks["source"] + ", copy (burst)",
                      "algorithmic_bytes_per_launch": scanned,

@@ -117,6 +117,7 @@ def run_dco(args, D):
         "roofline": {"bound": "hbm", "achieved": scanned / (float(np.mean(ms)) / 1e3) / 1e9,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": scanned / (float(np.mean(ms)) / 1e3) / 1e9 / peaks["hbm_gbs"],
+                     "frac_vs_nominal_8000": scanned / (float(np.mean(ms)) / 1e3) / 1e9 / 8000.0,
                      "traffic": ncu_traffic("cfg4-dco-10M-d256") if n >= 10_000_000 else None,
                      "traffic_unit": "GB per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
                      "kernel": "dco_fixed_kernel<4>",
