@@ -89,7 +89,6 @@ struct SearchLaunch {
     const double* tfac;
     int nseg, ntest, vec;
     int full;          // every segment is 32 floats (no per-line length shuffle)
-    int f32;           // certified fp32 walk + exact fp64 re-walk of undecided candidates (full only)
     int64_t first, step;
     int warps;         // per CTA
     int slots;         // queries served concurrently per CTA

@@ -16,7 +16,6 @@
 //                        with the reference's strict rule (ivf.cpp:273-280),
 //                        then thr[t] = factor[d_t] * r^2 is rebuilt.
 #include <cfloat>
-#include <type_traits>
 
 #include <cub/cub.cuh>
 
@@ -439,22 +438,8 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
     return true;
 }
 
-// Bound factors of the certified fp32 walk at depth d (terms accumulated):
-// with S the exact sum, |s32 - S| <= g32 S + nabs and |s64 - S| <= g64 S,
-// g(n, u) = n u / (1 - n u), n = d + 2 (difference, square, d additions),
-// nabs covering fp32 underflow.  lo/hi absorb the rounding of the test's own
-// two fp64 operations (the 1% widening of g32 dwarfs it).
-__device__ __forceinline__ double2 f32_band(int d) {
-    const double n = d + 2;
-    const double g32 = 1.01 * n * 0x1p-24 / (1.0 - n * 0x1p-24);
-    const double g64 = 1.01 * n * 0x1p-53 / (1.0 - n * 0x1p-53);
-    return make_double2((1.0 - g64) / (1.0 + g32) * (1.0 - 0x1p-50), (1.0 + g64) / (1.0 - g32) * (1.0 + 0x1p-50));
-}
-
-template <int VEC, bool FULL, bool F32 = false>
+template <int VEC, bool FULL>
 __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
-    static_assert(!F32 || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
-    using acc_t = typename std::conditional<F32, float, double>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SearchShared sh;
     const int nwarps = blockDim.x >> 5;
@@ -473,22 +458,11 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     int32_t* pend_i = topi + a.K;
     int32_t* pre = pend_i + chunk_cap;
     unsigned* pflag = reinterpret_cast<unsigned*>(pre + a.nprobe + 1);
-    // F32: undecided slots of the chunk; the query staged as fp32 and the
-    // per-test band factors share qseg's slot
-    unsigned* vflag = pflag + ((chunk_cap + 31) >> 5);
-    float* qsegf = reinterpret_cast<float*>(qseg);
-    double2* gband = reinterpret_cast<double2*>(qsegf + a.nseg * kQPitchF);
-    const double2 band_d = f32_band(a.D);
-    const double nabs = (a.D + 2) * 0x1p-148;
 
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     float* wbuf = wbuf_all + warp * 1024;
-    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) {
-        const Seg sg = a.segs[i];
-        segs[i] = sg;
-        if (F32 && sg.test >= 0) gband[sg.test] = f32_band(sg.col + sg.len);
-    }
+    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
     for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) tfac[i] = a.tfac[i];
     // VEC=4 line descriptor = pos * stride + column offset, 16-byte units from a.a1
     const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
@@ -531,8 +505,7 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
         __syncthreads();
         if (sh.stop) break;
         const int qi = sh.q;
-        if constexpr (F32) stage_query_f32(qsegf, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
-        else stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
         for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = __dmul_rn(tfac[i], sh.r_sq);
         if (warp == 0) {  // probed lists -> stream prefix offsets
             int carry = 0;
@@ -572,31 +545,18 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
             for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) cpos[sl] = locate(lo + sl);
             if (threadIdx.x == 0) {
-                // F32 with no finite radius: nothing to claim (see `open` below)
-                sh.next = (F32 && !(sh.r_sq < kInf)) ? hi : lo;
+                sh.next = lo;
                 sh.pnext = 0;
             }
-            const double r = sh.r, r_sq = sh.r_sq;
-            // F32 with no finite radius yet: every candidate reaches d == D
-            // undecided, so the chunk goes straight to the exact re-walk
-            const bool open = F32 && !(r_sq < kInf);
-            for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) {
-                pflag[w] = 0;
-                if constexpr (F32) {
-                    const int rem = hi - lo - w * 32;
-                    vflag[w] = open ? (rem >= 32 ? ~0u : (1u << rem) - 1u) : 0u;
-                }
-            }
+            for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
             __syncthreads();
+            const double r = sh.r, r_sq = sh.r_sq;
             const int pc = sh.pcount[j & 1];  // [lo, lo + pc) carry their prefix in pre_cur
-            const bool can_pre = nseg0 > 0 && nhi > hi && !open;
-            // F32 final test: certainly negative above rfin (kFd: sqrt(s) > r
-            // is certain once s > r_sq (1 + 2^-48))
-            const double rfin = a.final_fd ? __dmul_rn(r_sq, 1.0 + 0x1p-47) : r_sq;
+            const bool can_pre = nseg0 > 0 && nhi > hi;
 
             int cand = -1, seg = 0, pos = 0;
             bool prew = false;  // lane holds a next-chunk candidate's untested prefix
-            acc_t s = 0.0;
+            double s = 0.0;
             for (;;) {
                 unsigned need = __ballot_sync(kFull, cand < 0);
                 if (need) {
@@ -611,7 +571,7 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                             prew = false;
                             if (i - lo < pc) {
                                 seg = nseg0;
-                                s = static_cast<acc_t>(pre_cur[i - lo]);
+                                s = pre_cur[i - lo];
                             } else {
                                 seg = 0;
                                 s = 0.0;
@@ -653,36 +613,10 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 cp_async_wait_group<0>();
                 __syncwarp();
                 if (cand >= 0) {
-                    if constexpr (F32) s = accumulate_line_f32(wbuf, qsegf + seg * kQPitchF, s);
-                    else s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                    s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
                     if (prew) {
                         if (seg + 1 == nseg0) {
                             pre_nxt[cand] = s;
-                            cand = -1;
-                        } else {
-                            ++seg;
-                        }
-                    } else if constexpr (F32) {
-                        // decide only what the band proves; the rest is re-walked exactly
-                        const double sd = s;
-                        int verdict = 0;  // 1 reject, 2 undecided, 3 certainly negative at D
-                        if (sg.test >= 0) {
-                            const double t = thr[sg.test];
-                            const double2 g = gband[sg.test];
-                            if (__dmul_rn(sd - nabs, g.x) > t) verdict = 1;
-                            else if (!(__dmul_rn(sd + nabs, g.y) <= t)) verdict = 2;
-                        }
-                        if (verdict == 0 && seg == a.nseg - 1)
-                            verdict = __dmul_rn(sd - nabs, band_d.x) > rfin ? 3 : 2;
-                        if (verdict == 1) {
-                            my_dims += static_cast<unsigned long long>(sg.col + sg.len);
-                            cand = -1;
-                        } else if (verdict == 3) {
-                            my_dims += static_cast<unsigned long long>(a.D);
-                            cand = -1;
-                        } else if (verdict == 2) {
-                            const int slot = cand - lo;
-                            atomicOr(&vflag[slot >> 5], 1u << (slot & 31));
                             cand = -1;
                         } else {
                             ++seg;
@@ -707,55 +641,6 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 }
             }
             __syncthreads();
-            if constexpr (F32) {
-                // exact re-walk of the undecided slots, one thread each, in the
-                // reference's order and arithmetic (dco.hpp:130-150)
-                const int nw = (hi - lo + 31) >> 5;
-                int nv = 0;
-                for (int w = 0; w < nw; ++w) nv += __popc(vflag[w]);
-                for (int k = threadIdx.x; k < nv; k += blockDim.x) {
-                    int w = 0, c = k;
-                    for (;; ++w) {
-                        const int p = __popc(vflag[w]);
-                        if (c < p) break;
-                        c -= p;
-                    }
-                    unsigned bits = vflag[w];
-                    for (; c > 0; --c) bits &= bits - 1;
-                    const int slot = w * 32 + __ffs(bits) - 1;
-                    const int64_t pos = cpos[slot];
-                    double se = 0.0;
-                    for (int g = 0; g < a.nseg; ++g) {
-                        const Seg sg = segs[g];
-                        const float* src = sg.arr == 0 ? a.a1 + pos * a.d1 + sg.col
-                                                       : a.a2 + pos * (a.D - a.d1) + (sg.col - a.d1);
-                        const float* qq = qsegf + g * kQPitchF;
-#pragma unroll
-                        for (int c4 = 0; c4 < 8; ++c4) {
-                            const float4 v = __ldg(reinterpret_cast<const float4*>(src) + c4);
-                            const float4 qv = *reinterpret_cast<const float4*>(qq + c4 * 4);
-                            se = sq_diff_acc(se, v.x, static_cast<double>(qv.x));
-                            se = sq_diff_acc(se, v.y, static_cast<double>(qv.y));
-                            se = sq_diff_acc(se, v.z, static_cast<double>(qv.z));
-                            se = sq_diff_acc(se, v.w, static_cast<double>(qv.w));
-                        }
-                        if (sg.test >= 0 && se > thr[sg.test]) {  // dco.hpp:141
-                            my_dims += static_cast<unsigned long long>(sg.col + sg.len);
-                            break;
-                        }
-                        if (g == a.nseg - 1) {  // dco.hpp:145; ivf.cpp:335-338
-                            my_dims += static_cast<unsigned long long>(a.D);
-                            const double dist = __dsqrt_rn(se);
-                            if (a.final_fd ? dist <= r : se <= r_sq) {
-                                pend_d[slot] = dist;
-                                pend_i[slot] = a.ids[pos];
-                                atomicOr(&pflag[slot >> 5], 1u << (slot & 31));
-                            }
-                        }
-                    }
-                }
-                __syncthreads();
-            }
             // offer the chunk's positives in candidate order: few -> one warp,
             // many -> the whole CTA, ties or oversize -> one by one
             const int n = hi - lo;
@@ -820,7 +705,7 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     b += sizeof(int32_t) * (a.nprobe + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + chunk_cap + a.nprobe + 1);
-    b += sizeof(unsigned) * ((chunk_cap + 31) / 32) * (a.f32 ? 2 : 1);
+    b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
     return b;
 }
 
@@ -882,9 +767,7 @@ void launch_ivf_search(const SearchLaunch& a_in, cudaStream_t st) {
     if (cap64 > 16384) throw std::invalid_argument("search: threshold refresh interval too long (max 16384)");
     const int cap = static_cast<int>(cap64);
     const size_t smem = search_smem(a, cap);
-    if (a.f32 && !(a.vec == 4 && a.full)) a.f32 = 0;
-    auto kern = a.vec == 4 ? (a.full ? (a.f32 ? ivf_search_kernel<4, true, true> : ivf_search_kernel<4, true>)
-                                     : ivf_search_kernel<4, false>)
+    auto kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
                            : ivf_search_kernel<1, false>;
     ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
