@@ -460,6 +460,32 @@ def run_search(args, D: Dist):
         else:
             cb, _, _ = cpu_baseline_reference(cfg, base, t, m, idx, q, gt, nprobe, args.cpu_budget, log)
             res["cpu_baseline"] = cb
+    if D.rank == 0 and args.mode == "search":
+        # the GPU's own FDScanning (kFd: full fp64 distances over the raw vectors) on the
+        # same index, queries and nprobe, next to the reference's CPU FD above
+        try:
+            fd_opts = ads.search_opts(time_stages=True)
+            ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kFd, opts=fd_opts)
+            fms, fscan = [], []
+            for _ in range(3):
+                ctx.flush_l2()
+                ctx.sync()
+                ctx.timer_start()
+                rf = ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kFd, opts=fd_opts)
+                fms.append(ctx.timer_stop())
+                fscan.append(float(idx.last_timings()[3]))
+            fd_dims = float(rf.dims.astype(np.float64).sum())
+            res["gpu_fd"] = {
+                "value": nq / (float(np.mean(fms)) / 1e3), "unit": "queries/s",
+                "recall_at_k": ads.recall_batch(rf.ids[:ngt], gt[:ngt], K),
+                "scan_ms": float(np.mean(fscan)),
+                "scan_gbs": 4.0 * fd_dims / (float(np.mean(fscan)) / 1e3) / 1e9,
+                "timing": "ivf_query_batch kFd through the host API (H2D queries, D2H results inside), "
+                          "3 runs after one warm-up, L2 flushed"}
+            log(f"GPU FDScanning: {res['gpu_fd']['value']:.0f} q/s, scan {res['gpu_fd']['scan_ms']:.2f} ms "
+                f"({res['gpu_fd']['scan_gbs']:.0f} GB/s), recall {res['gpu_fd']['recall_at_k']:.5f}")
+        except (RuntimeError, ValueError) as e:
+            res["gpu_fd"] = {"unavailable": str(e)[:200]}
     if args.sweep and D.rank == 0:
         sw = []
         for np_ in cfg.sweep:
