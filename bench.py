@@ -297,12 +297,21 @@ def cpu_baseline_reference(cfg, base, t, m, idx, q, gt, nprobe, budget_s=12.0, l
     rec = float(np.mean([len(np.intersect1d(ids[i], gt[i])) for i in range(ns)]) / cfg.K)
     fd_ns = min(ns, max(probe, ns // 3))
     _, _, fd_secs = run("fd", q[:fd_ns], cores)
-    log(f"cpu baseline ({kind}): {ns} queries IVF++ {ns / secs:.0f} QPS, FD {fd_ns / fd_secs:.0f} QPS")
+    # IVF+ (kAd: the contiguous transformed rows) and the reference's own single-thread
+    # run_timed protocol (bench.cpp:125-182), on smaller samples of the same queries
+    _, _, ad_secs = run("ad", q[:fd_ns], cores)
+    st_ns = max(8, min(ns, int(budget_s / 4 / max(per_q * cores, 1e-9))))
+    _, _, st_secs = run("ad-split", q[:st_ns], 1)
+    log(f"cpu baseline ({kind}): {ns} queries IVF++ {ns / secs:.0f} QPS, FD {fd_ns / fd_secs:.0f} QPS, "
+        f"IVF+ {fd_ns / ad_secs:.0f} QPS ({cores} threads); IVF++ single thread {st_ns / st_secs:.0f} QPS")
     return {"value": ns / secs, "unit": "queries/s", "cores": cores, "kind": kind,
             "sample": f"first {ns} of {len(q)} queries, ivf_query kAdSplit, rotation inside the loop "
                       f"(run_timed protocol), {cores} host threads over queries, same index",
             "recall_at_k": rec, "fd_value": fd_ns / fd_secs,
-            "fd_sample": f"first {fd_ns} queries, ivf_query kFd"}, ids, ns
+            "fd_sample": f"first {fd_ns} queries, ivf_query kFd",
+            "ivf_plus_value": fd_ns / ad_secs, "ivf_plus_sample": f"first {fd_ns} queries, ivf_query kAd",
+            "single_thread_value": st_ns / st_secs,
+            "single_thread_sample": f"first {st_ns} queries, ivf_query kAdSplit, 1 thread"}, ids, ns
 
 
 # ---------------------------------------------------------------- search bench
@@ -486,6 +495,20 @@ def run_search(args, D: Dist):
                 f"({res['gpu_fd']['scan_gbs']:.0f} GB/s), recall {res['gpu_fd']['recall_at_k']:.5f}")
         except (RuntimeError, ValueError) as e:
             res["gpu_fd"] = {"unavailable": str(e)[:200]}
+        try:  # IVF+ (kAd) on the GPU, same index
+            ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kAd, opts=fd_opts)
+            ams = []
+            for _ in range(3):
+                ctx.flush_l2()
+                ctx.sync()
+                ctx.timer_start()
+                ra = ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kAd, opts=fd_opts)
+                ams.append(ctx.timer_stop())
+            res["gpu_ivf_plus"] = {"value": nq / (float(np.mean(ams)) / 1e3), "unit": "queries/s",
+                                   "recall_at_k": ads.recall_batch(ra.ids[:ngt], gt[:ngt], K),
+                                   "timing": "ivf_query_batch kAd, as gpu_fd"}
+        except (RuntimeError, ValueError) as e:
+            res["gpu_ivf_plus"] = {"unavailable": str(e)[:200]}
     if args.sweep and D.rank == 0:
         sw = []
         for np_ in cfg.sweep:
