@@ -393,11 +393,7 @@ static void apply_tc(ads_transform* t, const float* dX, int64_t n, float* dY) {
         ADS_CUDA(cudaStreamSynchronize(st));
         t->split_ready = true;
     }
-    const size_t cnt = static_cast<size_t>(n) * t->dim;
-    float* xh = t->xh.get<float>(cnt);
-    float* xl = t->xl.get<float>(cnt);
-    launch_split_tf32(dX, static_cast<int64_t>(cnt), xh, xl, st);
-    launch_tc_transform(xh, xl, n, t->ph.get<float>(dd), t->pl.get<float>(dd), t->dim, dY, st);
+    launch_tc_transform(dX, n, t->ph.get<float>(dd), t->pl.get<float>(dd), t->dim, dY, t->xh, t->xl, st);
 }
 
 int ads_apply_dataset_tc(ads_transform* t, const float* X, int64_t n, float* Y) {
@@ -1154,11 +1150,7 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
                 ADS_CUDA(cudaStreamSynchronize(st));
                 x->p_split = true;
             }
-            const size_t cnt = static_cast<size_t>(nq) * D;
-            float* qh = x->qh.get<float>(cnt);
-            float* ql = x->ql.get<float>(cnt);
-            launch_split_tf32(dQraw, static_cast<int64_t>(cnt), qh, ql, st);
-            launch_tc_transform(qh, ql, nq, x->ph.get<float>(dd), x->pl.get<float>(dd), D, qr, st);
+            launch_tc_transform(dQraw, nq, x->ph.get<float>(dd), x->pl.get<float>(dd), D, qr, x->qh, x->ql, st);
         } else {
             launch_apply(x->P, D, dQraw, nq, qr, st);
         }

@@ -196,8 +196,10 @@ void launch_tc_coarse_gemm(const float* Qc, int nq, const float* Cc, int L, int 
                            const float* cn2, float* out, cudaStream_t st);
 // 3xTF32 transform on the tensor cores (tc_gemm.cu): hi/lo split, then Y = X P^T.
 void launch_split_tf32(const float* x, int64_t n, float* hi, float* lo, cudaStream_t st);
-void launch_tc_transform(const float* Xh, const float* Xl, int64_t n, const float* Ph, const float* Pl, int D,
-                         float* Y, cudaStream_t st);
+// Y = X P^T on the tensor cores (3xTF32; Ph/Pl = P split into TF32 pairs).
+// xh/xl: scratch for the experiment variants that pre-split X (unused by default).
+void launch_tc_transform(const float* X, int64_t n, const float* Ph, const float* Pl, int D, float* Y, DevBuf& xh,
+                         DevBuf& xl, cudaStream_t st);
 // gemm: 0 = tensor cores when supported (D % 4 == 0), 1 = fp32 FMA on the CUDA cores.
 void launch_coarse_probes_fast(const float* Q, int nq, const float* C, int L, int D, int nprobe,
                                const CoarseCentroids& cc, CoarseScratch& s, int32_t* probes, int gemm,

@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "engine.hpp"
@@ -49,6 +50,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100): start >> 4
 // [0,14), LBO >> 4 [16,30) (unused by swizzled K-major: 1), SBO >> 4 [32,46)
 // = 1024 B between 8-row atoms, version 1 [46,48), SWIZZLE_128B = 2 [61,64).
+// K-major swizzled descriptor for a KB-fp32-wide row: 128 B (type 2), 64 B (4), 32 B (6);
+// SBO = 8 rows.
+template <int KB>
+__device__ __forceinline__ uint64_t swz_desc(uint32_t saddr) {
+    uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(KB * 4 * 8 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(KB == 32 ? 2 : KB == 16 ? 4 : 6) << 61;
+    return d;
+}
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
     d |= static_cast<uint64_t>(1) << 16;
@@ -231,6 +243,224 @@ __global__ void __launch_bounds__(kThreads) tc_gemm_kernel(const __grid_constant
                      : "memory");
 }
 
+__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(smem_u32(src))
+                 : "memory");
+}
+
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+    uint32_t h, l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - __uint_as_float(h)));
+    hi = __uint_as_float(h);
+    lo = __uint_as_float(l);
+}
+
+// Persistent 3xTF32 rotation Y = Xh Ph^T + Xh Pl^T + Xl Ph^T, one CTA per SM
+// walking 128 x BN output tiles (tile t -> rows (t / nN) * 128, columns
+// (t % nN) * BN, so the CTAs in flight share X row blocks through L2).
+// Warp 0 lane 0: TMA producer over a STAGES-deep ring of K blocks (KB fp32
+// wide: 32 with SWIZZLE_128B, 16 with SWIZZLE_64B).  Warp 1 lane 0: the MMA
+// issuer, alternating two TMEM accumulators of BN columns so a tile's
+// epilogue overlaps the next tile's MMAs.  Warps 2-5: the epilogue, warp w
+// reading TMEM lanes 32 (w % 4) .. + 31 (its row quadrant) 32 columns at a
+// time into a 128-byte-swizzled 32 x 32 staging box that one TMA store
+// writes out (double-buffered per warp; rows/columns past the matrix are
+// clipped by the tensor map).
+// FUSED: X arrives unsplit (tXl unused) and warps 6-9 split each staged X
+// block in place into its TF32 pair (hi over x, lo beside it; the same
+// cvt.rna arithmetic as split_tf32_kernel, so the result is bit-identical),
+// then release the stage to the MMA issuer through `conv`.
+template <int BN, int STAGES, int KB, bool FUSED, int CW = 4, int EPIB = 2>
+__global__ void __launch_bounds__(192 + (FUSED ? 32 * CW : 0), 1) tc_rotate_kernel(const __grid_constant__ CUtensorMap tXh,
+                                                           const __grid_constant__ CUtensorMap tXl,
+                                                           const __grid_constant__ CUtensorMap tPh,
+                                                           const __grid_constant__ CUtensorMap tPl,
+                                                           const __grid_constant__ CUtensorMap tY, int M, int N,
+                                                           int K) {
+    static_assert(KB == 32 || KB == 16 || KB == 8, "K block: one 128-, 64- or 32-byte swizzle row");
+    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: 32-column epilogue chunks, MMA N <= 256");
+    constexpr int ATILE = kTM * KB * 4, BTILE = BN * KB * 4;
+    constexpr int STAGE = 2 * ATILE + 2 * BTILE;
+    constexpr uint32_t IDESC = idesc_tf32<BN>();
+    constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE);  // 4 warps x 2 x (32 x 32)
+    __shared__ uint64_t full[STAGES], empty[STAGES], conv[STAGES], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_holder;
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = threadIdx.x & 31u;
+    const int nkb = (K + KB - 1) / KB;
+    const int nN = (N + BN - 1) / BN;
+    const int64_t ntiles = static_cast<int64_t>((M + kTM - 1) / kTM) * nN;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s]);
+            mbar_init(&empty[s]);
+            mbar_init_n(&conv[s], CW);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a]);
+            mbar_init_n(&tempty[a], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tXh)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tPh)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
+                     "r"(TCOLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            int g = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int m0 = static_cast<int>(t / nN) * kTM, n0 = static_cast<int>(t % nN) * BN;
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = static_cast<uint32_t>(g / STAGES) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char* st = smem + s * STAGE;
+                    mbar_expect(&full[s], FUSED ? STAGE - ATILE : STAGE);
+                    tma_load(st, &tXh, &full[s], kb * KB, m0);
+                    if constexpr (!FUSED) tma_load(st + ATILE, &tXl, &full[s], kb * KB, m0);
+                    tma_load(st + 2 * ATILE, &tPh, &full[s], kb * KB, n0);
+                    tma_load(st + 2 * ATILE + BTILE, &tPl, &full[s], kb * KB, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            int g = 0, it = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int acc = it & 1;
+                mbar_wait(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = static_cast<uint32_t>(g / STAGES) & 1u;
+                    mbar_wait(FUSED ? &conv[s] : &full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    unsigned char* st = smem + s * STAGE;
+                    const uint32_t sa = smem_u32(st);
+                    const uint64_t xh = swz_desc<KB>(sa);
+                    const uint64_t xl = swz_desc<KB>(sa + ATILE);
+                    const uint64_t ph_ = swz_desc<KB>(sa + 2 * ATILE);
+                    const uint64_t pl = swz_desc<KB>(sa + 2 * ATILE + BTILE);
+#pragma unroll
+                    for (int k = 0; k < KB / 8; ++k) {
+                        const uint64_t dk = static_cast<uint64_t>(k * 2);
+                        umma_tf32(d, xh + dk, ph_ + dk, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+                        umma_tf32(d, xh + dk, pl + dk, IDESC, 1u);
+                        umma_tf32(d, xl + dk, ph_ + dk, IDESC, 1u);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+    } else if (FUSED && warp >= 6) {  // split warps
+        const int ct = threadIdx.x - 192;
+        int g = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int kb = 0; kb < nkb; ++kb, ++g) {
+                const int s = g % STAGES;
+                mbar_wait(&full[s], static_cast<uint32_t>(g / STAGES) & 1u);
+                float4* xa = reinterpret_cast<float4*>(smem + s * STAGE);
+                float4* la = reinterpret_cast<float4*>(smem + s * STAGE + ATILE);
+#pragma unroll
+                for (int i = ct; i < ATILE / 16; i += 32 * CW) {
+                    const float4 v = xa[i];
+                    float4 h, l;
+                    split_tf32(v.x, h.x, l.x);
+                    split_tf32(v.y, h.y, l.y);
+                    split_tf32(v.z, h.z, l.z);
+                    split_tf32(v.w, h.w, l.w);
+                    xa[i] = h;
+                    la[i] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv[s]);
+            }
+        }
+    } else {  // epilogue warps 2..5
+        const int q = warp & 3;
+        float* mine = epi + (warp - 2) * EPIB * 1024;
+        int it = 0, sb = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int m0 = static_cast<int>(t / nN) * kTM, n0 = static_cast<int>(t % nN) * BN;
+            const int acc = it & 1;
+            mbar_wait(&tfull[acc], static_cast<uint32_t>(it >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int cb = 0; cb < BN; cb += 32) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cb);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float* box = mine + sb * 1024;
+                if (lane == 0) {
+                    if constexpr (EPIB == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+                __syncwarp();
+                // row = lane; 16-byte chunk c of the row lands at c ^ (row & 7) (SWIZZLE_128B)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int pc = c ^ static_cast<int>(lane & 7u);
+                    *reinterpret_cast<uint4*>(box + lane * 32 + pc * 4) =
+                        make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store(&tY, box, n0 + cb, m0 + q * 32);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                if constexpr (EPIB == 2) sb ^= 1;
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
+}
+
 __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ hi,
                                   float* __restrict__ lo) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -260,14 +490,17 @@ EncodeTiledFn encode_tiled() {
 }
 
 // rows x width row-major fp32 (width % 4 == 0); box = 32 columns x box_rows rows, SWIZZLE_128B.
-CUtensorMap tile_map(const float* base, int width, int64_t rows, int box_rows) {
+CUtensorMap tile_map(const float* base, int width, int64_t rows, int box_rows, int box_cols = kTK) {
     CUtensorMap m{};
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * sizeof(float)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      box_cols == 32   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                      : box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                       : CU_TENSOR_MAP_SWIZZLE_32B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
     return m;
@@ -313,11 +546,54 @@ void launch_split_tf32(const float* x, int64_t n, float* hi, float* lo, cudaStre
     ADS_LAUNCH_CHECK();
 }
 
-void launch_tc_transform(const float* Xh, const float* Xl, int64_t n, const float* Ph, const float* Pl, int D,
-                         float* Y, cudaStream_t st) {
+namespace {
+template <int BN, int STAGES, int KB, bool FUSED, int CW = 4, int EPIB = 2>
+void launch_rotate(const float* Xh, const float* Xl, int64_t n, const float* Ph, const float* Pl, int D, float* Y,
+                   cudaStream_t st) {
+    constexpr int smem = STAGES * (2 * kTM * KB * 4 + 2 * BN * KB * 4) + 4 * EPIB * 4096 + 1024;
+    static_assert(smem <= 227 * 1024, "rotation kernel shared memory");
+    const CUtensorMap xh = tile_map(Xh, D, n, kTM, KB), xl = tile_map(Xl, D, n, kTM, KB);
+    const CUtensorMap ph = tile_map(Ph, D, D, BN, KB), pl = tile_map(Pl, D, D, BN, KB);
+    const CUtensorMap y = tile_map(Y, D, n, 32, 32);
+    auto kern = tc_rotate_kernel<BN, STAGES, KB, FUSED, CW, EPIB>;
+    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t tiles = ((n + kTM - 1) / kTM) * ((D + BN - 1) / BN);
+    const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+    kern<<<grid, 192 + (FUSED ? 32 * CW : 0), smem, st>>>(xh, xl, ph, pl, y, static_cast<int>(n), D, D);
+    ADS_LAUNCH_CHECK();
+}
+}  // namespace
+
+
+void launch_tc_transform(const float* X, int64_t n, const float* Ph, const float* Pl, int D, float* Y, DevBuf& xh_buf,
+                         DevBuf& xl_buf, cudaStream_t st) {
     if (n <= 0) return;
     if (D % 4 != 0 || D < kTK)
         throw std::invalid_argument("apply (tensor cores): dimension must be a multiple of 4 and >= 32");
+    // ADS_TC_ROTATE (A/B experiments): 0 the tiled kernel on a pre-split X, 1 the
+    // persistent kernel on a pre-split X, 2 (default) persistent with the split fused
+    static const int variant = [] {
+        const char* e = std::getenv("ADS_TC_ROTATE");
+        return e ? std::atoi(e) : 2;
+    }();
+    if (variant == 2 && n < (int64_t(1) << 31)) {
+        // widest N tile that divides D (fewer X re-reads, better MMA shape); the split
+        // fused (8 split warps); the deepest ring that fits beside a single-buffered
+        // epilogue (profiles/r01_ncu_tensorcore.md)
+        if (D % 256 == 0) return launch_rotate<256, 4, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
+        if (D % 192 == 0) return launch_rotate<192, 5, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
+        if (D % 128 == 0) return launch_rotate<128, 6, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
+        if (D % 96 == 0) return launch_rotate<96, 7, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
+        return launch_rotate<128, 6, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
+    }
+    const size_t cnt = static_cast<size_t>(n) * D;
+    float* Xh = xh_buf.get<float>(cnt);
+    float* Xl = xl_buf.get<float>(cnt);
+    launch_split_tf32(X, static_cast<int64_t>(cnt), Xh, Xl, st);
+    if (variant == 1 && n < (int64_t(1) << 31)) {
+        if (D % 192 == 0) return launch_rotate<192, 4, 16, false>(Xh, Xl, n, Ph, Pl, D, Y, st);
+        return launch_rotate<128, 6, 16, false>(Xh, Xl, n, Ph, Pl, D, Y, st);
+    }
     const CUtensorMap ph = tile_map(Ph, D, D, 128), pl = tile_map(Pl, D, D, 128);
     const int64_t chunk = static_cast<int64_t>(65535) * kTM;
     for (int64_t r = 0; r < n; r += chunk) {
