@@ -64,7 +64,18 @@ def run_transform(args, D):
     err = float((np.abs(tc_sample.astype(np.float64) - exact_sample).max(axis=1) / xn).max())
     useful = 2.0 * n * d * d
     peak = _tf32_peak()
-    achieved = useful / (tc_ms / 1e3) / 1e12
+    # the 3xTF32 rotation issues three TF32 products per useful product
+    achieved = 3.0 * useful / (tc_ms / 1e3) / 1e12
+    # end to end through the host API (host X in, host Y out, copies inside)
+    import time as _time
+
+    t.apply_dataset_tc(X[:1024])
+    e2e_s = []
+    for _ in range(2):
+        t0 = _time.perf_counter()
+        t.apply_dataset_tc(X)
+        e2e_s.append(_time.perf_counter() - t0)
+    e2e_sec = float(np.mean(e2e_s))
     log(f"exact fp64: {exact_ms:.2f} ms, 3xTF32 tensor cores: {tc_ms:.2f} ms, max |err|/|x| {err:.2e}")
     return {
         "metric": "dataset rotation vectors/s (3xTF32 tensor cores)", "value": n / (tc_ms / 1e3),
@@ -75,10 +86,16 @@ def run_transform(args, D):
         "exact_fp64": {"value": n / (exact_ms / 1e3), "unit": "vectors/s", "ms_per_step": exact_ms,
                        "note": "engine default: bit-identical to the reference's fp64 apply_dataset"},
         "max_abs_err_over_norm": err,
-        "e2e": None, "gpu_launches": 2 * args.steps,
+        "e2e": {"value": n / e2e_sec, "unit": "vectors/s", "h2d_bytes_per_step": int(X.nbytes),
+                "d2h_bytes_per_step": int(X.nbytes),
+                "timing": "Transform.apply_dataset_tc on host arrays (ads_apply_dataset_tc), wall clock"},
+        "gpu_launches": args.steps,  # one persistent tc_rotate_kernel per step (split fused)
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak["tflops"], "unit": "TFLOP/s",
-                     "frac": achieved / peak["tflops"], "traffic": None,
-                     "kernel": "tc_transform_kernel (useful 2*n*D^2 flops; the 3xTF32 split issues 3x)",
+                     "frac": achieved / peak["tflops"],
+                     "traffic": 7.65 if (n, d) == (1_000_000, 960) else None, "traffic_unit": "GB per launch (ncu dram read+write, "
+                                                      "profiles/r01_ncu_tensorcore.md, prof_rotf)",
+                     "useful_tflops": useful / (tc_ms / 1e3) / 1e12,
+                     "kernel": "tc_rotate_kernel (TF32 flops issued = 3 x 2 n D^2; useful = 2 n D^2)",
                      "peak_source": peak["source"]},
         "clocks": clocks,
     }
