@@ -1,6 +1,7 @@
-"""Parity at BASELINE.json's full config-2 size: the 1 M x 128 index (4096 lists,
-k-means++ + 25 Lloyd iterations, built on the GPU) exported and searched by the
-C oracle for a subset of queries, bit for bit: ids, distances and dims under the
+"""Parity at BASELINE.json's full sizes: config 2's 1 M x 128 index (4096 lists,
+k-means++ + 25 Lloyd iterations) and config 3's 1 M x 960 index (10-warp CTAs,
+30 segments per walk), built on the GPU, exported and searched by the C oracle
+for a subset of queries, bit for bit: ids, distances and dims under the
 engine's default batched refresh schedule, and under the reference's
 per-candidate schedule (first = step = 1)."""
 import numpy as np
@@ -11,11 +12,12 @@ from helpers import MODE_ID
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def test_config2_full_size_vs_oracle(eng, orc):
+@pytest.mark.parametrize("cfgid,nq", [(2, 64), (3, 24)])
+def test_full_size_vs_oracle(eng, orc, cfgid, nq):
     from paper_2303_09855_b200 import configs
 
-    cfg = configs.CONFIGS[2]
-    base, q = configs.generate(cfg, nq=64)
+    cfg = configs.CONFIGS[cfgid]
+    base, q = configs.generate(cfg, nq=nq)
     m = eng.generate_orthogonal(cfg.d, cfg.seed)
     t = eng.apply_dataset(m, base)
     idx = eng.build_ivf(base, t, m, cfg.nlist, cfg.seed, eng.IvfLayout.kSplit, 32,
