@@ -398,6 +398,34 @@ def test_transform_tensor_cores(eng, orc, n, d):
         eng.apply_dataset_tc(eng.generate_orthogonal(6, 1), rng.normal(size=(3, 6)).astype(np.float32))
 
 
+def test_tc_rotation_kernels_agree(eng, tmp_path):
+    """The persistent tcgen05 rotation with the TF32 split fused (default) is bit-identical
+    to the first tiled kernel on a pre-split X (ADS_TC_ROTATE=0, run in a subprocess):
+    same products, same K order, same cvt.rna split; shapes cover every N-tile width
+    (96, 128, 192, 256, and the D = 32 fallback) and row tails."""
+    import os
+    import subprocess
+    import sys
+
+    shapes = [(300, 96), (1000, 128), (129, 32), (777, 960), (5000, 256), (1, 960), (4099, 192)]
+    code = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "import paper_2303_09855_b200 as ads\n"
+        "out = {}\n"
+        f"for n, d in {shapes!r}:\n"
+        "    X = np.random.default_rng(n + d).normal(0, 3, (n, d)).astype(np.float32)\n"
+        "    out[f'{n}x{d}'] = ads.apply_dataset_tc(ads.generate_orthogonal(d, 5), X)\n"
+        f"np.savez({str(tmp_path / 'tiled.npz')!r}, **out)\n")
+    env = dict(os.environ, ADS_TC_ROTATE="0")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+    ref = np.load(tmp_path / "tiled.npz")
+    for n, d in shapes:
+        X = np.random.default_rng(n + d).normal(0, 3, (n, d)).astype(np.float32)
+        got = eng.apply_dataset_tc(eng.generate_orthogonal(d, 5), X)
+        np.testing.assert_array_equal(got, ref[f"{n}x{d}"], err_msg=f"{n}x{d}")
+
+
 def test_ivf_tensor_core_query_rotation(eng, orc):
     """rotate_mode 1 (queries rotated by the 3xTF32 tensor-core transform on the GPU)
     == the oracle run on the same TC-rotated queries, bit for bit."""
