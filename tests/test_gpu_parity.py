@@ -16,8 +16,10 @@ pytestmark = pytest.mark.gpu
 
 
 # ------------------------------------------------------------------ transform
-@pytest.mark.parametrize("d,n", [(1, 5), (7, 33), (64, 1000), (128, 517), (200, 64)])
+@pytest.mark.parametrize("d,n", [(1, 5), (7, 33), (64, 1000), (128, 517), (200, 64), (960, 700), (30, 2049),
+                                 (96, 1300)])
 def test_apply_dataset_bitexact(eng, orc, d, n):
+    """n >= 512 runs the register-blocked tile kernel, smaller n the row kernel."""
     rng = np.random.default_rng(d * 7 + n)
     X = rng.normal(0, 3, (n, d)).astype(np.float32)
     m = eng.generate_orthogonal(d, 11)
@@ -28,6 +30,10 @@ def test_apply_dataset_bitexact(eng, orc, d, n):
     np.testing.assert_array_equal(yt, orc.apply_transpose(m.entries, X[0]))
     np.testing.assert_array_equal(eng.apply_prefix(m, X[1], d // 2),
                                   orc.apply_prefix(m.entries, X[1], d // 2))
+    if n >= 512:  # apply_transpose over a whole dataset (the same kernels on P^T)
+        yT = eng.Transform(m).apply_transpose_dataset(X)
+        for i in range(0, n, max(1, n // 17)):
+            np.testing.assert_array_equal(yT[i], orc.apply_transpose(m.entries, X[i]))
 
 
 # ------------------------------------------------------------------ fixed-threshold DCOs
