@@ -19,7 +19,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("d,n", [(1, 5), (7, 33), (64, 1000), (128, 517), (200, 64), (960, 700), (30, 2049),
                                  (96, 1300)])
 def test_apply_dataset_bitexact(eng, orc, d, n):
-    """n >= 512 runs the register-blocked tile kernel, smaller n the row kernel."""
+    """Tile edges in both dimensions (D not a multiple of the 64-row tile or the
+    32-column stage, ragged vector counts) and apply_transpose over a dataset."""
     rng = np.random.default_rng(d * 7 + n)
     X = rng.normal(0, 3, (n, d)).astype(np.float32)
     m = eng.generate_orthogonal(d, 11)
