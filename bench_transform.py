@@ -92,10 +92,10 @@ def run_transform(args, D):
         "gpu_launches": args.steps,  # one persistent tc_rotate_kernel per step (split fused)
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak["tflops"], "unit": "TFLOP/s",
                      "frac": achieved / peak["tflops"],
-                     "traffic": 7.65 if (n, d) == (1_000_000, 960) else None, "traffic_unit": "GB per launch (ncu dram read+write, "
-                                                      "profiles/r01_ncu_tensorcore.md, prof_rotf)",
+                     "traffic": 7.66 if (n, d) == (1_000_000, 960) else None, "traffic_unit": "GB per launch (ncu dram read+write, "
+                                                      "profiles/r01_ncu_tensorcore.md, prof_pair2)",
                      "useful_tflops": useful / (tc_ms / 1e3) / 1e12,
-                     "kernel": "tc_rotate_kernel (TF32 flops issued = 3 x 2 n D^2; useful = 2 n D^2)",
+                     "kernel": "tc_rotate_pair_kernel (TF32 flops issued = 3 x 2 n D^2; useful = 2 n D^2)",
                      "peak_source": peak["source"]},
         "clocks": clocks,
     }

@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -461,6 +462,232 @@ __global__ void __launch_bounds__(192 + (FUSED ? 32 * CW : 0), 1) tc_rotate_kern
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
 }
 
+// CTA-pair (cta_group::2) variant of the fused rotation, M = 256 per MMA: CTA
+// rank r of a cluster of two loads X rows m0 + 128 r and P rows n0 + (BN/2) r
+// into its own ring (its own `full` barrier), splits its X block in place and
+// arrives on the LEADER's `conv` barrier (count 2 CW); the leader's lane issues
+// tcgen05.mma.cta_group::2 on its own descriptors (the pair's tensor cores take
+// the same offsets in the peer) and commits `empty` / `tfull` to both CTAs;
+// each CTA drains its own 128 TMEM lanes and arrives on the leader's `tempty`
+// (count 8).  Each SM thus reads its 128 X rows and only half of P per K step.
+// the cluster-window address of the leader's (rank 0) copy of a shared variable
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+template <int BN, int STAGES, int KB, int CW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192 + 32 * CW, 1)
+    tc_rotate_pair_kernel(const __grid_constant__ CUtensorMap tX, const __grid_constant__ CUtensorMap tPh,
+                          const __grid_constant__ CUtensorMap tPl, const __grid_constant__ CUtensorMap tY, int M,
+                          int N, int K) {
+    static_assert(KB == 16, "K block: one 64-byte swizzle row");
+    static_assert(BN % 32 == 0 && BN <= 256 && (BN / 2) % 16 == 0, "BN: 32-column epilogue chunks, N/2 per CTA");
+    constexpr int HB = BN / 2;
+    constexpr int ATILE = kTM * KB * 4, BTILE = HB * KB * 4;
+    constexpr int STAGE = 2 * ATILE + 2 * BTILE;
+    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                               (static_cast<uint32_t>(256 >> 4) << 24);
+    constexpr uint32_t TCOLS = 2 * BN <= 256 ? 256 : 512;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE);  // 4 warps x (32 x 32)
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], conv[STAGES], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_holder;
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = threadIdx.x & 31u;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int nkb = (K + KB - 1) / KB;
+    const int nN = (N + BN - 1) / BN;
+    const int64_t ntiles = static_cast<int64_t>((M + 2 * kTM - 1) / (2 * kTM)) * nN;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s]);
+            mbar_init(&empty[s]);
+            mbar_init_n(&conv[s], 2 * CW);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a]);
+            mbar_init_n(&tempty[a], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tX)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tPh)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
+                     "r"(TCOLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {  // producer (both CTAs: own X rows, own half of P)
+            int g = 0;
+            for (int64_t t = cid; t < ntiles; t += ncl) {
+                const int m0 = static_cast<int>(t / nN) * 2 * kTM + static_cast<int>(rank) * kTM;
+                const int n0 = static_cast<int>(t % nN) * BN + static_cast<int>(rank) * HB;
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = static_cast<uint32_t>(g / STAGES) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char* st = smem + s * STAGE;
+                    mbar_expect(&full[s], ATILE + 2 * BTILE);
+                    tma_load(st, &tX, &full[s], kb * KB, m0);
+                    tma_load(st + 2 * ATILE, &tPh, &full[s], kb * KB, n0);
+                    tma_load(st + 2 * ATILE + BTILE, &tPl, &full[s], kb * KB, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {  // MMA issuer for the pair
+            int g = 0, it = 0;
+            for (int64_t t = cid; t < ntiles; t += ncl, ++it) {
+                const int acc = it & 1;
+                mbar_wait_cluster(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    mbar_wait_cluster(&conv[s], static_cast<uint32_t>(g / STAGES) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = smem_u32(smem + s * STAGE);
+                    const uint64_t xh = swz_desc<KB>(sa), xl = swz_desc<KB>(sa + ATILE);
+                    const uint64_t ph_ = swz_desc<KB>(sa + 2 * ATILE), pl = swz_desc<KB>(sa + 2 * ATILE + BTILE);
+#pragma unroll
+                    for (int k = 0; k < KB / 8; ++k) {
+                        const uint64_t dk = static_cast<uint64_t>(k * 2);
+                        umma_tf32_pair(d, xh + dk, ph_ + dk, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+                        umma_tf32_pair(d, xh + dk, pl + dk, IDESC, 1u);
+                        umma_tf32_pair(d, xl + dk, ph_ + dk, IDESC, 1u);
+                    }
+                    umma_commit_pair(&empty[s]);
+                }
+                umma_commit_pair(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 6) {  // split warps: own X block, then the leader's conv barrier
+        const int ct = threadIdx.x - 192;
+        const uint32_t conv_leader = leader_addr(&conv[0]);
+        int g = 0;
+        for (int64_t t = cid; t < ntiles; t += ncl) {
+            for (int kb = 0; kb < nkb; ++kb, ++g) {
+                const int s = g % STAGES;
+                mbar_wait(&full[s], static_cast<uint32_t>(g / STAGES) & 1u);
+                float4* xa = reinterpret_cast<float4*>(smem + s * STAGE);
+                float4* la = reinterpret_cast<float4*>(smem + s * STAGE + ATILE);
+#pragma unroll
+                for (int i = ct; i < ATILE / 16; i += 32 * CW) {
+                    const float4 v = xa[i];
+                    float4 h, l;
+                    split_tf32(v.x, h.x, l.x);
+                    split_tf32(v.y, h.y, l.y);
+                    split_tf32(v.z, h.z, l.z);
+                    split_tf32(v.w, h.w, l.w);
+                    xa[i] = h;
+                    la[i] = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(conv_leader + static_cast<uint32_t>(s) * 8u);
+            }
+        }
+    } else {  // epilogue warps 2..5: own 128 rows
+        const int q = warp & 3;
+        float* box = epi + (warp - 2) * 1024;
+        const uint32_t tempty_leader = leader_addr(&tempty[0]);
+        int it = 0;
+        for (int64_t t = cid; t < ntiles; t += ncl, ++it) {
+            const int m0 = static_cast<int>(t / nN) * 2 * kTM + static_cast<int>(rank) * kTM;
+            const int n0 = static_cast<int>(t % nN) * BN;
+            const int acc = it & 1;
+            mbar_wait(&tfull[acc], static_cast<uint32_t>(it >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int cb = 0; cb < BN; cb += 32) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cb);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                    "[%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int pc = c ^ static_cast<int>(lane & 7u);
+                    *reinterpret_cast<uint4*>(box + lane * 32 + pc * 4) =
+                        make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store(&tY, box, n0 + cb, m0 + q * 32);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(acc) * 8u);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
+}
+
 __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ hi,
                                   float* __restrict__ lo) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -547,6 +774,37 @@ void launch_split_tf32(const float* x, int64_t n, float* hi, float* lo, cudaStre
 }
 
 namespace {
+template <int BN, int STAGES, int CW>
+void launch_rotate_pair(const float* X, int64_t n, const float* Ph, const float* Pl, int D, float* Y, cudaStream_t st) {
+    constexpr int smem = STAGES * (2 * kTM * 16 * 4 + 2 * (BN / 2) * 16 * 4) + 4 * 4096 + 1024;
+    static_assert(smem <= 227 * 1024, "pair rotation kernel shared memory");
+    const CUtensorMap x = tile_map(X, D, n, kTM, 16);
+    const CUtensorMap ph = tile_map(Ph, D, D, BN / 2, 16), pl = tile_map(Pl, D, D, BN / 2, 16);
+    const CUtensorMap y = tile_map(Y, D, n, 32, 32);
+    auto kern = tc_rotate_pair_kernel<BN, STAGES, 16, CW>;
+    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * num_sms());
+        cfg.blockDim = dim3(192 + 32 * CW);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = 2;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        ADS_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+        if (max_clusters < 1) throw CudaError("pair rotation: no co-resident CTA pair");
+    }
+    const int64_t tiles = ((n + 2 * kTM - 1) / (2 * kTM)) * ((D + BN - 1) / BN);
+    const int clusters = static_cast<int>(tiles < max_clusters ? tiles : max_clusters);
+    kern<<<2 * clusters, 192 + 32 * CW, smem, st>>>(x, ph, pl, y, static_cast<int>(n), D, D);
+    ADS_LAUNCH_CHECK();
+}
+
 template <int BN, int STAGES, int KB, bool FUSED, int CW = 4, int EPIB = 2>
 void launch_rotate(const float* Xh, const float* Xl, int64_t n, const float* Ph, const float* Pl, int D, float* Y,
                    cudaStream_t st) {
@@ -571,15 +829,22 @@ void launch_tc_transform(const float* X, int64_t n, const float* Ph, const float
     if (D % 4 != 0 || D < kTK)
         throw std::invalid_argument("apply (tensor cores): dimension must be a multiple of 4 and >= 32");
     // ADS_TC_ROTATE (A/B experiments): 0 the tiled kernel on a pre-split X, 1 the
-    // persistent kernel on a pre-split X, 2 (default) persistent with the split fused
+    // persistent kernel on a pre-split X, 2 persistent with the split fused,
+    // 3 (default) the fused CTA-pair kernel (profiles/r01_ncu_tensorcore.md)
     static const int variant = [] {
         const char* e = std::getenv("ADS_TC_ROTATE");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 3;
     }();
+    if (variant == 3 && n < (int64_t(1) << 31)) {
+        // widest N tile that divides D; each CTA of the pair stages BN/2 rows of P;
+        // the deepest K-16 ring that fits beside the epilogue box
+        if (D % 256 == 0) return launch_rotate_pair<256, 6, 8>(X, n, Ph, Pl, D, Y, st);
+        if (D % 192 == 0) return launch_rotate_pair<192, 7, 8>(X, n, Ph, Pl, D, Y, st);
+        if (D % 128 == 0) return launch_rotate_pair<128, 8, 8>(X, n, Ph, Pl, D, Y, st);
+        if (D % 96 == 0) return launch_rotate_pair<96, 9, 8>(X, n, Ph, Pl, D, Y, st);
+        return launch_rotate_pair<128, 8, 8>(X, n, Ph, Pl, D, Y, st);
+    }
     if (variant == 2 && n < (int64_t(1) << 31)) {
-        // widest N tile that divides D (fewer X re-reads, better MMA shape); the split
-        // fused (8 split warps); the deepest ring that fits beside a single-buffered
-        // epilogue (profiles/r01_ncu_tensorcore.md)
         if (D % 256 == 0) return launch_rotate<256, 4, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
         if (D % 192 == 0) return launch_rotate<192, 5, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
         if (D % 128 == 0) return launch_rotate<128, 6, 16, true, 8, 1>(X, X, n, Ph, Pl, D, Y, st);
