@@ -783,8 +783,8 @@ void launch_rotate_pair(const float* X, int64_t n, const float* Ph, const float*
     const CUtensorMap y = tile_map(Y, D, n, 32, 32);
     auto kern = tc_rotate_pair_kernel<BN, STAGES, 16, CW>;
     ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    static int max_clusters = -1;
-    if (max_clusters < 0) {
+    // co-resident CTA pairs for this instantiation (thread-safe one-time init)
+    static const int max_clusters = [&] {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * num_sms());
         cfg.blockDim = dim3(192 + 32 * CW);
@@ -796,9 +796,11 @@ void launch_rotate_pair(const float* X, int64_t n, const float* Ph, const float*
         attr.val.clusterDim.z = 1;
         cfg.attrs = &attr;
         cfg.numAttrs = 1;
-        ADS_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
-        if (max_clusters < 1) throw CudaError("pair rotation: no co-resident CTA pair");
-    }
+        int c = 0;
+        ADS_CUDA(cudaOccupancyMaxActiveClusters(&c, kern, &cfg));
+        if (c < 1) throw CudaError("pair rotation: no co-resident CTA pair");
+        return c;
+    }();
     const int64_t tiles = ((n + 2 * kTM - 1) / (2 * kTM)) * ((D + BN - 1) / BN);
     const int clusters = static_cast<int>(tiles < max_clusters ? tiles : max_clusters);
     kern<<<2 * clusters, 192 + 32 * CW, smem, st>>>(x, ph, pl, y, static_cast<int>(n), D, D);
