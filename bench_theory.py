@@ -31,11 +31,16 @@ def run_theory(args, D):
     K = cfg.K
     for _ in range(args.warmup):
         ads.verify_theory(t, qt, K, GRID)
+    from bench import ClockSampler
+
+    clocks = ClockSampler(D.local)
+    clocks.start()
     secs = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
         rows = ads.verify_theory(t, qt, K, GRID)
         secs.append(time.perf_counter() - t0)
+    clk = clocks.stop()
     sec = float(np.mean(secs))
     pairs = float(cfg.n) * qt.shape[0]
     res = {
@@ -46,6 +51,7 @@ def run_theory(args, D):
         "config": {"workload": "theory-cfg1-100k-d128", "n": cfg.n, "d": cfg.d, "nq": int(qt.shape[0]), "K": K,
                    "grid": GRID, "timing": "host API call (H2D of the dataset and queries inside)"},
         "rows": [r._asdict() for r in rows],
+        "clocks": clk,
         "e2e": {"value": pairs / sec, "unit": "pairs/s", "h2d_bytes_per_step": int(t.nbytes + qt.nbytes),
                 "d2h_bytes_per_step": 0},
         # per call: brute-force distances + select (one batch), kth distance, theory kernel

@@ -48,6 +48,7 @@ def run_transform(args, D):
             fn()
         ctx.sync()
         clocks = ClockSampler(D.local)
+        clocks.start()
         ms = []
         for _ in range(args.steps):
             ctx.flush_l2()

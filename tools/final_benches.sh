@@ -1,0 +1,14 @@
+#!/bin/bash
+# Every bench line of the round on one box, outputs under gpurun_out/final/.
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out/final
+cd "${GRAFT_REPO_ROOT:-.}"
+run() { local tag=$1; shift; timeout 1500 python bench.py "$@" > gpurun_out/final/$tag.json 2> gpurun_out/final/$tag.log; echo "$tag rc=$?" >> gpurun_out/final/rc.txt; }
+run default
+run reference --impl reference --steps 3 --warmup 3
+run cfg1 --config 1
+run cfg3 --config 3
+run transform --mode transform --steps 5 --warmup 3
+run dco --mode dco --steps 3 --warmup 3
+run theory --mode theory --steps 3 --warmup 3
+run cfg5 --config 5 --steps 3 --warmup 3
