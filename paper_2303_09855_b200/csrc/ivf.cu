@@ -234,7 +234,6 @@ __device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double 
 struct SearchShared {
     double r, r_sq;
     int q, stop, total, next, cnt, pnext;
-    int wc[64];  // per-(round, warp) counts of the CTA-wide merge compaction
     int pcount[2];
     unsigned long long dims;
 };
@@ -245,7 +244,7 @@ struct SearchShared {
 // -(m + 1) on a tie (the compacted batch is then offered sequentially).
 // Needs n <= 2 * blockDim.x and sh.cnt <= 2 * blockDim.x; call with all threads.
 __device__ __noinline__ int cta_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, int K, double* pend_d,
-                               int32_t* pend_i, const unsigned* pflag, int n) {
+                               int32_t* pend_i, const unsigned* pflag, int n, int* wc) {
     const int tid = threadIdx.x, nthr = blockDim.x, nwarps = nthr >> 5, warp = tid >> 5;
     const unsigned lane = lane_id();
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -268,12 +267,12 @@ __device__ __noinline__ int cta_merge_chunk(double* topd, int32_t* topi, SearchS
             keep[r] = !full || d[r] < maxd;  // the max only decreases
         }
         kb[r] = __ballot_sync(kFull, keep[r]);
-        if (lane == 0) sh.wc[r * nwarps + warp] = __popc(kb[r]);
+        if (lane == 0) wc[r * nwarps + warp] = __popc(kb[r]);
     }
     __syncthreads();
     int m = 0, off[2] = {0, 0};
     for (int e = 0; e < 2 * nwarps; ++e) {
-        const int v = sh.wc[e];
+        const int v = wc[e];
         if (e < warp) off[0] += v;
         if (e < nwarps + warp) off[1] += v;
         m += v;
@@ -438,8 +437,13 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
     return true;
 }
 
+#ifdef ADS_MAXNREG
+#define ADS_SCAN_REGS __maxnreg__(ADS_MAXNREG)
+#else
+#define ADS_SCAN_REGS
+#endif
 template <int VEC, bool FULL>
-__global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+__global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SearchShared sh;
     const int nwarps = blockDim.x >> 5;
@@ -449,14 +453,19 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     double* thr = qseg + a.nseg * kQPitch;
     double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
     double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
-    double* pend_d = topd + a.K;
-    double* pre_s = pend_d + chunk_cap;  // 2 x chunk_cap: untested-prefix sums, by chunk parity
+    // 2 x chunk_cap: untested-prefix sums, by chunk parity.  A chunk's positives'
+    // distances reuse its own prefix half (pend_d = pre_cur): a slot's prefix is
+    // consumed when the slot is claimed, before it can turn positive.
+    double* pre_s = topd + a.K;
     int32_t* lstart = reinterpret_cast<int32_t*>(pre_s + 2 * chunk_cap);
     int32_t* cpos = lstart + a.nprobe;
     Seg* segs = reinterpret_cast<Seg*>(cpos + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
-    int32_t* pend_i = topi + a.K;
-    int32_t* pre = pend_i + chunk_cap;
+    int32_t* pre = topi + a.K;
+    // positives' ids reuse the slot -> position map (read only at the slot's claim)
+    int32_t* pend_i = cpos;
+    // CTA-merge compaction counts: warp 0's gather line (idle at a chunk end)
+    int* wc = reinterpret_cast<int*>(wbuf_all);
     unsigned* pflag = reinterpret_cast<unsigned*>(pre + a.nprobe + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -542,6 +551,7 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
             const int hi = static_cast<int>(lo + span < total ? lo + span : total);
             const int nhi = static_cast<int>(hi + a.step < total ? hi + a.step : total);  // next chunk [hi, nhi)
             double* pre_cur = pre_s + (j & 1) * chunk_cap;
+            double* pend_d = pre_cur;
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
             for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) cpos[sl] = locate(lo + sl);
             if (threadIdx.x == 0) {
@@ -648,7 +658,7 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
             for (int w = 0; w < (n + 31) >> 5; ++w) npos += __popc(pflag[w]);
             int seq = -1;  // >= 0: offer pend[0, seq) sequentially (compacted batch)
             if (npos > 32 && n <= 2 * static_cast<int>(blockDim.x) && sh.cnt <= 2 * static_cast<int>(blockDim.x)) {
-                const int rc = cta_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n);
+                const int rc = cta_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n, wc);
                 if (rc < 0) seq = -rc - 1;
                 npos = 0;
             }
@@ -701,10 +711,10 @@ __global__ void ivf_search_kernel(SearchLaunch a, int chunk_cap) {
 size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
     size_t b = sizeof(float) * a.warps * 1024;
-    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + 3 * chunk_cap);
+    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + 2 * chunk_cap);
     b += sizeof(int32_t) * (a.nprobe + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     b += sizeof(Seg) * a.nseg;
-    b += sizeof(int32_t) * (a.K + chunk_cap + a.nprobe + 1);
+    b += sizeof(int32_t) * (a.K + a.nprobe + 1);
     b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
     return b;
 }
