@@ -445,8 +445,10 @@ def run_search(args, D: Dist):
         "e2e": {"value": world_q / e2e_total, "unit": "queries/s",
                 "h2d_bytes_per_step": nq * d * 4,
                 "d2h_bytes_per_step": nq * K * (4 + 8) + nq * (4 + 8 + 8)},
-        # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, scan
-        "gpu_launches": 5 * args.steps,
+        # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, the
+        # longest-first order (key kernel + CUB radix sort: histogram, bin scan, three
+        # onesweep passes), scan (ncu launch list: profiles/r01g_launches.csv)
+        "gpu_launches": 11 * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "frac_vs_nominal_8000": achieved / 8000.0,
                      "traffic": ncu_traffic(cfg.key),
@@ -663,9 +665,9 @@ def run_search_sharded(args, D: Dist):
         "config": dict(cfg.describe(), nprobe=nprobe, nq_total=nq,
                        parallelism=f"list-sharded x{W} + NCCL all-gather + merge",
                        threshold_exchange={"first_wave_probes": w} if w else None),
-        # per step: 5 search kernels per wave + merge_topk (NCCL collectives and the torch.where
-        # of the exchange are library kernels)
-        "gpu_launches": (11 if w else 6) * args.steps,
+        # per step: 11 search kernels per wave (see run_search) + merge_topk (NCCL collectives
+        # and the torch.where of the exchange are library kernels)
+        "gpu_launches": (23 if w else 12) * args.steps,
         "scanned_gb_per_step_all_ranks": 4.0 * dims / 1e9,
         "clocks": clk,
     }
@@ -769,7 +771,8 @@ def main():
     ap.add_argument("--step", type=int, default=0, help="threshold refresh interval (0: 64 x warps)")
     ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0: 4 for D <= 256, else 10)")
     ap.add_argument("--slots", type=int, default=4, help="queries served concurrently per CTA")
-    ap.add_argument("--query-order", type=int, default=0, help="1: L2-locality query order (experiments)")
+    ap.add_argument("--query-order", type=int, default=2,
+                    help="2: longest queries first (default), 1: L2-locality order, 0: input order")
     ap.add_argument("--same-query", action="store_true", help="experiment: all queries = query 0")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true", help="time (step, warps) variants after setup")

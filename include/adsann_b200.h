@@ -243,9 +243,11 @@ typedef struct {
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */
     int32_t scheduler;     /* 0 query-major (default), 1 list-major waves (16-byte-aligned layouts) */
     int32_t tile;          /* list-major: candidates staged per shared-memory tile (default 64) */
-    int32_t query_order;   /* 1: run the batch's queries in an L2-friendly order (by the
-                              nearest list's position in a nearest-neighbour chain of centroids);
-                              results do not depend on it */
+    int32_t query_order;   /* order in which the batch's queries are served; results do not
+                              depend on it.  2 (default): longest first (descending candidate
+                              count), which shortens the tail of the persistent scan grid;
+                              1: L2-friendly (by the nearest list's position in a
+                              nearest-neighbour chain of centroids); 0: input order */
     int32_t coarse_mode;   /* 0 (default): certified prefilter — approximate distances from a
                               tcgen05 TF32 GEMM (fp32 FMA when D % 4 != 0) with a rigorous error
                               bound — plus exact fp64 rescoring of every centroid that can reach the

@@ -505,7 +505,7 @@ def search_shape(d: int, step: int = 0, warps_per_cta: int = 0) -> tuple:
 
 def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
-                tile: int = 64, query_order: int = 0, coarse_mode: int = 0,
+                tile: int = 64, query_order: int = 2, coarse_mode: int = 0,
                 rotate_mode: int = 0, probe_lo: int = 0, r0=None) -> L.SearchOpts:
     """scheduler 0: query-major, first/step in candidates; scheduler 1: list-major
     waves, first/step in probed lists (see include/adsann_b200.h)."""

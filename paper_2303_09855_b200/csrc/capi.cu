@@ -1058,7 +1058,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->time_stages = 0;
     o->scheduler = 0;
     o->tile = 64;
-    o->query_order = 0;
+    o->query_order = 2;
     o->coarse_mode = 0;
     o->rotate_mode = 0;
     o->probe_lo = 0;
@@ -1213,7 +1213,11 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.out_cand = reinterpret_cast<unsigned long long*>(dcand);
     a.counter = x->ctx->counter;
     a.order = nullptr;
-    if (o.query_order && x->chain_rank && nq > 1) {
+    if (o.query_order == 2 && nq > 1) {  // longest queries first
+        int32_t* ord = x->order.get<int32_t>(nq);
+        launch_query_order_work(probes, nq, nprobe, o.probe_lo, a.list_off, x->order_tmp, ord, st);
+        a.order = ord;
+    } else if (o.query_order == 1 && x->chain_rank && nq > 1) {
         int32_t* ord = x->order.get<int32_t>(nq);
         launch_query_order(probes, nq, nprobe, x->chain_rank, x->k, x->order_tmp, ord, st);
         a.order = ord;

@@ -245,6 +245,10 @@ void launch_merge_topk(const double* dists, const int32_t* ids, int G, int nq, i
 // L2-locality order of a query batch: stable sort by rank[nearest list].
 void launch_query_order(const int32_t* probes, int nq, int nprobe, const int32_t* rank, int k,
                         DevBuf& scratch, int32_t* order, cudaStream_t st);
+// Longest-first order of a query batch: descending candidate count over probe
+// ranks [probe_lo, nprobe) (shortens the tail of the persistent scan grid).
+void launch_query_order_work(const int32_t* probes, int nq, int nprobe, int probe_lo, const int64_t* list_off,
+                             DevBuf& scratch, int32_t* order, cudaStream_t st);
 // Greedy nearest-neighbour chain over the centroids (host, fp32 heuristic):
 // rank[c] = position of list c in the chain.
 std::vector<int32_t> centroid_chain_rank(const float* C, int k, int D);

@@ -747,6 +747,39 @@ void launch_query_order(const int32_t* probes, int nq, int nprobe, const int32_t
     ADS_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, order, nq, 0, bits, st));
 }
 
+namespace {
+// key = 2^24 - 1 - (candidates the query will stream) / 4, so an ascending
+// sort puts the longest queries first
+__global__ void work_keys_kernel(const int32_t* probes, int nq, int nprobe, int probe_lo,
+                                 const int64_t* list_off, uint32_t* keys, int32_t* vals) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    int64_t tot = 0;
+    for (int i = probe_lo; i < nprobe; ++i) {
+        const int p = probes[static_cast<int64_t>(q) * nprobe + i];
+        tot += list_off[p + 1] - list_off[p];
+    }
+    // 24-bit key (three radix passes): candidates / 4, saturating at 2^26
+    const int64_t v = tot >> 2;
+    keys[q] = 0xFFFFFFu - static_cast<uint32_t>(v < 0xFFFFFF ? v : 0xFFFFFF);
+    vals[q] = q;
+}
+}  // namespace
+
+void launch_query_order_work(const int32_t* probes, int nq, int nprobe, int probe_lo, const int64_t* list_off,
+                             DevBuf& scratch, int32_t* order, cudaStream_t st) {
+    uint32_t* kin = scratch.get<uint32_t>(static_cast<size_t>(nq) * 3 + 64);
+    uint32_t* kout = kin + nq;
+    int32_t* vin = reinterpret_cast<int32_t*>(kout + nq);
+    work_keys_kernel<<<(nq + 255) / 256, 256, 0, st>>>(probes, nq, nprobe, probe_lo, list_off, kin, vin);
+    ADS_LAUNCH_CHECK();
+    size_t tmp = 0;
+    ADS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, order, nq, 0, 24, st));
+    static thread_local DevBuf tmpbuf;
+    void* t = tmpbuf.get<unsigned char>(tmp);
+    ADS_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, order, nq, 0, 24, st));
+}
+
 void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,
                         cudaStream_t st) {
     if (nq <= 0 || L <= 0) return;

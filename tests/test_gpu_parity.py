@@ -505,6 +505,21 @@ def test_ivf_empty_lists_and_empty_streams(eng, orc):
         assert (res.ids[empty] == -1).all() and np.isnan(res.dists[empty]).all()
 
 
+def test_ivf_query_order_invariant(eng, orc):
+    """The order in which a batch's queries are served (input, L2 chain, longest first
+    (the default)) changes nothing: ids, dists, dims and candidates are identical, and
+    the default order matches the oracle."""
+    raw, t, qr, qt, P = make_fixture(orc, 6000, 96, 24, 61, 91)
+    lay = oracle_index(orc, raw, t, P, 48, 92, d1=32)
+    idx = gpu_index(eng, lay, P)
+    res = {qo: eng.ivf_query_batch(idx, qt, qr, 10, 9, eng.IvfMode.kAdSplit, opts=eng.search_opts(query_order=qo))
+           for qo in (0, 1, 2)}
+    for qo in (1, 2):
+        for f in ("ids", "dists", "counts", "dims", "candidates"):
+            np.testing.assert_array_equal(getattr(res[qo], f), getattr(res[0], f), err_msg=f"order {qo} {f}")
+    assert_same_results(res[2], orc, lay, qt, qr, 10, 9, "ad-split", 2.1, 32, 10, 256)
+
+
 @pytest.mark.parametrize("probe_lo,rscale", [(0, 1.0), (3, 1.0), (3, 0.5), (5, 2.0), (17, 1.3), (0, 0.0)])
 def test_ivf_probe_range_and_initial_radius(eng, orc, probe_lo, rscale):
     """probe_lo / r0 (the sharded search's second wave): only probe ranks
