@@ -156,6 +156,21 @@ def test_ivf_reference_schedule_bitexact(eng, orc, case):
             assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, dd, 1, 1)
 
 
+@pytest.mark.parametrize("eps,dd", [(0.5, 32), (4.0, 32), (1e6, 32), (2.1, 64), (2.1, 8), (0.2, 16)])
+def test_ivf_epsilon_and_delta_d(eng, orc, eps, dd):
+    """ADSampling knobs beyond the defaults (dco.cpp:32-37: eps0 > 0, 1 <= delta_d <= D):
+    a tight eps0 (many rejections), a loose one, eps0 = 1e6 (never rejects,
+    test_dco.cpp:166-178), and delta_d below / above d1, in both refresh schedules."""
+    raw, t, qr, qt, P = make_fixture(orc, 3000, 128, 24, 21, 301)
+    lay = oracle_index(orc, raw, t, P, 30, 302, d1=32)
+    idx = gpu_index(eng, lay, P)
+    cfg = eng.DcoConfig(eps, dd)
+    for mode in ("ad-split", "ad"):
+        for first, step in ((1, 1), (10, 256)):
+            res = eng.ivf_query_batch(idx, qt, qr, 10, 6, eng.IvfMode(MODE_ID[mode]), cfg, first=first, step=step)
+            assert_same_results(res, orc, lay, qt, qr, 10, 6, mode, eps, dd, first, step)
+
+
 @pytest.mark.parametrize("first,step", [(0, 256), (0, 64), (1, 1000), (37, 5)])
 def test_ivf_batched_schedule_bitexact(eng, orc, first, step):
     """Batched threshold refresh == the oracle's same schedule, bit for bit."""
