@@ -25,9 +25,16 @@
 // round-off (coarse.cu); every centroid that can reach the exact top-nprobe is
 // rescored in fp64, so the probe order stays exact.
 //
-// Rotation (NPROD = 3): Y = X P^T (y_i = sum_j P[i][j] x_j, transform.cpp:99-117)
-// with X = Xh + Xl, P = Ph + Pl split into TF32 pairs and
+// Rotation: Y = X P^T (y_i = sum_j P[i][j] x_j, transform.cpp:99-117) with
+// X = Xh + Xl, P = Ph + Pl split into TF32 pairs and
 // Y ~= Xh Ph^T + Xh Pl^T + Xl Ph^T (the Xl Pl term, ~2^-22 relative, dropped).
+// Default: tc_rotate_pair_kernel, persistent and warp-specialised on CTA pairs
+// (cta_group::2, M = 256 per MMA), the TF32 split of X fused into shared
+// memory, two TMEM accumulators so the epilogue (TMA stores) overlaps the next
+// tile's MMAs.  Kept for A/B (ADS_TC_ROTATE): the one-CTA persistent kernel
+// (tc_rotate_kernel, fused or on a pre-split X) and the tiled kernel below
+// (NPROD = 3) on a pre-split X.  All of them are bit-identical: the same
+// products accumulate in the same K order.
 #include <cuda.h>
 
 #include <cstdint>
