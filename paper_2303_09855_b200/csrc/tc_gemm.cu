@@ -684,11 +684,10 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t n, float*
                                   float* __restrict__ lo) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        uint32_t h, l;
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x[i]));
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x[i] - __uint_as_float(h)));
-        hi[i] = __uint_as_float(h);
-        lo[i] = __uint_as_float(l);
+        float h, l;
+        split_tf32(x[i], h, l);
+        hi[i] = h;
+        lo[i] = l;
     }
 }
 
