@@ -1213,7 +1213,8 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.out_cand = reinterpret_cast<unsigned long long*>(dcand);
     a.counter = x->ctx->counter;
     a.order = nullptr;
-    if (o.query_order == 2 && nq > 1) {  // longest queries first
+    // longest queries first; pointless when the whole batch is resident at once
+    if (o.query_order == 2 && nq > 1 && nq > search_resident_ctas(a)) {
         int32_t* ord = x->order.get<int32_t>(nq);
         launch_query_order_work(probes, nq, nprobe, o.probe_lo, a.list_off, x->order_tmp, ord, st);
         a.order = ord;

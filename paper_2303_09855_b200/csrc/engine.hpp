@@ -102,6 +102,8 @@ struct SearchLaunch {
     const int32_t* order;  // nullable: work item w searches query order[w]
 };
 void launch_ivf_search(const SearchLaunch& a, cudaStream_t st);
+// CTAs of the search grid resident at once (num_sms x occupancy for this launch shape).
+int64_t search_resident_ctas(const SearchLaunch& a);
 
 // Device buffer that only grows (scratch owned by index handles).
 struct DevBuf {

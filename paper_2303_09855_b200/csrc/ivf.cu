@@ -802,26 +802,43 @@ void launch_select_probes(const double* dist, int nq, int L, int nprobe, int32_t
     ADS_LAUNCH_CHECK();
 }
 
-void launch_ivf_search(const SearchLaunch& a_in, cudaStream_t st) {
-    SearchLaunch a = a_in;
-    if (a.nq <= 0) return;
+namespace {
+struct SearchShape {
+    void (*kern)(SearchLaunch, int);
+    int cap;
+    size_t smem;
+    int occ;  // resident CTAs per SM
+};
+
+SearchShape search_shape_of(const SearchLaunch& a) {
     const int64_t cap64 = a.first > a.step ? a.first : a.step;
     if (a.first < 1 || a.step < 1) throw std::invalid_argument("search: threshold schedule must be >= 1");
     if (cap64 > 16384) throw std::invalid_argument("search: threshold refresh interval too long (max 16384)");
-    const int cap = static_cast<int>(cap64);
-    const size_t smem = search_smem(a, cap);
-    auto kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
-                           : ivf_search_kernel<1, false>;
-    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    int occ = 0;
-    ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, a.warps * 32, smem));
-    if (occ < 1) throw std::invalid_argument("search: configuration exceeds shared memory");
-    if (a.ctas_per_sm > 0 && a.ctas_per_sm < occ) occ = a.ctas_per_sm;
+    SearchShape sh{};
+    sh.cap = static_cast<int>(cap64);
+    sh.smem = search_smem(a, sh.cap);
+    sh.kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
+                         : ivf_search_kernel<1, false>;
+    ADS_CUDA(cudaFuncSetAttribute(sh.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sh.smem)));
+    ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sh.occ, sh.kern, a.warps * 32, sh.smem));
+    if (sh.occ < 1) throw std::invalid_argument("search: configuration exceeds shared memory");
+    if (a.ctas_per_sm > 0 && a.ctas_per_sm < sh.occ) sh.occ = a.ctas_per_sm;
+    return sh;
+}
+}  // namespace
+
+int64_t search_resident_ctas(const SearchLaunch& a) {
+    return static_cast<int64_t>(num_sms()) * search_shape_of(a).occ;
+}
+
+void launch_ivf_search(const SearchLaunch& a, cudaStream_t st) {
+    if (a.nq <= 0) return;
+    const SearchShape sh = search_shape_of(a);
     ADS_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
-    int64_t grid = static_cast<int64_t>(num_sms()) * occ;
+    int64_t grid = static_cast<int64_t>(num_sms()) * sh.occ;
     if (grid > a.nq) grid = a.nq;
-    kern<<<static_cast<unsigned>(grid), a.warps * 32, smem, st>>>(a, cap);
+    sh.kern<<<static_cast<unsigned>(grid), a.warps * 32, sh.smem, st>>>(a, sh.cap);
     ADS_LAUNCH_CHECK();
 }
 
