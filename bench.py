@@ -253,6 +253,18 @@ def setup(cfg, dev, rank, log):
     return ads, ctx, base, t, q, m, idx, gt
 
 
+def order_sorted(args, nq: int, d: int) -> bool:
+    """Whether the library sorts the batch longest-first (capi.cu: query_order 2 and more
+    queries than resident search CTAs: 9 per SM for D <= 256 (4-warp CTAs), 3 above)."""
+    try:
+        import torch
+
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        sms = 148
+    return args.query_order == 2 and nq > sms * (9 if d <= 256 else 3)
+
+
 def cpu_baseline_reference(cfg, base, t, m, idx, q, gt, nprobe, budget_s=12.0, log=print):
     """The reference's ivf_query (oracle/_ref, or the oracle port) on the same index,
     run_timed protocol (rotation inside the loop), all host threads, bounded sample."""
@@ -445,10 +457,11 @@ def run_search(args, D: Dist):
         "e2e": {"value": world_q / e2e_total, "unit": "queries/s",
                 "h2d_bytes_per_step": nq * d * 4,
                 "d2h_bytes_per_step": nq * K * (4 + 8) + nq * (4 + 8 + 8)},
-        # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, the
-        # longest-first order (key kernel + CUB radix sort: histogram, bin scan, three
-        # onesweep passes), scan (ncu launch list: profiles/r01g_launches.csv)
-        "gpu_launches": 11 * args.steps,
+        # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, scan, plus
+        # the longest-first order when the batch exceeds one wave of resident CTAs (key
+        # kernel + CUB radix sort: histogram, bin scan, three onesweep passes)
+        # (ncu launch list: profiles/r01g_launches.csv)
+        "gpu_launches": (11 if order_sorted(args, nq, d) else 5) * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "frac_vs_nominal_8000": achieved / 8000.0,
                      "traffic": ncu_traffic(cfg.key),
