@@ -118,7 +118,9 @@ __device__ __forceinline__ unsigned fkey(float x) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-constexpr int kPT = 256;
+// prefilter threads per query (one CTA per query): 128 for nprobe <= 128
+// (twice the queries in flight per SM; +3.8 % end to end at nprobe 8), else 256
+constexpr int kPTSmall = 128, kPTLarge = 256;
 
 // Exact l2_sq(centroid, q) (ivf.cpp:287), reference order, one thread per
 // centroid: the row streams in with 16-float prefetched vector loads while the
@@ -153,6 +155,7 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ c, const do
     return s;
 }
 
+template <int kPT>
 __global__ void __launch_bounds__(kPT) prefilter_kernel(const float* __restrict__ approx, int L,
                                                         const float* __restrict__ Q,
                                                         const float* __restrict__ C, int D, int nprobe,
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kPT) prefilter_kernel(const float* __restrict_
         s_rank = static_cast<unsigned>(nprobe - 1 < 2 * kPT - 1 ? nprobe - 1 : 2 * kPT - 1);
     }
     for (int shift = 24; shift >= 0; shift -= 8) {
-        hist[tid] = 0u;  // kPT == 256 bins
+        for (int b = tid; b < 256; b += kPT) hist[b] = 0u;  // 256 bins
         __syncthreads();
         const unsigned pre = s_prefix;
         const unsigned hmask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
@@ -393,17 +396,18 @@ void launch_coarse_probes_fast(const float* Q, int nq, const float* C, int L, in
     unsigned long long* stats = s.stats.get<unsigned long long>(2);
     ADS_CUDA(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st));
     s.last_nq = nq;
-    if (nprobe > 2 * kPT) throw std::invalid_argument("coarse prefilter: nprobe > 512 (use coarse_mode 1)");
+    if (nprobe > 2 * kPTLarge) throw std::invalid_argument("coarse prefilter: nprobe > 512 (use coarse_mode 1)");
+    const int pt = nprobe <= kPTSmall ? kPTSmall : kPTLarge;
     int cap = 4 * nprobe + 256;
     if (cap > L) cap = L;
-    int P2 = 2 * kPT;  // also hosts the 2*kPT threshold keys
+    int P2 = 2 * pt;  // also hosts the 2*pt threshold keys and the 256 radix bins
+    if (P2 < 256) P2 = 256;
     while (P2 < cap) P2 <<= 1;
     const size_t smem = static_cast<size_t>(P2) * (sizeof(double) + sizeof(int32_t)) + sizeof(double) * D;
     if (smem > 200 * 1024) throw std::invalid_argument("coarse: nprobe too large for the prefilter");
-    ADS_CUDA(cudaFuncSetAttribute(prefilter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    prefilter_kernel<<<nq, kPT, smem, st>>>(approx, L, Q, C, D, nprobe, qnrm, cmax, gamma, cap, P2, probes,
-                                            stats);
+    auto kern = pt == kPTSmall ? prefilter_kernel<kPTSmall> : prefilter_kernel<kPTLarge>;
+    ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<nq, pt, smem, st>>>(approx, L, Q, C, D, nprobe, qnrm, cmax, gamma, cap, P2, probes, stats);
     ADS_LAUNCH_CHECK();
 }
 

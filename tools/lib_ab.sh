@@ -11,7 +11,7 @@ echo "variant parity rc=$?" >> gpurun_out/lib_ab.log
 for cfg in ${CFGS:-2}; do
   for rep in 1 2 3; do
     for lib in paper_2303_09855_b200/libadsann_b200.so $V; do
-      ADS_LIB_PATH=$lib timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null \
+      ADS_LIB_PATH=$lib timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS:-} 2>/dev/null \
         | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg $cfg', '$lib'.split('/')[-1], round(d['value']), 'scan', round(d['stages_ms']['scan'], 3), d['clocks']['sm_mhz'])" \
         >> gpurun_out/lib_ab.log 2>&1
     done
