@@ -40,6 +40,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <string>
 
 #include "engine.hpp"
@@ -132,6 +133,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+
+// Epilogue transforms of the persistent kernels: value stored at (row, col).
+struct XfId {
+    __device__ __forceinline__ float operator()(int, int, float v) const { return v; }
+};
+struct XfCoarse {  // approx(q, c) = (|q~|^2 + |c~|^2) - 2 q^.c^ (the tiled CoarseEpi's arithmetic)
+    const float* qn2;
+    const float* cn2;
+    int M, N;
+    __device__ __forceinline__ float operator()(int r, int c, float v) const {
+        return (r < M && c < N) ? (qn2[r] + cn2[c]) - 2.f * v : 0.f;
+    }
+};
 
 // Epilogues: called with (row, col, accumulator) for in-range elements.
 struct CoarseEpi {
@@ -292,17 +306,20 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
 // block in place into its TF32 pair (hi over x, lo beside it; the same
 // cvt.rna arithmetic as split_tf32_kernel, so the result is bit-identical),
 // then release the stage to the MMA issuer through `conv`.
-template <int BN, int STAGES, int KB, bool FUSED, int CW = 4, int EPIB = 2>
+template <int BN, int STAGES, int KB, bool FUSED, int CW = 4, int EPIB = 2, int NPROD = 3, class Xf = XfId>
 __global__ void __launch_bounds__(192 + (FUSED ? 32 * CW : 0), 1) tc_rotate_kernel(const __grid_constant__ CUtensorMap tXh,
                                                            const __grid_constant__ CUtensorMap tXl,
                                                            const __grid_constant__ CUtensorMap tPh,
                                                            const __grid_constant__ CUtensorMap tPl,
                                                            const __grid_constant__ CUtensorMap tY, int M, int N,
-                                                           int K) {
+                                                           int K, Xf xf) {
     static_assert(KB == 32 || KB == 16 || KB == 8, "K block: one 128-, 64- or 32-byte swizzle row");
     static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN: 32-column epilogue chunks, MMA N <= 256");
+    static_assert(NPROD == 3 || (NPROD == 1 && !FUSED), "NPROD 1: one plain TF32 product (A = Xh, B = Ph)");
     constexpr int ATILE = kTM * KB * 4, BTILE = BN * KB * 4;
-    constexpr int STAGE = 2 * ATILE + 2 * BTILE;
+    // NPROD 3: [Xh | Xl | Ph | Pl]; NPROD 1: [Xh | Ph]
+    constexpr int STAGE = NPROD == 3 ? 2 * ATILE + 2 * BTILE : ATILE + BTILE;
+    constexpr int BOFF = NPROD == 3 ? 2 * ATILE : ATILE;
     constexpr uint32_t IDESC = idesc_tf32<BN>();
     constexpr uint32_t TCOLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -354,9 +371,9 @@ __global__ void __launch_bounds__(192 + (FUSED ? 32 * CW : 0), 1) tc_rotate_kern
                     unsigned char* st = smem + s * STAGE;
                     mbar_expect(&full[s], FUSED ? STAGE - ATILE : STAGE);
                     tma_load(st, &tXh, &full[s], kb * KB, m0);
-                    if constexpr (!FUSED) tma_load(st + ATILE, &tXl, &full[s], kb * KB, m0);
-                    tma_load(st + 2 * ATILE, &tPh, &full[s], kb * KB, n0);
-                    tma_load(st + 2 * ATILE + BTILE, &tPl, &full[s], kb * KB, n0);
+                    if constexpr (NPROD == 3 && !FUSED) tma_load(st + ATILE, &tXl, &full[s], kb * KB, m0);
+                    tma_load(st + BOFF, &tPh, &full[s], kb * KB, n0);
+                    if constexpr (NPROD == 3) tma_load(st + BOFF + BTILE, &tPl, &full[s], kb * KB, n0);
                 }
             }
         }
@@ -377,14 +394,16 @@ __global__ void __launch_bounds__(192 + (FUSED ? 32 * CW : 0), 1) tc_rotate_kern
                     const uint32_t sa = smem_u32(st);
                     const uint64_t xh = swz_desc<KB>(sa);
                     const uint64_t xl = swz_desc<KB>(sa + ATILE);
-                    const uint64_t ph_ = swz_desc<KB>(sa + 2 * ATILE);
-                    const uint64_t pl = swz_desc<KB>(sa + 2 * ATILE + BTILE);
+                    const uint64_t ph_ = swz_desc<KB>(sa + BOFF);
+                    const uint64_t pl = swz_desc<KB>(sa + BOFF + BTILE);
 #pragma unroll
                     for (int k = 0; k < KB / 8; ++k) {
                         const uint64_t dk = static_cast<uint64_t>(k * 2);
                         umma_tf32(d, xh + dk, ph_ + dk, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
-                        umma_tf32(d, xh + dk, pl + dk, IDESC, 1u);
-                        umma_tf32(d, xl + dk, ph_ + dk, IDESC, 1u);
+                        if constexpr (NPROD == 3) {
+                            umma_tf32(d, xh + dk, pl + dk, IDESC, 1u);
+                            umma_tf32(d, xl + dk, ph_ + dk, IDESC, 1u);
+                        }
                     }
                     umma_commit(&empty[s]);
                 }
@@ -437,6 +456,11 @@ __global__ void __launch_bounds__(192 + (FUSED ? 32 * CW : 0), 1) tc_rotate_kern
                 }
                 __syncwarp();
                 // row = lane; 16-byte chunk c of the row lands at c ^ (row & 7) (SWIZZLE_128B)
+                {  // epilogue transform (identity for the rotation)
+                    const int row = m0 + q * 32 + static_cast<int>(lane);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(xf(row, n0 + cb + j, __uint_as_float(v[j])));
+                }
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     const int pc = c ^ static_cast<int>(lane & 7u);
@@ -749,6 +773,25 @@ double tc_coarse_gamma(int D) {
 void launch_tc_coarse_gemm(const float* Qc, int nq, const float* Cc, int L, int D, const float* qn2,
                            const float* cn2, float* out, cudaStream_t st) {
     if (nq <= 0 || L <= 0) return;
+    static const bool tiled = [] {
+        const char* e = std::getenv("ADS_TC_COARSE");
+        return e && e[0] == '0';
+    }();
+    if (!tiled && L % 4 == 0) {  // the TMA-stored output needs 16-byte row strides
+        // persistent, one product, 256-column tiles of K-16 blocks; the epilogue forms
+        // approx = (|q~|^2 + |c~|^2) - 2 v and leaves through TMA stores
+        constexpr int BN = 256, STAGES = 6, KB = 16;
+        constexpr int smem = STAGES * (kTM * KB * 4 + BN * KB * 4) + 4 * 2 * 4096 + 1024;
+        const CUtensorMap a = tile_map(Qc, D, nq, kTM, KB), b = tile_map(Cc, D, L, BN, KB);
+        const CUtensorMap y = tile_map(out, L, nq, 32, 32);
+        auto kern = tc_rotate_kernel<BN, STAGES, KB, false, 4, 2, 1, XfCoarse>;
+        ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const int64_t tiles = (static_cast<int64_t>(nq + kTM - 1) / kTM) * ((L + BN - 1) / BN);
+        const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+        kern<<<grid, 192, smem, st>>>(a, a, b, b, y, nq, L, D, XfCoarse{qn2, cn2, nq, L});
+        ADS_LAUNCH_CHECK();
+        return;
+    }
     const CUtensorMap a = tile_map(Qc, D, nq, kTM);
     const CUtensorMap b = tile_map(Cc, D, L, 256);
     // short K: two stages (96 KB, two CTAs per SM overlap one's epilogue with the
@@ -810,7 +853,7 @@ void launch_rotate(const float* Xh, const float* Xl, int64_t n, const float* Ph,
     ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t tiles = ((n + kTM - 1) / kTM) * ((D + BN - 1) / BN);
     const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-    kern<<<grid, 192 + (FUSED ? 32 * CW : 0), smem, st>>>(xh, xl, ph, pl, y, static_cast<int>(n), D, D);
+    kern<<<grid, 192 + (FUSED ? 32 * CW : 0), smem, st>>>(xh, xl, ph, pl, y, static_cast<int>(n), D, D, XfId{});
     ADS_LAUNCH_CHECK();
 }
 }  // namespace
