@@ -233,7 +233,7 @@ __device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double 
 
 struct SearchShared {
     double r, r_sq;
-    int q, stop, total, next, cnt, pnext, fast_active;
+    int q, stop, total, next, cnt, pnext;
     int pcount[2];
     unsigned long long dims;
 };
@@ -437,30 +437,13 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
     return true;
 }
 
-// Certified fp32 walk (MIXED): bound factors at depth d.  With S the exact sum,
-// |s32 - S| <= g32 S + nabs and |s64 - S| <= g64 S, g(n, u) = n u / (1 - n u),
-// n = d + 3 (difference, square, d additions, one rounding of an exact prefix
-// to fp32), nabs covering fp32 underflow; lo/hi absorb the test's own two fp64
-// roundings (the 1 % widening of g32 dwarfs them).
-__device__ __forceinline__ double2 f32_band(int d) {
-    const double n = d + 3;
-    const double g32 = 1.01 * n * 0x1p-24 / (1.0 - n * 0x1p-24);
-    const double g64 = 1.01 * n * 0x1p-53 / (1.0 - n * 0x1p-53);
-    return make_double2((1.0 - g64) / (1.0 + g32) * (1.0 - 0x1p-50), (1.0 + g64) / (1.0 - g32) * (1.0 + 0x1p-50));
-}
-
 #ifdef ADS_MAXNREG
 #define ADS_SCAN_REGS __maxnreg__(ADS_MAXNREG)
 #else
 #define ADS_SCAN_REGS
 #endif
-// MIXED: warps 0 .. nwarps-2 walk in certified fp32 and hand every candidate
-// the band cannot decide (and every possible positive) to the last warp, which
-// walks exactly in fp64 (the reference arithmetic), re-walking those while the
-// others continue; results are identical to the all-fp64 kernel.
-template <int VEC, bool FULL, bool MIXED = false>
+template <int VEC, bool FULL>
 __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
-    static_assert(!MIXED || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SearchShared sh;
     const int nwarps = blockDim.x >> 5;
@@ -484,29 +467,12 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     // CTA-merge compaction counts: warp 0's gather line (idle at a chunk end)
     int* wc = reinterpret_cast<int*>(wbuf_all);
     unsigned* pflag = reinterpret_cast<unsigned*>(pre + a.nprobe + 1);
-    // MIXED: slots handed to the exact warp / taken by it, its pick list, the
-    // query staged as fp32 and the per-test band factors
-    unsigned* vflag = pflag + ((chunk_cap + 31) >> 5);
-    unsigned* vtaken = vflag + ((chunk_cap + 31) >> 5);
-    int* vlist = reinterpret_cast<int*>(vtaken + ((chunk_cap + 31) >> 5));
-    auto align16 = [](void* p) {
-        return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
-    };
-    float* qsegf = reinterpret_cast<float*>(align16(vlist + 32));
-    double2* gband = reinterpret_cast<double2*>(align16(qsegf + a.nseg * kQPitchF));  // padded as in search_smem
 
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     float* wbuf = wbuf_all + warp * 1024;
-    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) {
-        const Seg sg = a.segs[i];
-        segs[i] = sg;
-        if (MIXED && sg.test >= 0) gband[sg.test] = f32_band(sg.col + sg.len);
-    }
+    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
     for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) tfac[i] = a.tfac[i];
-    const double2 band_d = f32_band(a.D);
-    const double nabs = (a.D + 3) * 0x1p-148;
-    const bool exact_warp = !MIXED || warp == nwarps - 1;
     // VEC=4 line descriptor = pos * stride + column offset, 16-byte units from a.a1
     const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
     const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
@@ -549,7 +515,6 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
         if (sh.stop) break;
         const int qi = sh.q;
         stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
-        if constexpr (MIXED) stage_query_f32(qsegf, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
         for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = __dmul_rn(tfac[i], sh.r_sq);
         if (warp == 0) {  // probed lists -> stream prefix offsets
             int carry = 0;
@@ -589,73 +554,21 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
             double* pend_d = pre_cur;
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
             for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) cpos[sl] = locate(lo + sl);
-            // MIXED and no finite radius yet: the band decides nothing, every warp walks exactly
-            const bool open = !(sh.r_sq < kInf);
-            const bool exact_mode = exact_warp || open;
             if (threadIdx.x == 0) {
                 sh.next = lo;
                 sh.pnext = 0;
-                sh.fast_active = (MIXED && !open) ? nwarps - 1 : 0;
             }
-            for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) {
-                pflag[w] = 0;
-                if constexpr (MIXED) {
-                    vflag[w] = 0;
-                    vtaken[w] = 0;
-                }
-            }
+            for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
             __syncthreads();
             const double r = sh.r, r_sq = sh.r_sq;
             const int pc = sh.pcount[j & 1];  // [lo, lo + pc) carry their prefix in pre_cur
-            // prework (next chunk's untested prefixes, fp64) only by exact-mode warps
-            const bool can_pre = nseg0 > 0 && nhi > hi && exact_mode;
-            // fp32 final test: certainly negative above rfin (kFd: sqrt(s) > r is
-            // certain once s > r_sq (1 + 2^-48))
-            const double rfin = a.final_fd ? __dmul_rn(r_sq, 1.0 + 0x1p-47) : r_sq;
+            const bool can_pre = nseg0 > 0 && nhi > hi;
 
             int cand = -1, seg = 0, pos = 0;
             bool prew = false;  // lane holds a next-chunk candidate's untested prefix
             double s = 0.0;
-            float sf = 0.f;  // MIXED fast warps
             for (;;) {
                 unsigned need = __ballot_sync(kFull, cand < 0);
-                if (MIXED && exact_warp && !open && need) {
-                    // slots the fp32 warps could not decide come first (exact re-walk)
-                    int nv = 0;
-                    if (lane == 0) {
-                        const int want = __popc(need);
-                        const int nw = (hi - lo + 31) >> 5;
-                        for (int w = 0; w < nw && nv < want; ++w) {
-                            unsigned pnd = *reinterpret_cast<volatile unsigned*>(&vflag[w]) & ~vtaken[w];
-                            while (pnd && nv < want) {
-                                const int b = __ffs(pnd) - 1;
-                                pnd &= pnd - 1;
-                                vtaken[w] |= 1u << b;
-                                vlist[nv++] = w * 32 + b;
-                            }
-                        }
-                    }
-                    nv = __shfl_sync(kFull, nv, 0);
-                    __syncwarp();
-                    if (cand < 0) {
-                        const int k = __popc(need & ((1u << lane) - 1u));
-                        if (k < nv) {
-                            const int slot = vlist[k];
-                            cand = lo + slot;
-                            pos = cpos[slot];
-                            prew = false;
-                            if (slot < pc) {
-                                seg = nseg0;
-                                s = pre_cur[slot];
-                            } else {
-                                seg = 0;
-                                s = 0.0;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                    need = __ballot_sync(kFull, cand < 0);
-                }
                 if (need) {
                     int base = 0;
                     if (lane == 0) base = atomicAdd(&sh.next, __popc(need));
@@ -673,7 +586,6 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                                 seg = 0;
                                 s = 0.0;
                             }
-                            if constexpr (MIXED) sf = static_cast<float>(s);
                         }
                     }
                     if (can_pre) {
@@ -695,25 +607,7 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                         }
                     }
                 }
-                if (!__any_sync(kFull, cand >= 0)) {
-                    if (!MIXED || open) break;
-                    if (!exact_warp) {  // fp32 warp done: hand over to the exact warp
-                        __threadfence_block();
-                        if (lane == 0) atomicSub(&sh.fast_active, 1);
-                        break;
-                    }
-                    // exact warp: leave once every fp32 warp is done and nothing is pending
-                    if (*reinterpret_cast<volatile int*>(&sh.fast_active) == 0) {
-                        __threadfence_block();
-                        int pending = 0;
-                        for (int w = static_cast<int>(lane); w < ((hi - lo + 31) >> 5); w += 32)
-                            pending |= *reinterpret_cast<volatile unsigned*>(&vflag[w]) & ~vtaken[w];
-                        if (!__any_sync(kFull, pending != 0)) break;
-                    } else {
-                        __nanosleep(64);
-                    }
-                    continue;
-                }
+                if (!__any_sync(kFull, cand >= 0)) break;
                 const Seg sg = segs[seg];
                 if constexpr (VEC == 4) {
                     uint32_t dsc = kNoLine;
@@ -728,35 +622,7 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 }
                 cp_async_wait_group<0>();
                 __syncwarp();
-                if (MIXED && !exact_mode) {
-                    if (cand >= 0) {
-                        sf = accumulate_line_f32(wbuf, qsegf + seg * kQPitchF, sf);
-                        // decide only what the band proves; hand the rest to the exact warp
-                        const double sd = sf;
-                        int verdict = 0;  // 1 reject, 2 undecided, 3 certainly negative at D
-                        if (sg.test >= 0) {
-                            const double t = thr[sg.test];
-                            const double2 g = gband[sg.test];
-                            if (__dmul_rn(sd - nabs, g.x) > t) verdict = 1;
-                            else if (!(__dmul_rn(sd + nabs, g.y) <= t)) verdict = 2;
-                        }
-                        if (verdict == 0 && seg == a.nseg - 1)
-                            verdict = __dmul_rn(sd - nabs, band_d.x) > rfin ? 3 : 2;
-                        if (verdict == 1) {
-                            my_dims += static_cast<unsigned long long>(sg.col + sg.len);
-                            cand = -1;
-                        } else if (verdict == 3) {
-                            my_dims += static_cast<unsigned long long>(a.D);
-                            cand = -1;
-                        } else if (verdict == 2) {
-                            const int slot = cand - lo;
-                            atomicOr(&vflag[slot >> 5], 1u << (slot & 31));
-                            cand = -1;
-                        } else {
-                            ++seg;
-                        }
-                    }
-                } else if (cand >= 0) {
+                if (cand >= 0) {
                     s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
                     if (prew) {
                         if (seg + 1 == nseg0) {
@@ -850,13 +716,6 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + a.nprobe + 1);
     b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
-    if (a.f32) {  // MIXED extras: vflag, vtaken, vlist[32], fp32 query, band factors
-        b += sizeof(unsigned) * 2 * ((chunk_cap + 31) / 32) + sizeof(int) * 32;
-        b = (b + 15) & ~static_cast<size_t>(15);
-        b += sizeof(float) * a.nseg * kQPitchF;
-        b = (b + 15) & ~static_cast<size_t>(15);
-        b += 16 * (a.ntest > 0 ? a.ntest : 1);
-    }
     return b;
 }
 
@@ -958,9 +817,7 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     SearchShape sh{};
     sh.cap = static_cast<int>(cap64);
     sh.smem = search_smem(a, sh.cap);
-    const bool mixed = a.f32 && a.vec == 4 && a.full && a.warps >= 2;
-    sh.kern = a.vec == 4 ? (a.full ? (mixed ? ivf_search_kernel<4, true, true> : ivf_search_kernel<4, true>)
-                                   : ivf_search_kernel<4, false>)
+    sh.kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
                          : ivf_search_kernel<1, false>;
     ADS_CUDA(cudaFuncSetAttribute(sh.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sh.smem)));
