@@ -596,14 +596,14 @@ static void heap_offer(heap_t *h, double dist, int32_t id) {
 static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                           int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                           int64_t step, int32_t probe_lo, double r0, const int32_t *waves,
-                          int32_t nwaves, int32_t *ids, double *dists, int32_t *count,
+                          int32_t nwaves, int32_t lag, int32_t *ids, double *dists, int32_t *count,
                           uint64_t *stats);
 
 int orc_ivf_query(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                   int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                   int64_t step, int32_t *ids, double *dists, int32_t *count, uint64_t *stats) {
     return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, 0, INFINITY,
-                          NULL, 0, ids, dists, count, stats);
+                          NULL, 0, 0, ids, dists, count, stats);
 }
 
 int orc_ivf_query_waves(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
@@ -611,7 +611,7 @@ int orc_ivf_query_waves(const orc_ivf *idx, const float *q_t, const float *q_raw
                         const int32_t *wave_ranks, int32_t nwaves, int32_t *ids, double *dists,
                         int32_t *count, uint64_t *stats) {
     return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, 1, 1, 0, INFINITY,
-                          wave_ranks, nwaves, ids, dists, count, stats);
+                          wave_ranks, nwaves, 0, ids, dists, count, stats);
 }
 
 int orc_ivf_query_ext(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
@@ -621,7 +621,19 @@ int orc_ivf_query_ext(const orc_ivf *idx, const float *q_t, const float *q_raw, 
     if (probe_lo < 0 || probe_lo > nprobe) return fail(1, "ivf_query: probe_lo must be in [0, n_probe]");
     if (!(r0 >= 0.0)) return fail(1, "ivf_query: the initial radius must be >= 0");
     return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, probe_lo, r0,
-                          NULL, 0, ids, dists, count, stats);
+                          NULL, 0, 0, ids, dists, count, stats);
+}
+
+/* lag = 1: the positives of a chunk are offered one refresh later, so the
+ * candidates of chunk j see the heap after chunks 0 .. j-2 (the GPU's mixed
+ * scan re-walks a chunk's undecided candidates during the next chunk). */
+int orc_ivf_query_lag(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                      int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
+                      int64_t step, int32_t lag, int32_t *ids, double *dists, int32_t *count,
+                      uint64_t *stats) {
+    if (lag < 0 || lag > 1) return fail(1, "ivf_query: lag must be 0 or 1");
+    return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, 0, INFINITY,
+                          NULL, 0, lag, ids, dists, count, stats);
 }
 
 /* probe_lo / r0 (the sharded search's second wave): only the lists at probe
@@ -631,7 +643,7 @@ int orc_ivf_query_ext(const orc_ivf *idx, const float *q_t, const float *q_raw, 
 static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                           int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                           int64_t step, int32_t probe_lo, double r0, const int32_t *waves,
-                          int32_t nwaves, int32_t *ids, double *dists, int32_t *count,
+                          int32_t nwaves, int32_t lag, int32_t *ids, double *dists, int32_t *count,
                           uint64_t *stats) {
     /* ivf.cpp:299-307 */
     if (K < 1) return fail(1, "ivf_query: K must be >= 1");
@@ -665,6 +677,9 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
     for (int32_t i = probe_lo; i < nprobe; ++i) total += idx->list_off[probes[i] + 1] - idx->list_off[probes[i]];
     pair_t *pending = malloc(sizeof(pair_t) * (size_t)(total > 0 ? total : 1));
     int64_t npend = 0;
+    /* lag 1: the previous chunk's positives, offered at the next refresh */
+    pair_t *held = malloc(sizeof(pair_t) * (size_t)(total > 0 ? total : 1));
+    int64_t nheld = 0;
     uint64_t dims = 0;
     double r = r0;
 
@@ -704,7 +719,15 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
         const int32_t c = probes[pi];
         for (int64_t p = idx->list_off[c]; p < idx->list_off[c + 1]; ++p, ++i) {
             if (i == 0 || (waves ? mark[i] : (i >= first && (i - first) % step == 0))) {
-                for (int64_t j = 0; j < npend; ++j) heap_offer(&heap, pending[j].dist, pending[j].id);
+                if (lag) {
+                    for (int64_t j = 0; j < nheld; ++j) heap_offer(&heap, held[j].dist, held[j].id);
+                    pair_t *t = held;
+                    held = pending;
+                    pending = t;
+                    nheld = npend;
+                } else {
+                    for (int64_t j = 0; j < npend; ++j) heap_offer(&heap, pending[j].dist, pending[j].id);
+                }
                 npend = 0;
                 const double ht = heap_threshold(&heap); /* ivf.cpp:331, 391 */
                 r = ht < r0 ? ht : r0;
@@ -732,6 +755,7 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
             }
         }
     }
+    for (int64_t j = 0; j < nheld; ++j) heap_offer(&heap, held[j].dist, held[j].id);
     for (int64_t j = 0; j < npend; ++j) heap_offer(&heap, pending[j].dist, pending[j].id);
 
     *count = heap.cnt;
@@ -746,6 +770,7 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
     free(probes);
     free(heap.a);
     free(pending);
+    free(held);
     free(prefix);
     free(mark);
     return 0;

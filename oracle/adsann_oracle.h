@@ -123,6 +123,12 @@ int orc_ivf_query_ext(const orc_ivf *idx, const float *q_t, const float *q_raw, 
                       int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                       int64_t step, int32_t probe_lo, double r0, int32_t *ids, double *dists,
                       int32_t *count, uint64_t *stats);
+/* lag 1: a chunk's positives are offered one refresh later (chunk j sees the
+ * heap after chunks 0 .. j-2); lag 0 = orc_ivf_query. */
+int orc_ivf_query_lag(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
+                      int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
+                      int64_t step, int32_t lag, int32_t *ids, double *dists, int32_t *count,
+                      uint64_t *stats);
 int orc_probe_order(const float *centroids, int32_t L, int32_t d, const float *q,
                     int32_t nprobe, int32_t *order);
 

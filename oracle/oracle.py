@@ -197,6 +197,9 @@ class Oracle(_Common):
         self._fn("orc_ivf_query_ext", [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int, C.c_double,
                                        C.c_int32, C.c_int64, C.c_int64, C.c_int32, C.c_double, _i32p,
                                        _f64p, C.POINTER(C.c_int32), _u64p])
+        self._fn("orc_ivf_query_lag", [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int, C.c_double,
+                                       C.c_int32, C.c_int64, C.c_int64, C.c_int32, _i32p, _f64p,
+                                       C.POINTER(C.c_int32), _u64p])
         self._fn("orc_verify_theory", [_f32p, C.c_int32, C.c_int32, _f32p, C.c_int32, C.c_int32,
                                        _f64p, C.c_int32, _f64p, _u64p, _u64p,
                                        C.POINTER(C.c_uint64)])
@@ -230,10 +233,11 @@ class Oracle(_Common):
         return out
 
     def ivf_query(self, index, q_t, q_raw, K, nprobe, mode, eps0=2.1, delta_d=32, first=1, step=1,
-                  waves=None, probe_lo=0, r0=float("inf")):
+                  waves=None, probe_lo=0, r0=float("inf"), lag=0):
         """Returns (ids, dists, stats[dims, dco, cand]).  first=step=1 == reference;
         waves = ascending probe ranks where the threshold is refreshed (list-major schedule);
-        probe_lo / r0: scan only probe ranks [probe_lo, nprobe) with the radius starting at r0."""
+        probe_lo / r0: scan only probe ranks [probe_lo, nprobe) with the radius starting at r0;
+        lag = 1: a chunk's positives are offered one refresh later (the mixed GPU scan)."""
 
         class _Ivf(C.Structure):
             _fields_ = [("n", C.c_int32), ("d", C.c_int32), ("k", C.c_int32), ("d1", C.c_int32),
@@ -257,6 +261,10 @@ class Oracle(_Common):
             self._check(self._ivf_query_waves(C.addressof(s), _nullable(qt), _nullable(qr), K, nprobe,
                                               m, eps0, delta_d, w, len(w), ids, dists, C.byref(cnt),
                                               stats))
+        elif lag:
+            self._check(self._ivf_query_lag(C.addressof(s), _nullable(qt), _nullable(qr), K, nprobe, m,
+                                            eps0, delta_d, first, step, lag, ids, dists, C.byref(cnt),
+                                            stats))
         elif probe_lo or r0 != float("inf"):
             self._check(self._ivf_query_ext(C.addressof(s), _nullable(qt), _nullable(qr), K, nprobe, m,
                                             eps0, delta_d, first, step, probe_lo, r0, ids, dists,
