@@ -3,7 +3,6 @@
 // segment plans, and the kernel launch sequence.  No compute runs on the
 // host: every DCO, distance, transform, selection and k-means step is a
 // kernel in this library.
-#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1201,10 +1200,6 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     if (gap < 0 || gap % 4 != 0 || units >= int64_t(0xffffffff)) {
         a.vec = 1;
         a.full = 0;
-    }
-    {
-        const char* e = std::getenv("ADS_SCAN_MIXED");
-        a.f32 = (e && e[0] == '1') ? 1 : 0;
     }
     a.first = o.first;
     a.step = o.step;

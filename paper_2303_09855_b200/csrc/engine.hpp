@@ -89,7 +89,6 @@ struct SearchLaunch {
     const double* tfac;
     int nseg, ntest, vec;
     int full;          // every segment is 32 floats (no per-line length shuffle)
-    int f32;           // MIXED: certified fp32 walkers + one exact fp64 warp (full lines only)
     int64_t first, step;
     int warps;         // per CTA
     int slots;         // queries served concurrently per CTA

@@ -243,9 +243,6 @@ struct SearchShared {
 // in candidate order to pend_d/pend_i[0, m) first.  Returns m on success,
 // -(m + 1) on a tie (the compacted batch is then offered sequentially).
 // Needs n <= 2 * blockDim.x and sh.cnt <= 2 * blockDim.x; call with all threads.
-// Tag: one instantiation per kernel (a shared non-inlined callee would be
-// compiled for the larger register budget of the two).
-template <int Tag = 0>
 __device__ __noinline__ int cta_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, int K, double* pend_d,
                                int32_t* pend_i, const unsigned* pflag, int n, int* wc) {
     const int tid = threadIdx.x, nthr = blockDim.x, nwarps = nthr >> 5, warp = tid >> 5;
@@ -711,187 +708,6 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     }
 }
 
-// Certified fp32 walk (MIXED): bound factors at depth d.  With S the exact sum,
-// |s32 - S| <= g32 S + nabs and |s64 - S| <= g64 S, g(n, u) = n u / (1 - n u),
-// n = d + 3 (difference, square, d additions, one rounding of an exact prefix
-// to fp32), nabs covering fp32 underflow; lo/hi absorb the test's own two fp64
-// roundings (the 1 % widening of g32 dwarfs them).
-__device__ __forceinline__ double2 f32_band(int d) {
-    const double n = d + 3;
-    const double g32 = 1.01 * n * 0x1p-24 / (1.0 - n * 0x1p-24);
-    const double g64 = 1.01 * n * 0x1p-53 / (1.0 - n * 0x1p-53);
-    return make_double2((1.0 - g64) / (1.0 + g32) * (1.0 - 0x1p-50), (1.0 + g64) / (1.0 - g32) * (1.0 + 0x1p-50));
-}
-
-// MIXED scan (lag-1 schedule, orc_ivf_query_lag): warps 0 .. nwarps-2 walk in
-// certified fp32 and hand every candidate the band cannot decide (and every
-// possible positive) to the last warp, which walks exactly in fp64 and re-walks
-// chunk j's hand-overs during chunk j + 1; chunk j's positives are merged at the
-// end of chunk j + 1, so chunk j is tested against the heap after chunk j - 2.
-// A separate kernel so the exact kernel's code generation stays untouched.
-__global__ void __launch_bounds__(128, 8) ivf_search_mixed_kernel(SearchLaunch a, int chunk_cap) {
-    constexpr int VEC = 4;
-    constexpr bool FULL = true;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ SearchShared sh;
-    const int nwarps = blockDim.x >> 5;
-    // dynamic layout (8-byte items first)
-    float* wbuf_all = reinterpret_cast<float*>(smem_raw);
-    double* qseg = reinterpret_cast<double*>(wbuf_all + nwarps * 1024);
-    double* thr = qseg + a.nseg * kQPitch;
-    double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
-    double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
-    // 2 x chunk_cap: untested-prefix sums, by chunk parity.  A chunk's positives'
-    // distances reuse its own prefix half (pend_d = pre_cur): a slot's prefix is
-    // consumed when the slot is claimed, before it can turn positive.
-    double* pre_s = topd + a.K;
-    int32_t* lstart = reinterpret_cast<int32_t*>(pre_s + 2 * chunk_cap);
-    int32_t* cpos = lstart + a.nprobe;
-    Seg* segs = reinterpret_cast<Seg*>(cpos + chunk_cap + ((chunk_cap + a.nprobe) & 1));
-    int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
-    int32_t* pre = topi + a.K;
-    // positives' ids reuse the slot -> position map (read only at the slot's claim)
-    int32_t* pend_i = cpos;
-    // CTA-merge compaction counts: warp 0's gather line (idle at a chunk end)
-    int* wc = reinterpret_cast<int*>(wbuf_all);
-    unsigned* pflag = reinterpret_cast<unsigned*>(pre + a.nprobe + 1);
-    // MIXED extras (search_smem): second-parity chunk state, hand-over flags,
-    // the fp32 query, band factors, per-parity thresholds and positives
-    struct MixedSmem {
-        int W, nt1;
-        unsigned *pflagB, *vflag2, *vtaken2;
-        int *vlist;
-        int32_t *cposB, *pend_i2;
-        float* qsegf;
-        double2* gband;
-        double *thr2, *pend_d2;
-    };
-    auto mixed_smem = [&]() {
-        MixedSmem m;
-        auto align16 = [](void* p) {
-            return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) &
-                                                    ~static_cast<uintptr_t>(15));
-        };
-        m.W = (chunk_cap + 31) >> 5;
-        m.nt1 = a.ntest > 0 ? a.ntest : 1;
-        m.pflagB = pflag + m.W;
-        m.vflag2 = m.pflagB + m.W;
-        m.vtaken2 = m.vflag2 + 2 * m.W;
-        m.vlist = reinterpret_cast<int*>(m.vtaken2 + 2 * m.W);
-        m.cposB = m.vlist + 32;
-        m.pend_i2 = m.cposB + chunk_cap;
-        m.qsegf = reinterpret_cast<float*>(align16(m.pend_i2 + 2 * chunk_cap));
-        m.gband = reinterpret_cast<double2*>(align16(m.qsegf + a.nseg * kQPitchF));
-        m.thr2 = reinterpret_cast<double*>(m.gband + m.nt1);
-        m.pend_d2 = m.thr2 + 2 * m.nt1;
-        return m;
-    };
-
-    const int warp = threadIdx.x >> 5;
-    const unsigned lane = lane_id();
-    float* wbuf = wbuf_all + warp * 1024;
-    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) {
-        const Seg sg = a.segs[i];
-        segs[i] = sg;
-        if (sg.test >= 0) mixed_smem().gband[sg.test] = f32_band(sg.col + sg.len);
-    }
-    for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) tfac[i] = a.tfac[i];
-    // VEC=4 line descriptor = pos * stride + column offset, 16-byte units from a.a1
-    const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
-    const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
-    const char* gbase = lane_base16(a.a1);
-    // stream index -> flat position (last probed list with pre[l] <= i)
-    const int nl = a.nprobe - a.probe_lo;  // lists scanned per query
-    auto locate = [&](int i) {
-        int l = 0, h = nl - 1;
-        while (l < h) {
-            const int mid = (l + h + 1) >> 1;
-            if (pre[mid] <= i) l = mid;
-            else h = mid - 1;
-        }
-        return lstart[l] + (i - pre[l]);
-    };
-    int nseg0 = -1;  // leading segments no threshold test depends on (set after the first barrier)
-
-    for (;;) {
-        __syncthreads();
-        if (nseg0 < 0) {
-            // The split layouts' A1 prefix (and FD's whole walk but the last
-            // segment) is tested against nothing (ivf.cpp:366-386): lanes left
-            // idle at a chunk's tail precompute it for the next chunk.
-            nseg0 = 0;
-            while (nseg0 < a.nseg - 1 && segs[nseg0].test < 0) ++nseg0;
-        }
-        if (threadIdx.x == 0) {
-            const int w = static_cast<int>(atomicAdd(a.counter, 1ull));
-            sh.stop = w >= a.nq;
-            sh.q = sh.stop ? w : (a.order ? a.order[w] : w);
-            sh.cnt = 0;
-            // the radius starts at the caller's bound (the sharded search's second
-            // wave) or +inf; thresholds follow it until the heap is full
-            const double r0 = (!sh.stop && a.r0) ? a.r0[sh.q] : kInf;
-            sh.r = r0;
-            sh.r_sq = __dmul_rn(r0, r0);
-            sh.dims = 0;
-        }
-        __syncthreads();
-        if (sh.stop) break;
-        const int qi = sh.q;
-        stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
-        {
-            const MixedSmem mm = mixed_smem();
-            stage_query_f32(mm.qsegf, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
-            for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) mm.thr2[i] = __dmul_rn(tfac[i], sh.r_sq);
-        }
-        if (warp == 0) {  // probed lists -> stream prefix offsets
-            int carry = 0;
-            for (int base = 0; base < nl; base += 32) {  // probe ranks probe_lo .. nprobe-1
-                const int i = base + static_cast<int>(lane);
-                int len = 0;
-                if (i < nl) {
-                    const int p = a.probes[static_cast<int64_t>(qi) * a.nprobe + a.probe_lo + i];
-                    const int64_t s0 = a.list_off[p];
-                    lstart[i] = static_cast<int32_t>(s0);
-                    len = static_cast<int>(a.list_off[p + 1] - s0);
-                }
-                int incl = len;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(kFull, incl, o);
-                    if (static_cast<int>(lane) >= o) incl += v;
-                }
-                if (i < nl) pre[i + 1] = carry + incl;
-                carry += __shfl_sync(kFull, incl, 31);
-            }
-            if (lane == 0) {
-                pre[0] = 0;
-                sh.total = carry;
-            }
-        }
-        __syncthreads();
-        const int total = sh.total;
-        unsigned long long my_dims = 0;
-
-        if (threadIdx.x == 0) sh.pcount[0] = 0;
-#include "ivf_mixed_loop.inc"
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) my_dims += __shfl_xor_sync(kFull, my_dims, o);
-        if (lane == 0) atomicAdd(&sh.dims, my_dims);
-        __syncthreads();
-        const int cnt = sh.cnt;
-        for (int i = threadIdx.x; i < a.K; i += blockDim.x) {
-            const int64_t o = static_cast<int64_t>(qi) * a.K + i;
-            a.out_ids[o] = i < cnt ? topi[i] : -1;
-            a.out_dists[o] = i < cnt ? topd[i] : __longlong_as_double(0x7ff8000000000000ll);
-        }
-        if (threadIdx.x == 0) {
-            a.out_cnt[qi] = cnt;
-            a.out_dims[qi] = sh.dims;
-            if (a.out_cand) a.out_cand[qi] = static_cast<unsigned long long>(total);
-        }
-    }
-}
-
 size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
     size_t b = sizeof(float) * a.warps * 1024;
@@ -900,14 +716,6 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + a.nprobe + 1);
     b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
-    if (a.f32) {  // MIXED extras, laid out as in ivf_search_mixed_kernel
-        const size_t W = (chunk_cap + 31) / 32;
-        b += sizeof(unsigned) * 5 * W + sizeof(int) * 32 + sizeof(int32_t) * 3 * chunk_cap;
-        b = (b + 15) & ~static_cast<size_t>(15);
-        b += sizeof(float) * a.nseg * kQPitchF;
-        b = (b + 15) & ~static_cast<size_t>(15);
-        b += 16 * nt + sizeof(double) * (2 * nt + 2 * chunk_cap);
-    }
     return b;
 }
 
@@ -1009,10 +817,8 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     SearchShape sh{};
     sh.cap = static_cast<int>(cap64);
     sh.smem = search_smem(a, sh.cap);
-    const bool mixed = a.f32 && a.vec == 4 && a.full && a.warps == 4;  // 128-thread launch bounds
-    sh.kern = mixed ? ivf_search_mixed_kernel
-                    : a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
-                                 : ivf_search_kernel<1, false>;
+    sh.kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
+                         : ivf_search_kernel<1, false>;
     ADS_CUDA(cudaFuncSetAttribute(sh.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sh.smem)));
     ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sh.occ, sh.kern, a.warps * 32, sh.smem));

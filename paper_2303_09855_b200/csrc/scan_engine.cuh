@@ -132,38 +132,6 @@ __device__ __forceinline__ double accumulate_line(const float* wbuf, const doubl
     return s;
 }
 
-// Certified fp32 walk (ivf.cu MIXED): the same line, fp32 difference and fused
-// square-add.  |s32 - s_fp64| stays within a relative bound the caller widens
-// its tests by; whatever the band cannot decide is walked again in fp64.
-__device__ __forceinline__ float accumulate_line_f32(const float* wbuf, const float* qq, float s) {
-    const unsigned lane = lane_id();
-    const float* row = wbuf + lane * 32;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        const float4 v = *reinterpret_cast<const float4*>(row + (((c + static_cast<int>(lane)) & 7) << 2));
-        const float4 q = *reinterpret_cast<const float4*>(qq + c * 4);
-        float d = __fsub_rn(v.x, q.x);
-        s = __fmaf_rn(d, d, s);
-        d = __fsub_rn(v.y, q.y);
-        s = __fmaf_rn(d, d, s);
-        d = __fsub_rn(v.z, q.z);
-        s = __fmaf_rn(d, d, s);
-        d = __fsub_rn(v.w, q.w);
-        s = __fmaf_rn(d, d, s);
-    }
-    return s;
-}
-
-constexpr int kQPitchF = 36;  // floats per segment slot of the fp32-staged query
-
-__device__ __forceinline__ void stage_query_f32(float* qseg, const Seg* segs, int nseg, const float* q) {
-    for (int i = threadIdx.x; i < nseg * 32; i += blockDim.x) {
-        const int s = i >> 5, k = i & 31;
-        const Seg sg = segs[s];
-        if (k < sg.len) qseg[s * kQPitchF + k] = q[sg.col + k];
-    }
-}
-
 // Stage query coordinates per segment: qseg[s*34 + k] = (double)q[seg.col + k].
 __device__ __forceinline__ void stage_query(double* qseg, const Seg* segs, int nseg,
                                             const float* q) {
