@@ -221,3 +221,26 @@ def test_oracle_rejects_layouts_missing_mode_arrays(orc):
     orc.ivf_query(lay, qt[0], qr[0], 5, 2, "ad-split", 2.1, 16)  # split arrays present
     with pytest.raises(ValueError):
         orc.ivf_query(lay, qt[0], qr[0], 5, 2, "fd")
+
+
+def test_oracle_lag_schedule(orc):
+    """orc_ivf_query_lag: with a single chunk the lag changes nothing; with short
+    chunks it still returns K exact (dist, id) pairs sorted ascending, each distance
+    the exact fp64 distance of its id, and it never scans fewer dims than lag 0
+    (a staler radius only rejects later)."""
+    from helpers import make_fixture, oracle_index
+
+    raw, t, qr, qt, P = make_fixture(orc, 2000, 64, 12, 6, 41)
+    lay = oracle_index(orc, raw, t, P, 20, 42, d1=32)
+    for qi in range(qt.shape[0]):
+        a = orc.ivf_query(lay, qt[qi], qr[qi], 10, 6, "ad-split", 2.1, 32, 10**9, 1)
+        b = orc.ivf_query(lay, qt[qi], qr[qi], 10, 6, "ad-split", 2.1, 32, 10**9, 1, lag=1)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+        assert int(a[2][0]) == int(b[2][0])
+        c0 = orc.ivf_query(lay, qt[qi], qr[qi], 10, 6, "ad-split", 2.1, 32, 10, 16)
+        c1 = orc.ivf_query(lay, qt[qi], qr[qi], 10, 6, "ad-split", 2.1, 32, 10, 16, lag=1)
+        assert len(c1[0]) == 10 and np.all(np.diff(c1[1]) >= 0)
+        exact = np.sqrt(((t[c1[0]].astype(np.float64) - qt[qi].astype(np.float64)) ** 2).sum(axis=1))
+        np.testing.assert_allclose(c1[1], exact, rtol=1e-12)
+        assert int(c1[2][0]) >= int(c0[2][0])
