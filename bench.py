@@ -348,7 +348,8 @@ def run_search(args, D: Dist):
     K, nq, d = cfg.K, cfg.nq, cfg.d
     mode = ads.IvfMode.kAdSplit
     opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps,
-                           queries_per_cta=args.slots, time_stages=True, query_order=args.query_order)
+                           queries_per_cta=args.slots, time_stages=True, query_order=args.query_order,
+                           ctas_per_sm=args.ctas_per_sm)
 
     # HBM-resident inputs / outputs
     dq = ads.DeviceArray.from_host(ctx, q)
@@ -784,6 +785,7 @@ def main():
     ap.add_argument("--step", type=int, default=0, help="threshold refresh interval (0: 64 x warps)")
     ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0: 4 for D <= 256, else 10)")
     ap.add_argument("--slots", type=int, default=4, help="queries served concurrently per CTA")
+    ap.add_argument("--ctas-per-sm", type=int, default=0, help="cap on resident search CTAs per SM (0: occupancy)")
     ap.add_argument("--query-order", type=int, default=2,
                     help="2: longest queries first (default), 1: L2-locality order, 0: input order")
     ap.add_argument("--same-query", action="store_true", help="experiment: all queries = query 0")
