@@ -2,26 +2,39 @@
 """bench.py — IVF++ ADSampling queries/sec at fixed recall@K on B200.
 
 Metric (BASELINE.json): "IVF++ ADSampling queries/sec at fixed recall@K;
-scanned GB/s vs HBM peak".  Workload: configs[1] (1M x 128, 4096 lists,
-10 000 queries, K=100) at the headline nprobe.  One step = one batch of all
-queries through the whole hot path on the GPU: query rotation (apply, fp64),
-coarse quantizer (fp64 centroid distances + top-nprobe), ADSampling scan
-with top-K (ivf_query, split layout).  Inputs are HBM-resident when the timed
-region starts (`value`); `e2e` repeats the step through the host API with
-pinned host buffers, H2D of the queries and D2H of the results inside.
+scanned GB/s vs HBM peak".  Default workload: configs[4] = config 5, the
+largest config (1e8 x 96 unit-sphere rows, 16 384 lists, 10 000 queries,
+K = 100, nprobe 64), which fits one B200:
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--nprobe 64]
+* N = 1: the whole index on one GPU; one step = all 10 000 queries through
+  query rotation (exact fp64) + coarse quantizer + the ADSampling scan with
+  top-K.  `value` has the queries resident in HBM; `e2e` repeats the step
+  through the host API (pinned host queries in, results out, copies inside the
+  timed region).  Config 3 (1M x 960) is measured the same way and reported
+  under "cfg3" on the same line.
+* N > 1: IVF lists partitioned over the N GPUs (LPT on list sizes), every
+  rank answers the same fixed 10 000-query batch over its own lists (strong
+  scaling) with the two-wave threshold exchange and the NCCL all-gather +
+  merge of shard.ShardedIvf.  `python bench.py --gpus N` spawns the N ranks
+  itself (torch.distributed.run) when WORLD_SIZE is unset.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--nprobe 64]
     python bench.py --impl reference ...   # the reference's CPU ivf_query (oracle/_ref)
     python bench.py --mode dco ...         # config-4 fixed-threshold DCO microbench
 
-N > 1 (torchrun): query-sharded replicas (weak scaling): every rank holds the
-index and answers its own 10 000-query batch; no data-path collective.
+The reference arm never loads libadsann_b200.so: it generates config 5 with
+the oracle's restated generator, rotates it with the reference's own
+apply_dataset, assembles the reference IvfIndex around the committed
+centroids (tests/golden/cfg5_centroids.npy, reproduced bit-for-bit by the GPU
+arm's k-means) and times adsann::ivf_query on all host threads.
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -31,52 +44,57 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+CFG5_CENTROIDS = os.path.join(ROOT, "tests", "golden", "cfg5_centroids.npy")
+METRIC = "IVF++ ADSampling queries/sec at fixed recall@K"
 
 
 # ---------------------------------------------------------------- distributed plumbing
 class Dist:
-    def __init__(self, backend="gloo", force=False):
+    """One process per GPU: gloo for the control plane (barriers, max over ranks),
+    an NCCL group for the data path of the list-sharded search."""
+
+    def __init__(self, backend="gloo", force=False, expect=None):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
         self.nccl = None
-        if self.world > 1 or force or os.environ.get("ADS_FORCE_DIST") == "1":
-            # a one-rank group needs the rendezvous variables torchrun would set
+        if expect is not None and self.world != expect:
+            raise SystemExit(f"bench.py: --gpus {expect} but WORLD_SIZE={self.world}")
+        if self.world > 1 or force:
             for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"),
                          ("WORLD_SIZE", "1")):
                 os.environ.setdefault(k, v)
             import torch
             import torch.distributed as dist
 
-            # control plane (barriers, max-over-ranks) on gloo; data path on NCCL
             dist.init_process_group("gloo")
             self.pg = dist
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
                 self.nccl = dist.new_group(backend="nccl")
+                n = dist.get_world_size(self.nccl)
+                if n != self.world:
+                    raise SystemExit(f"bench.py: NCCL communicator holds {n} ranks, expected {self.world}")
 
     def barrier(self):
         if self.pg:
             self.pg.barrier()
 
-    def allmax(self, v: float) -> float:
+    def _reduce(self, v: float, op) -> float:
         if not self.pg:
             return v
         import torch
 
         t = torch.tensor([v], dtype=torch.float64)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        self.pg.all_reduce(t, op=op)
         return float(t.item())
+
+    def allmax(self, v: float) -> float:
+        return self._reduce(v, self.pg.ReduceOp.MAX) if self.pg else v
 
     def allsum(self, v: float) -> float:
-        if not self.pg:
-            return v
-        import torch
-
-        t = torch.tensor([v], dtype=torch.float64)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
-        return float(t.item())
+        return self._reduce(v, self.pg.ReduceOp.SUM) if self.pg else v
 
     def close(self):
         if self.pg:
@@ -155,14 +173,25 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-# ---------------------------------------------------------------- workload setup
-def config_for(args):
+def load_configs():
+    """paper_2303_09855_b200/configs.py loaded by path (no package import, so the
+    reference arm does not map libadsann_b200.so)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "ads_bench_configs", os.path.join(ROOT, "paper_2303_09855_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["ads_bench_configs"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def config_for(args, configs=None):
     """BASELINE config args.config, with --cfg-override applied (calibration runs only)."""
     import copy
     import dataclasses
 
-    from paper_2303_09855_b200 import configs
-
+    configs = configs or load_configs()
     cfg = copy.deepcopy(configs.CONFIGS[args.config])
     for kv in filter(None, getattr(args, "cfg_override", "").split(",")):
         k, v = kv.split("=")
@@ -172,85 +201,92 @@ def config_for(args):
         else:
             cfg.extra[k] = int(float(v))
         cfg.key += f"-{k}{v}"
+    if getattr(args, "nq", 0):
+        cfg.nq = args.nq
+    if getattr(args, "kmeans_iters", 0):
+        cfg.kmeans_iters = args.kmeans_iters
+    if getattr(args, "kmeans_init", -1) >= 0:
+        cfg.kmeans_init = args.kmeans_init
     return cfg
 
 
-def large_rotated_dataset(cfg, m, ctx):
-    """Config 5's 1e8 rows, generated on the host, rotated on the device (exact fp64);
-    the host copy and the unrotated device copy are released."""
-    import paper_2303_09855_b200 as ads
-    from paper_2303_09855_b200 import api
-
-    kw = dict(kind=cfg.kind, center_scale=cfg.center_scale, center_lo=cfg.center_lo,
-              center_hi=cfg.center_hi, sigma=cfg.sigma, decay=cfg.decay, assign_mode=cfg.assign_mode)
-    base = api.synth(cfg.n, cfg.d, cfg.components, cfg.seed, 1, **kw)
-    dX = ads.DeviceArray.from_host(ctx, base)
-    del base
-    dT = ads.DeviceArray(ctx, (cfg.n, cfg.d), np.float32)
-    ads.Transform(m, ctx).apply_dataset_device(dX, dT)
-    ctx.sync()
-    dX.free()
-    return dT
+def workload_config(cfg, nprobe) -> dict:
+    """The line's `config`: what defines the workload, identical in both arms."""
+    return dict(cfg.describe(), nprobe=nprobe, queries_per_step=cfg.nq,
+                l2=f"flushed between timed steps; index {cfg.n * cfg.d * 4 / 1e9:.2f} GB vs 126 MB L2")
 
 
-def device_ground_truth(ads, ctx, dT, qt, K):
-    """Exact top-K of the rotated queries qt over the device-resident rotated rows dT
-    (P is orthogonal, so this is the raw-space neighbour set up to rounding)."""
+def is_large(cfg) -> bool:
+    return cfg.n > 20_000_000
+
+
+def recall_of(ids, gt, K) -> float:
+    ngt = min(len(ids), len(gt))
+    return float(np.mean([len(np.intersect1d(ids[i][ids[i] >= 0], gt[i])) for i in range(ngt)]) / K)
+
+
+# ---------------------------------------------------------------- workload setup (GPU arm)
+def setup(cfg, D, log, world=1, rank=0):
+    """Index (this rank's shard when world > 1), queries (the same on every rank), ground
+    truth (rank 0; first gt_queries queries for config 5).  Returns a dict."""
     import ctypes as C
 
+    import paper_2303_09855_b200 as ads
     from paper_2303_09855_b200 import _lib as L
-
-    dq = ads.DeviceArray.from_host(ctx, np.ascontiguousarray(qt, np.float32))
-    dg = ads.DeviceArray(ctx, (qt.shape[0], K), np.int32)
-    L.check(L.ads_brute_force_knn_device(ctx.h, C.c_void_p(dT.ptr), dT.shape[0], dT.shape[1],
-                                         C.c_void_p(dq.ptr), qt.shape[0], K, C.c_void_p(dg.ptr)))
-    return dg.to_host()
-
-
-def setup_large(cfg, dev, rank, log):
-    """Config 5 (1e8 rows): generate on the host, rotate and build on the device
-    (ads_ivf_build_sampled_device), ground truth for the first gt_queries queries
-    in the rotated space (P is orthogonal); the host copies are released."""
-    import paper_2303_09855_b200 as ads
     from paper_2303_09855_b200 import configs
+    from paper_2303_09855_b200.shard import partition_lists, shard_index
 
     t0 = time.time()
-    q = configs.generate_queries(cfg, role_base=rank)
+    ctx = ads.Context.default(D.local)
     m = ads.generate_orthogonal(cfg.d, cfg.seed)
-    ctx = ads.Context.default(dev)
-    dT = large_rotated_dataset(cfg, m, ctx)
-    t1 = time.time()
-    idx = ads.build_ivf_sampled_device(dT, m, cfg.nlist, cfg.seed, 32, cfg.kmeans_iters,
-                                       cfg.extra.get("sample", 2_000_000), ctx=ctx)
-    t2 = time.time()
-    ng = min(cfg.extra.get("gt_queries", 100), q.shape[0])
-    gt = device_ground_truth(ads, ctx, dT, ads.Transform(m, ctx).apply_dataset(q[:ng]), cfg.K)
-    dT.free()
-    t3 = time.time()
-    log(f"setup: data+rotate {t1 - t0:.1f}s, build_ivf (sampled k-means + certified assignment) "
-        f"{t2 - t1:.1f}s, ground truth ({ng} queries) {t3 - t2:.1f}s")
-    return ads, ctx, None, None, q, m, idx, gt
+    q = configs.generate_queries(cfg)
+    owner = (lambda sizes: partition_lists(sizes, world)) if world > 1 else None
+    out = {"ads": ads, "ctx": ctx, "m": m, "q": q, "base": None, "t": None, "gt": None, "info": {}}
+    if is_large(cfg):
+        ng = min(cfg.extra.get("gt_queries", 100), cfg.nq)
+        gt_box = {}
 
+        def on_rows(ptr):  # exact top-K in the rotated space over every row (P is orthogonal)
+            if rank != 0:
+                return
+            qt = ads.Transform(m, ctx).apply_dataset(q[:ng])
+            dq = ads.DeviceArray.from_host(ctx, qt)
+            dg = ads.DeviceArray(ctx, (ng, cfg.K), np.int32)
+            L.check(L.ads_brute_force_knn_device(ctx.h, C.c_void_p(ptr), cfg.n, cfg.d, C.c_void_p(dq.ptr),
+                                                 ng, cfg.K, C.c_void_p(dg.ptr)))
+            gt_box["gt"] = dg.to_host()
 
-def setup(cfg, dev, rank, log):
-    import paper_2303_09855_b200 as ads
-    from paper_2303_09855_b200 import configs
-
-    if cfg.n > 20_000_000:
-        return setup_large(cfg, dev, rank, log)
-    t0 = time.time()
-    base, q = configs.generate(cfg, role_base=rank)
-    m = ads.generate_orthogonal(cfg.d, cfg.seed)
-    ctx = ads.Context.default(dev)
-    t = ads.Transform(m, ctx).apply_dataset(base)
-    t1 = time.time()
-    idx = ads.build_ivf(base, t, m, cfg.nlist, cfg.seed, ads.IvfLayout.kSplit, 32,
-                        max_iters=cfg.kmeans_iters, init=cfg.kmeans_init, ctx=ctx)
-    t2 = time.time()
-    gt = ads.brute_force_knn(base, q, cfg.K, ctx=ctx)
-    t3 = time.time()
-    log(f"setup: data+rotate {t1 - t0:.1f}s, build_ivf {t2 - t1:.1f}s, ground truth {t3 - t2:.1f}s")
-    return ads, ctx, base, t, q, m, idx, gt
+        idx, sizes, cent = ads.build_ivf_streamed(
+            configs.row_source(cfg), cfg.n, cfg.d, m, cfg.nlist, cfg.seed, 32, cfg.kmeans_iters,
+            cfg.extra.get("sample", 2_000_000), chunk=4_000_000, owner=owner, rank=rank,
+            on_rows=on_rows, ctx=ctx)
+        out["gt"] = gt_box.get("gt")
+        if cfg.key == configs.CONFIGS[5].key and os.path.exists(CFG5_CENTROIDS):
+            out["info"]["centroids_match_fixture"] = bool(np.array_equal(cent, np.load(CFG5_CENTROIDS)))
+        out["info"]["list_rows_max_min"] = [int(sizes.max()), int(sizes.min())]
+        if world > 1:
+            loads = np.bincount(partition_lists(sizes, world), weights=sizes, minlength=world)
+            out["info"]["shard_rows_max_min"] = [int(loads.max()), int(loads.min())]
+        log(f"setup: generate + rotate + build_ivf (sampled k-means, certified assignment) "
+            f"{time.time() - t0:.1f}s; ground truth on {ng} queries")
+    else:
+        base, _ = configs.generate(cfg, nq=1)
+        t = ads.Transform(m, ctx).apply_dataset(base)
+        full = ads.build_ivf(base, t, m, cfg.nlist, cfg.seed, ads.IvfLayout.kSplit, 32,
+                             max_iters=cfg.kmeans_iters, init=cfg.kmeans_init, ctx=ctx)
+        t1 = time.time()
+        if rank == 0:
+            out["gt"] = ads.brute_force_knn(base, q, cfg.K, ctx=ctx)
+        if world > 1:
+            sizes = np.diff(full.list_offsets())
+            idx = shard_index(full, partition_lists(sizes, world), rank)
+            del full
+        else:
+            idx = full
+        out["base"], out["t"] = base, t
+        log(f"setup: data + rotate + build_ivf {t1 - t0:.1f}s, ground truth {time.time() - t1:.1f}s")
+    out["idx"] = idx
+    return out
 
 
 def order_sorted(args, nq: int, d: int) -> bool:
@@ -265,137 +301,42 @@ def order_sorted(args, nq: int, d: int) -> bool:
     return args.query_order == 2 and nq > sms * (9 if d <= 256 else 3)
 
 
-def cpu_baseline_reference(cfg, base, t, m, idx, q, gt, nprobe, budget_s=12.0, log=print):
-    """The reference's ivf_query (oracle/_ref, or the oracle port) on the same index,
-    run_timed protocol (rotation inside the loop), all host threads, bounded sample."""
-    from paper_2303_09855_b200 import configs
-
-    ex = idx.export()
-    asg = configs.list_assignment(ex["list_off"], ex["ids_flat"])
-    cores = os.cpu_count() or 1
-    from oracle import load_oracle, load_ref, ref_available
-
-    if ref_available():
-        ref = load_ref()
-        h = ref.assemble_ivf(base, t, m.entries, ex["centroids_t"], asg, seed=cfg.seed, split=True, d1=32)
-        kind = "reference"
-
-        def run(mode, qs, nthreads):
-            ids, dists, dims, secs = h.query_batch(None, qs, cfg.K, nprobe, mode, 2.1, 32,
-                                                   nthreads=nthreads, P=m.entries)
-            return ids, dims, secs
-    else:  # oracle port, single thread per query loop
-        orc = load_oracle()
-        lay = orc.ivf_layout(base, t, m.entries, ex["centroids_t"], asg, cfg.nlist, 32, True)
-        kind, cores = "port", 1
-
-        def run(mode, qs, nthreads):
-            qt = orc.apply_dataset(m.entries, qs)
-            t0 = time.perf_counter()
-            ids = np.full((len(qs), cfg.K), -1, np.int32)
-            dims = np.zeros(len(qs), np.uint64)
-            for i in range(len(qs)):
-                a, _, s = orc.ivf_query(lay, qt[i], qs[i], cfg.K, nprobe, mode)
-                ids[i, :len(a)] = a
-                dims[i] = s[0]
-            return ids, dims, time.perf_counter() - t0
-
-    # size the sample to ~budget_s of CPU work
-    probe = min(64, len(q))
-    _, _, s = run("ad-split", q[:probe], cores)
-    per_q = s / probe
-    ns = int(max(probe, min(len(q), budget_s / max(per_q, 1e-9))))
-    ids, dims, secs = run("ad-split", q[:ns], cores)
-    rec = float(np.mean([len(np.intersect1d(ids[i], gt[i])) for i in range(ns)]) / cfg.K)
-    fd_ns = min(ns, max(probe, ns // 3))
-    _, _, fd_secs = run("fd", q[:fd_ns], cores)
-    # IVF+ (kAd: the contiguous transformed rows) and the reference's own single-thread
-    # run_timed protocol (bench.cpp:125-182), on smaller samples of the same queries
-    _, _, ad_secs = run("ad", q[:fd_ns], cores)
-    st_ns = max(8, min(ns, int(budget_s / 4 / max(per_q * cores, 1e-9))))
-    _, _, st_secs = run("ad-split", q[:st_ns], 1)
-    log(f"cpu baseline ({kind}): {ns} queries IVF++ {ns / secs:.0f} QPS, FD {fd_ns / fd_secs:.0f} QPS, "
-        f"IVF+ {fd_ns / ad_secs:.0f} QPS ({cores} threads); IVF++ single thread {st_ns / st_secs:.0f} QPS")
-    return {"value": ns / secs, "unit": "queries/s", "cores": cores, "kind": kind,
-            "sample": f"first {ns} of {len(q)} queries, ivf_query kAdSplit, rotation inside the loop "
-                      f"(run_timed protocol), {cores} host threads over queries, same index",
-            "recall_at_k": rec, "fd_value": fd_ns / fd_secs,
-            "fd_sample": f"first {fd_ns} queries, ivf_query kFd",
-            "ivf_plus_value": fd_ns / ad_secs, "ivf_plus_sample": f"first {fd_ns} queries, ivf_query kAd",
-            "single_thread_value": st_ns / st_secs,
-            "single_thread_sample": f"first {st_ns} queries, ivf_query kAdSplit, 1 thread"}, ids, ns
-
-
-# ---------------------------------------------------------------- search bench
-def run_search(args, D: Dist):
-    import paper_2303_09855_b200 as ads  # noqa: F401
-    from paper_2303_09855_b200 import configs
-
-    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
-    cfg = config_for(args)
-    if args.nq:
-        cfg.nq = args.nq
-    if args.kmeans_init >= 0:
-        cfg.kmeans_init = args.kmeans_init
-    if args.kmeans_iters:
-        cfg.kmeans_iters = args.kmeans_iters
-    nprobe = args.nprobe or cfg.nprobe
-    dev = D.local
-    ads, ctx, base, t, q, m, idx, gt = setup(cfg, dev, D.rank, log)
-    if args.same_query:  # locality experiment: every query = query 0 (perfect L2 reuse)
-        q = np.ascontiguousarray(np.repeat(q[:1], q.shape[0], axis=0))
-        gt = np.repeat(gt[:1], gt.shape[0], axis=0)
-    K, nq, d = cfg.K, cfg.nq, cfg.d
-    mode = ads.IvfMode.kAdSplit
-    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps,
-                           queries_per_cta=args.slots, time_stages=True, query_order=args.query_order,
-                           ctas_per_sm=args.ctas_per_sm)
-
-    # HBM-resident inputs / outputs
-    dq = ads.DeviceArray.from_host(ctx, q)
-    d_ids = ads.DeviceArray(ctx, (nq, K), np.int32)
-    d_dst = ads.DeviceArray(ctx, (nq, K), np.float64)
-    d_cnt = ads.DeviceArray(ctx, (nq,), np.int32)
-    d_dims = ads.DeviceArray(ctx, (nq,), np.uint64)
-    d_cand = ads.DeviceArray(ctx, (nq,), np.uint64)
+# ---------------------------------------------------------------- one-GPU measurement
+def measure(S, cfg, nprobe, args, D, log, steps):
+    """Device-resident steps (value, roofline, stages) and host-API steps (e2e) of one index."""
     import ctypes as C
 
     from paper_2303_09855_b200 import _lib as L
 
-    def step():
-        L.check(L.ads_ivf_search_device(idx.h, None, C.c_void_p(dq.ptr), nq, K, nprobe, int(mode),
-                                        2.1, 32, C.byref(opts), C.c_void_p(d_ids.ptr),
-                                        C.c_void_p(d_dst.ptr), C.c_void_p(d_cnt.ptr),
-                                        C.c_void_p(d_dims.ptr), C.c_void_p(d_cand.ptr)))
+    ads, ctx, idx, q, gt = S["ads"], S["ctx"], S["idx"], S["q"], S["gt"]
+    K, nq, d = cfg.K, cfg.nq, cfg.d
+    mode = ads.IvfMode.kAdSplit
+    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True,
+                           query_order=args.query_order, ctas_per_sm=args.ctas_per_sm)
+    dq = ads.DeviceArray.from_host(ctx, q)
+    outs = {nm: ads.DeviceArray(ctx, shape, dt) for nm, shape, dt in (
+        ("ids", (nq, K), np.int32), ("dists", (nq, K), np.float64), ("cnt", (nq,), np.int32),
+        ("dims", (nq,), np.uint64), ("cand", (nq,), np.uint64))}
+    P = lambda a: C.c_void_p(a.ptr)  # noqa: E731
 
-    if args.tune and D.rank == 0:
-        grid = [(256, 4), (384, 6), (512, 8), (192, 3), (128, 2), (320, 5), (640, 10)]
-        if args.tune_grid:
-            grid = [tuple(int(v) for v in t.split("x")) for t in args.tune_grid.split(",")]
-        for st_, w_ in grid:
-            o2 = ads.search_opts(first=0, step=st_, warps_per_cta=w_, time_stages=True)
-            ts, dm = [], 0
-            for rep in range(4):
-                ctx.flush_l2()
-                r_ = ads.ivf_query_batch(idx, None, q, K, nprobe, mode, opts=o2)
-                ts.append(float(idx.last_timings()[3]))
-                dm = float(r_.dims.mean())
-            scan = float(np.min(ts))
-            log(f"tune step={st_} warps={w_}: scan {scan:.2f} ms, dims/query {dm:.0f}, "
-                f"recall {ads.recall_batch(r_.ids[:len(gt)], gt, K):.5f}")
+    def step():
+        L.check(L.ads_ivf_search_device(idx.h, None, P(dq), nq, K, nprobe, int(mode), 2.1, 32, C.byref(opts),
+                                        P(outs["ids"]), P(outs["dists"]), P(outs["cnt"]), P(outs["dims"]),
+                                        P(outs["cand"])))
+
     for _ in range(args.warmup):
         ctx.flush_l2()
         step()
     ctx.sync()
     cst = idx.coarse_stats()
-    log(f"coarse prefilter: {cst['rescored'] / max(1, cst['queries']):.1f} centroids rescored per query "
-        f"(nprobe {nprobe}), {cst['fallbacks']} exhaustive fallbacks")
-    clocks = ClockSampler(dev)
+    log(f"{cfg.key}: coarse prefilter rescored {cst['rescored'] / max(1, cst['queries']):.1f} centroids "
+        f"per query (nprobe {nprobe}), {cst['fallbacks']} exhaustive fallbacks")
+    clocks = ClockSampler(D.local)
     step_ms, scan_ms, stage_ms = [], [], []
     D.barrier()
     ctx.sync()
     clocks.start()
-    for _ in range(args.steps):
+    for _ in range(steps):
         ctx.flush_l2()  # L2 flushed between timed steps (outside the events)
         ctx.timer_start()
         step()
@@ -407,255 +348,273 @@ def run_search(args, D: Dist):
     clk = clocks.stop()
     D.barrier()
     total_ms = D.allmax(float(np.sum(step_ms)))
-    dims = d_dims.to_host()
-    ids = d_ids.to_host()
-    ngt = min(nq, len(gt))
-    recall = float(np.mean([len(np.intersect1d(ids[i][ids[i] >= 0], gt[i])) for i in range(ngt)]) / K)
+    dims = outs["dims"].to_host()
+    ids = outs["ids"].to_host()
+    cand = outs["cand"].to_host()
     scanned = 4.0 * float(dims.sum())  # algorithmic bytes per step
 
-    # end to end through the host API with pinned buffers
+    # end to end through the host API (pinned host buffers; H2D of the raw queries and
+    # D2H of every result array inside the timed region)
     qh = ads.PinnedArray((nq, d), np.float32)
     qh.array[:] = q
-    out = {nm: ads.PinnedArray(shape, dt) for nm, shape, dt in (
+    ho = {nm: ads.PinnedArray(shape, dt) for nm, shape, dt in (
         ("ids", (nq, K), np.int32), ("dists", (nq, K), np.float64), ("cnt", (nq,), np.int32),
         ("dims", (nq,), np.uint64), ("cand", (nq,), np.uint64))}
 
     def e2e_step():
         L.check(L.ads_ivf_search(idx.h, None, C.c_void_p(qh.ptr), nq, K, nprobe, int(mode), 2.1, 32,
-                                 C.byref(opts), C.c_void_p(out["ids"].ptr), C.c_void_p(out["dists"].ptr),
-                                 C.c_void_p(out["cnt"].ptr), C.c_void_p(out["dims"].ptr),
-                                 C.c_void_p(out["cand"].ptr)))
+                                 C.byref(opts), *[C.c_void_p(ho[nm].ptr) for nm in
+                                                   ("ids", "dists", "cnt", "dims", "cand")]))
 
     for _ in range(max(1, args.warmup // 2)):
         e2e_step()
     e2e_s = []
     D.barrier()
-    for _ in range(args.steps):
+    for _ in range(steps):
         ctx.flush_l2()
         ctx.sync()
         t0 = time.perf_counter()
         e2e_step()
         e2e_s.append(time.perf_counter() - t0)
     e2e_total = D.allmax(float(np.sum(e2e_s)))
-    assert np.array_equal(out["ids"].array, ids), "e2e and device-resident results differ"
+    assert np.array_equal(ho["ids"].array, ids), "e2e and device-resident results differ"
+    for a in list(outs.values()) + [dq]:
+        a.free()
 
-    world_q = nq * D.world * args.steps
-    value = world_q / (total_ms / 1e3)
     peaks = measured_peaks()
     scan_avg = float(np.mean(scan_ms))
     achieved = scanned / (scan_avg / 1e3) / 1e9
     stage = np.mean(np.array(stage_ms), axis=0)
-    res = {
-        "metric": "IVF++ ADSampling queries/sec at fixed recall@K",
-        "value": value, "unit": "queries/s", "n_gpus": D.world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(cfg.describe(), nprobe=nprobe, recall_at_k=recall,
-                       parallelism=f"replicas{D.world}" if D.world > 1 else "single-gpu",
-                       l2=f"flushed between timed steps (and index {cfg.n * d * 4 / 1e6:.0f} MB vs 126 MB L2)",
-                       threshold_refresh={"first": K, "step": ads.search_shape(d, args.step, args.warps)[0]},
-                       warps_per_cta=ads.search_shape(d, args.step, args.warps)[1]),
-        "e2e": {"value": world_q / e2e_total, "unit": "queries/s",
-                "h2d_bytes_per_step": nq * d * 4,
+    world_q = nq * D.world * steps
+    return {
+        "value": world_q / (total_ms / 1e3), "ms_per_step": total_ms / steps,
+        "recall_at_k": recall_of(ids, gt, K) if gt is not None else None,
+        "recall_queries": min(nq, len(gt)) if gt is not None else 0,
+        "e2e": {"value": world_q / e2e_total, "unit": "queries/s", "h2d_bytes_per_step": nq * d * 4,
                 "d2h_bytes_per_step": nq * K * (4 + 8) + nq * (4 + 8 + 8)},
-        # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, scan, plus
-        # the longest-first order when the batch exceeds one wave of resident CTAs (key
-        # kernel + CUB radix sort: histogram, bin scan, three onesweep passes)
-        # (ncu launch list: profiles/r01g_launches.csv)
-        "gpu_launches": (11 if order_sorted(args, nq, d) else 5) * args.steps,
+        # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, scan, plus the
+        # longest-first order when the batch exceeds one wave of resident CTAs (key kernel +
+        # radix sort) (ncu launch lists: profiles/)
+        "gpu_launches": (11 if order_sorted(args, nq, d) else 5) * steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "frac_vs_nominal_8000": achieved / 8000.0,
                      "traffic": ncu_traffic(cfg.key),
                      "traffic_unit": "GB per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
-                     "kernel": "ivf_search_kernel<4>", "peak_source": peaks["source"] + ", copy (burst)",
+                     "kernel": "ivf_search_kernel", "peak_source": peaks["source"] + ", copy (burst)",
                      "algorithmic_bytes_per_launch": scanned,
                      "scanned_gbs_whole_step": scanned / (float(np.mean(step_ms)) / 1e3) / 1e9},
         "stages_ms": {"rotate": float(stage[0]), "coarse": float(stage[1]), "select": float(stage[2]),
                       "scan": float(stage[3])},
-        "dims_per_query": float(dims.mean()), "dims_fraction": float(dims.mean()) / (
-            float(d_cand.to_host().mean()) * d),
-        "clocks": clk,
+        "dims_per_query": float(dims.mean()),
+        "dims_fraction": float(dims.mean()) / (float(cand.mean()) * d),
+        "clocks": clk, "ids": ids,
+        "threshold_refresh": {"first": K, "step": ads.search_shape(d, args.step, args.warps)[0]},
+        "warps_per_cta": ads.search_shape(d, args.step, args.warps)[1],
     }
-    if ngt < nq:
-        res["config"]["recall_queries"] = ngt
-    if D.rank == 0 and not args.no_cpu_baseline:
-        if base is None:
-            res["cpu_baseline"] = {"unavailable": "the reference's in-memory IvfIndex of 1e8 x 96 (raw, "
-                                                  "transformed, A1/A2 copies) exceeds the host's 196 GB"}
-        else:
-            cb, _, _ = cpu_baseline_reference(cfg, base, t, m, idx, q, gt, nprobe, args.cpu_budget, log)
-            res["cpu_baseline"] = cb
-    if D.rank == 0 and args.mode == "search":
-        # the GPU's own FDScanning (kFd: full fp64 distances over the raw vectors) on the
-        # same index, queries and nprobe, next to the reference's CPU FD above
-        try:
-            fd_opts = ads.search_opts(time_stages=True)
-            ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kFd, opts=fd_opts)
-            fms, fscan = [], []
-            for _ in range(3):
-                ctx.flush_l2()
-                ctx.sync()
-                ctx.timer_start()
-                rf = ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kFd, opts=fd_opts)
-                fms.append(ctx.timer_stop())
-                fscan.append(float(idx.last_timings()[3]))
-            fd_dims = float(rf.dims.astype(np.float64).sum())
-            res["gpu_fd"] = {
-                "value": nq / (float(np.mean(fms)) / 1e3), "unit": "queries/s",
-                "recall_at_k": ads.recall_batch(rf.ids[:ngt], gt[:ngt], K),
-                "scan_ms": float(np.mean(fscan)),
-                "scan_gbs": 4.0 * fd_dims / (float(np.mean(fscan)) / 1e3) / 1e9,
-                "timing": "ivf_query_batch kFd through the host API (H2D queries, D2H results inside), "
-                          "3 runs after one warm-up, L2 flushed"}
-            log(f"GPU FDScanning: {res['gpu_fd']['value']:.0f} q/s, scan {res['gpu_fd']['scan_ms']:.2f} ms "
-                f"({res['gpu_fd']['scan_gbs']:.0f} GB/s), recall {res['gpu_fd']['recall_at_k']:.5f}")
-        except (RuntimeError, ValueError) as e:
-            res["gpu_fd"] = {"unavailable": str(e)[:200]}
-        try:  # IVF+ (kAd) on the GPU, same index
-            ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kAd, opts=fd_opts)
-            ams = []
-            for _ in range(3):
-                ctx.flush_l2()
-                ctx.sync()
-                ctx.timer_start()
-                ra = ads.ivf_query_batch(idx, None, q, K, nprobe, ads.IvfMode.kAd, opts=fd_opts)
-                ams.append(ctx.timer_stop())
-            res["gpu_ivf_plus"] = {"value": nq / (float(np.mean(ams)) / 1e3), "unit": "queries/s",
-                                   "recall_at_k": ads.recall_batch(ra.ids[:ngt], gt[:ngt], K),
-                                   "timing": "ivf_query_batch kAd, as gpu_fd"}
-        except (RuntimeError, ValueError) as e:
-            res["gpu_ivf_plus"] = {"unavailable": str(e)[:200]}
-    if args.sweep and D.rank == 0:
-        sw = []
-        for np_ in cfg.sweep:
-            r1 = ads.ivf_query_batch(idx, None, q, K, np_, mode, opts=opts)
-            rf = ads.ivf_query_batch(idx, None, q, K, np_, ads.IvfMode.kFd, opts=opts)
+
+
+def gpu_mode_line(S, cfg, nprobe, mode_name):
+    """The GPU's own IVF+ (kAd) or FDScanning (kFd) on the same index, through the host API."""
+    ads, ctx, idx, q, gt = S["ads"], S["ctx"], S["idx"], S["q"], S["gt"]
+    mode = {"fd": ads.IvfMode.kFd, "ad": ads.IvfMode.kAd}[mode_name]
+    try:
+        o = ads.search_opts(time_stages=True)
+        ads.ivf_query_batch(idx, None, q, cfg.K, nprobe, mode, opts=o)
+        ms, scan = [], []
+        for _ in range(3):
+            ctx.flush_l2()
             ctx.sync()
             ctx.timer_start()
-            step_np = ads.ivf_query_batch(idx, None, q, K, np_, mode, opts=opts)
-            ms = ctx.timer_stop()
-            sw.append({"nprobe": np_, "recall": ads.recall_batch(r1.ids[:len(gt)], gt, K),
-                       "fd_recall": ads.recall_batch(rf.ids[:len(gt)], gt, K),
-                       "dims_frac": float(r1.dims.sum()) / float(rf.dims.sum()),
-                       "e2e_qps": nq / (ms / 1e3)})
-            del step_np
-        res["sweep"] = sw
+            r = ads.ivf_query_batch(idx, None, q, cfg.K, nprobe, mode, opts=o)
+            ms.append(ctx.timer_stop())
+            scan.append(float(idx.last_timings()[3]))
+        out = {"value": cfg.nq / (float(np.mean(ms)) / 1e3), "unit": "queries/s",
+               "recall_at_k": recall_of(r.ids, gt, cfg.K) if gt is not None else None,
+               "scan_ms": float(np.mean(scan)),
+               "scan_gbs": 4.0 * float(r.dims.astype(np.float64).sum()) / (float(np.mean(scan)) / 1e3) / 1e9,
+               "timing": f"ivf_query_batch {mode.name} through the host API, 3 runs after one warm-up, "
+                         f"L2 flushed"}
+        return out
+    except (RuntimeError, ValueError) as e:
+        return {"unavailable": str(e)[:200]}
+
+
+def cpu_baseline(S, cfg, nprobe, budget_s, log):
+    """The reference's ivf_query (oracle/_ref) on the same index, run_timed protocol
+    (rotation inside the loop), all host threads, bounded sample of the queries."""
+    from oracle import ref_available
+
+    if not ref_available():
+        return {"unavailable": "oracle/_ref/libadsann_ref.so not built"}, None
+    from oracle import load_ref
+
+    ref = load_ref()
+    ads, idx, q, gt, m = S["ads"], S["idx"], S["q"], S["gt"], S["m"]
+    t0 = time.time()
+    ex = idx.export()
+    h = ref.from_split_layout(ex["centroids_t"], ex["list_off"], ex["ids_flat"], ex["a1_t"], ex["a2_t"],
+                              seed=cfg.seed)
+    del ex
+    gc.collect()
+    log(f"cpu baseline: reference IvfIndex (kAdSplit arrays) from the GPU index in {time.time() - t0:.1f}s")
+    cores = os.cpu_count() or 1
+
+    def run(mode, qs, nthreads):
+        ids, _, dims, secs = h.query_batch(None, qs, cfg.K, nprobe, mode, 2.1, 32, nthreads=nthreads,
+                                           P=m.entries)
+        return ids, dims, secs
+
+    probe = min(64, len(q))
+    _, _, s = run("ad-split", q[:probe], cores)
+    per_q = s / probe
+    ns = int(max(probe, min(len(q), budget_s / max(per_q, 1e-9))))
+    ids, dims, secs = run("ad-split", q[:ns], cores)
+    st_ns = max(4, min(ns, int(budget_s / 4 / max(per_q * cores, 1e-9))))
+    _, _, st_secs = run("ad-split", q[:st_ns], 1)
+    out = {"value": ns / secs, "unit": "queries/s", "cores": cores, "kind": "reference",
+           "sample": f"first {ns} of {len(q)} queries, adsann::ivf_query kAdSplit with adsann::apply "
+                     f"inside the loop (run_timed protocol), {cores} host threads over queries, the "
+                     f"same index (reference IvfIndex assembled from the GPU layout)",
+           "recall_at_k": recall_of(ids, gt, cfg.K) if gt is not None else None,
+           "single_thread_value": st_ns / st_secs,
+           "single_thread_sample": f"first {st_ns} queries, 1 thread"}
+    if S["base"] is not None:  # configs 1-3: the reference's FD and IVF+ on the full index too
+        ex = idx.export()
+        from paper_2303_09855_b200 import configs as _c
+
+        asg = _c.list_assignment(ex["list_off"], ex["ids_flat"])
+        hf = ref.assemble_ivf(S["base"], S["t"], m.entries, ex["centroids_t"], asg, seed=cfg.seed,
+                              split=True, d1=32)
+        fd_ns = min(ns, max(probe, ns // 3))
+        _, _, _, fs = hf.query_batch(None, q[:fd_ns], cfg.K, nprobe, "fd", nthreads=cores)
+        _, _, _, as_ = hf.query_batch(None, q[:fd_ns], cfg.K, nprobe, "ad", nthreads=cores, P=m.entries)
+        out.update(fd_value=fd_ns / fs, fd_sample=f"first {fd_ns} queries, ivf_query kFd",
+                   ivf_plus_value=fd_ns / as_, ivf_plus_sample=f"first {fd_ns} queries, ivf_query kAd")
+    log(f"cpu baseline (reference): {ns} queries IVF++ {ns / secs:.0f} QPS on {cores} threads; "
+        f"single thread {st_ns / st_secs:.0f} QPS")
+    return out, ids
+
+
+# ---------------------------------------------------------------- search bench (N = 1)
+def run_search(args, D):
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
+    cfg = config_for(args)
+    nprobe = args.nprobe or cfg.nprobe
+    S = setup(cfg, D, log)
+    M = measure(S, cfg, nprobe, args, D, log, args.steps)
+    res = {
+        "metric": METRIC, "value": M["value"], "unit": "queries/s", "n_gpus": D.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": M["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak" if D.world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Gaussian mixtures with BASELINE.json's shapes; DESIGN.md §6)",
+        "config": workload_config(cfg, nprobe),
+        "parallelism": f"replicas x{D.world} (query-sharded)" if D.world > 1 else "single GPU, whole index",
+        "recall_at_k": M["recall_at_k"], "recall_queries": M["recall_queries"],
+        "e2e": M["e2e"], "gpu_launches": M["gpu_launches"], "roofline": M["roofline"],
+        "stages_ms": M["stages_ms"], "dims_per_query": M["dims_per_query"],
+        "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
+        "threshold_refresh": M["threshold_refresh"], "warps_per_cta": M["warps_per_cta"],
+        "setup": S["info"],
+    }
+    if D.rank == 0 and args.mode == "search":
+        res["gpu_ivf_plus"] = gpu_mode_line(S, cfg, nprobe, "ad")
+        if S["base"] is not None:
+            res["gpu_fd"] = gpu_mode_line(S, cfg, nprobe, "fd")
+    if D.rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"], _ = cpu_baseline(S, cfg, nprobe, args.cpu_budget, log)
+    if args.sweep and D.rank == 0:
+        res["sweep"] = sweep(S, cfg, args)
+    del S, M
+    gc.collect()
+    if D.rank == 0 and D.world == 1 and args.config == 5 and not args.no_extra:
+        res["cfg3"] = extra_config(args, D, log, 3)
     return res
 
 
-# ---------------------------------------------------------------- list-sharded search (N > 1)
-def run_search_sharded(args, D: Dist):
-    """IVF lists partitioned over the N GPUs (LPT on list sizes); every rank scans
-    all queries over its own lists, the per-rank top-K go through one NCCL
-    all-gather per result array on the engine's stream and a merge kernel keeps
-    the K smallest (dist, id) pairs.  Weak scaling: the job answers N x nq
-    queries per step (each rank contributes its own nq-query batch)."""
-    import ctypes as C
+def extra_config(args, D, log, cid):
+    """Another config measured by the same protocol, reported on the same line."""
+    import copy
 
+    a = copy.copy(args)
+    a.config, a.nprobe, a.nq, a.kmeans_iters, a.kmeans_init, a.cfg_override = cid, 0, 0, 0, -1, ""
+    cfg = config_for(a)
+    S = setup(cfg, D, log)
+    M = measure(S, cfg, cfg.nprobe, a, D, log, max(3, args.steps // 2))
+    out = {"workload": cfg.key, "config": workload_config(cfg, cfg.nprobe), "value": M["value"],
+           "unit": "queries/s", "ms_per_step": M["ms_per_step"], "steps": max(3, args.steps // 2),
+           "recall_at_k": M["recall_at_k"], "e2e": M["e2e"], "roofline": M["roofline"],
+           "stages_ms": M["stages_ms"], "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
+           "gpu_fd": gpu_mode_line(S, cfg, cfg.nprobe, "fd")}
+    del S
+    gc.collect()
+    return out
+
+
+def sweep(S, cfg, args):
+    """nprobe sweep: GPU IVF++ (q/s through the host API, recall, dims vs FD) and the
+    reference's recall on the same index at every nprobe (first 200 queries)."""
+    ads, ctx, idx, q, gt, m = S["ads"], S["ctx"], S["idx"], S["q"], S["gt"], S["m"]
+    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps)
+    href = None
+    from oracle import ref_available
+
+    if ref_available() and S["base"] is not None:
+        from oracle import load_ref
+        from paper_2303_09855_b200 import configs as _c
+
+        ex = idx.export()
+        href = load_ref().assemble_ivf(S["base"], S["t"], m.entries, ex["centroids_t"],
+                                       _c.list_assignment(ex["list_off"], ex["ids_flat"]), seed=cfg.seed,
+                                       split=True, d1=32)
+    nref = min(200, len(q))
+    out = []
+    for np_ in cfg.sweep:
+        r1 = ads.ivf_query_batch(idx, None, q, cfg.K, np_, ads.IvfMode.kAdSplit, opts=opts)
+        row = {"nprobe": np_, "recall": recall_of(r1.ids, gt, cfg.K)}
+        if S["base"] is not None:
+            rf = ads.ivf_query_batch(idx, None, q, cfg.K, np_, ads.IvfMode.kFd, opts=opts)
+            row.update(fd_recall=recall_of(rf.ids, gt, cfg.K),
+                       dims_frac=float(r1.dims.sum()) / float(rf.dims.sum()))
+        ctx.sync()
+        ctx.timer_start()
+        ads.ivf_query_batch(idx, None, q, cfg.K, np_, ads.IvfMode.kAdSplit, opts=opts)
+        row["e2e_qps"] = cfg.nq / (ctx.timer_stop() / 1e3)
+        if href is not None:
+            ids, _, _, _ = href.query_batch(None, q[:nref], cfg.K, np_, "ad-split", nthreads=os.cpu_count(),
+                                            P=m.entries)
+            row["ref_recall_first"] = nref
+            row["ref_recall"] = recall_of(ids, gt[:nref], cfg.K)
+            row["gpu_recall_same_queries"] = recall_of(r1.ids[:nref], gt[:nref], cfg.K)
+            row["recall_delta"] = abs(row["ref_recall"] - row["gpu_recall_same_queries"])
+        out.append(row)
+    return out
+
+
+# ---------------------------------------------------------------- list-sharded search (N > 1)
+def run_sharded(args, D):
+    """IVF lists partitioned over the N GPUs; every rank answers the same fixed query batch
+    over its lists (strong scaling) through shard.ShardedIvf (two waves with the threshold
+    all-reduce, NCCL all-gather, merge kernel)."""
     import torch
 
-    import paper_2303_09855_b200 as ads
-    from paper_2303_09855_b200 import _lib as L
-    from paper_2303_09855_b200 import configs
-    from paper_2303_09855_b200.shard import merge_topk_device, partition_lists, shard_index
+    from paper_2303_09855_b200.shard import ShardedIvf
 
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if D.rank == 0 else (lambda *a: None)
     cfg = config_for(args)
-    if args.nq:
-        cfg.nq = args.nq
-    if args.kmeans_init >= 0:
-        cfg.kmeans_init = args.kmeans_init
-    if args.kmeans_iters:
-        cfg.kmeans_iters = args.kmeans_iters
     nprobe = args.nprobe or cfg.nprobe
-    W, K, d = D.world, cfg.K, cfg.d
+    W, K, d, nq = D.world, cfg.K, cfg.d, cfg.nq
     torch.cuda.set_device(D.local)
-    t0 = time.time()
-    qs = np.concatenate([configs.generate_queries(cfg, role_base=r, nq=cfg.nq) for r in range(W)])
-    nq = qs.shape[0]
-    m = ads.generate_orthogonal(d, cfg.seed)
-    ctx = ads.Context.default(D.local)
-    if cfg.n > 20_000_000:
-        # config 5: every rank builds the same index on its device (seeded, deterministic),
-        # keeps its own lists and drops the rest; ground truth for the first gt_queries
-        dT = large_rotated_dataset(cfg, m, ctx)
-        full = ads.build_ivf_sampled_device(dT, m, cfg.nlist, cfg.seed, 32, cfg.kmeans_iters,
-                                            cfg.extra.get("sample", 2_000_000), ctx=ctx)
-        sizes = np.diff(full.list_offsets())
-        owner = partition_lists(sizes, W)
-        local = shard_index(full, owner, D.rank)
-        del full
-        gt = None
-        if D.rank == 0:
-            ng = min(cfg.extra.get("gt_queries", 100), nq)
-            gt = device_ground_truth(ads, ctx, dT, ads.Transform(m, ctx).apply_dataset(qs[:ng]), K)
-        dT.free()
-    else:
-        base, _ = configs.generate(cfg, nq=1)
-        t = ads.Transform(m, ctx).apply_dataset(base)
-        full = ads.build_ivf(base, t, m, cfg.nlist, cfg.seed, ads.IvfLayout.kSplit, 32,
-                             max_iters=cfg.kmeans_iters, init=cfg.kmeans_init, ctx=ctx)
-        sizes = np.diff(full.list_offsets())
-        owner = partition_lists(sizes, W)
-        local = shard_index(full, owner, D.rank)
-        del full
-        gt = ads.brute_force_knn(base, qs, K, ctx=ctx) if D.rank == 0 else None
-    log(f"sharded setup {time.time() - t0:.1f}s: {W} ranks, local rows {local.n} "
-        f"(max/min shard rows {np.bincount(owner, weights=sizes).max():.0f}/"
-        f"{np.bincount(owner, weights=sizes).min():.0f})")
-
+    S = setup(cfg, D, log, world=W, rank=D.rank)
+    ads, ctx, idx, q, gt = S["ads"], S["ctx"], S["idx"], S["q"], S["gt"]
+    Sh = ShardedIvf.on_device(idx, nq, K, nprobe, W, D.rank, D.nccl, waves=args.waves, step=args.step,
+                              warps=args.warps, P=S["m"].entries)
     dev = torch.device("cuda", D.local)
-    stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
-    dq = torch.from_numpy(qs).to(dev)
-    # two waves with the threshold exchange of SURVEY §8e (--waves 0 disables it): probe ranks
-    # [0, w) on every rank, an all-reduce (min) of the per-query K-th distances (an upper bound on
-    # the global K-th distance), then ranks [w, nprobe) starting from that bound; the merge keeps
-    # the K smallest (dist, id) pairs of the 2 x N local results
-    w = args.waves if args.waves >= 0 else (max(1, nprobe // 8) if W > 1 else 0)
-    w = w if 0 < w < nprobe else 0
-    G = 2 * W if w else W
-    li = torch.empty((G // W, nq, K), dtype=torch.int32, device=dev)
-    ld = torch.empty((G // W, nq, K), dtype=torch.float64, device=dev)
-    lc = torch.empty((G // W, nq), dtype=torch.int32, device=dev)
-    lm = torch.empty((G // W, nq), dtype=torch.int64, device=dev)
-    ln = torch.empty((G // W, nq), dtype=torch.int64, device=dev)
-    gi = torch.empty((W, G // W, nq, K), dtype=torch.int32, device=dev)
-    gd = torch.empty((W, G // W, nq, K), dtype=torch.float64, device=dev)
-    oi = torch.empty((nq, K), dtype=torch.int32, device=dev)
-    od = torch.empty((nq, K), dtype=torch.float64, device=dev)
-    oc = torch.empty((nq,), dtype=torch.int32, device=dev)
-    rb = torch.empty((nq,), dtype=torch.float64, device=dev)
-    opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True)
-    opts2 = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True,
-                            probe_lo=w)
-    opts2.r0 = rb.data_ptr()
-    mode = ads.IvfMode.kAdSplit
+    dq = torch.from_numpy(q).to(dev)  # raw queries: every step rotates them (exact fp64) first
     torch.cuda.synchronize()
-
-    def search(o, np_, k):
-        L.check(L.ads_ivf_search_device(local.h, None, C.c_void_p(dq.data_ptr()), nq, K, np_,
-                                        int(mode), 2.1, 32, C.byref(o), C.c_void_p(li[k].data_ptr()),
-                                        C.c_void_p(ld[k].data_ptr()), C.c_void_p(lc[k].data_ptr()),
-                                        C.c_void_p(lm[k].data_ptr()), C.c_void_p(ln[k].data_ptr())))
-
-    def step():
-        if w:
-            search(opts, w, 0)
-            with torch.cuda.stream(stream):
-                torch.where(lc[0] == K, ld[0][:, K - 1], torch.full_like(rb, float("inf")), out=rb)
-                D.pg.all_reduce(rb, op=D.pg.ReduceOp.MIN, group=D.nccl)
-            search(opts2, nprobe, 1)
-        else:
-            search(opts, nprobe, 0)
-        with torch.cuda.stream(stream):
-            D.pg.all_gather_into_tensor(gi, li, group=D.nccl)
-            D.pg.all_gather_into_tensor(gd, ld, group=D.nccl)
-        merge_topk_device(ctx, gd.data_ptr(), gi.data_ptr(), G, nq, K, oi.data_ptr(),
-                          od.data_ptr(), oc.data_ptr())
-
+    log(f"sharded: {W} ranks, rank 0 holds {idx.n} rows, first wave {Sh.w} of {nprobe} probes")
     for _ in range(args.warmup):
         ctx.flush_l2()
-        step()
+        Sh.step(dq, raw=True)
     ctx.sync()
     clocks = ClockSampler(D.local)
     D.barrier()
@@ -664,114 +623,178 @@ def run_search_sharded(args, D: Dist):
     ms = []
     for _ in range(args.steps):
         ctx.flush_l2()
+        ctx.sync()
         D.barrier()
         ctx.timer_start()
-        step()
+        Sh.step(dq, raw=True)
         ms.append(ctx.timer_stop())
     clk = clocks.stop()
     total_ms = D.allmax(float(np.sum(ms)))
-    dims = D.allsum(float(lm.sum().item()))
-    res = {
-        "metric": "IVF++ ADSampling queries/sec at fixed recall@K", "value": nq * args.steps / (total_ms / 1e3),
-        "unit": "queries/s", "n_gpus": W, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(cfg.describe(), nprobe=nprobe, nq_total=nq,
-                       parallelism=f"list-sharded x{W} + NCCL all-gather + merge",
-                       threshold_exchange={"first_wave_probes": w} if w else None),
-        # per step: 11 search kernels per wave (see run_search) + merge_topk (NCCL collectives
-        # and the torch.where of the exchange are library kernels)
-        "gpu_launches": (23 if w else 12) * args.steps,
-        "scanned_gb_per_step_all_ranks": 4.0 * dims / 1e9,
-        "clocks": clk,
-    }
-    if D.rank == 0:
-        ids = oi.cpu().numpy()
-        ngt = min(nq, len(gt))
-        res["config"]["recall_at_k"] = float(np.mean([len(np.intersect1d(ids[i][ids[i] >= 0], gt[i]))
-                                                      for i in range(ngt)]) / K)
-        if ngt < nq:
-            res["config"]["recall_queries"] = ngt
-    # e2e: host queries in, merged results out (pinned buffers), same collective path
-    qh = ads.PinnedArray((nq, d), np.float32)
-    qh.array[:] = qs
-    hout = ads.PinnedArray((nq, K), np.int32)
+    dims = D.allsum(float(Sh.dims_evaluated()))
+    ids = Sh.oi.cpu().numpy()
+    # e2e: pinned host queries in (rotated on the device), merged ids + dists out, per rank
+    qh = torch.from_numpy(q).pin_memory()
+    dq_raw = torch.empty_like(dq)
+    hi = torch.empty((nq, K), dtype=torch.int32).pin_memory()
+    hd = torch.empty((nq, K), dtype=torch.float64).pin_memory()
     e2e = []
     for _ in range(args.steps):
+        ctx.flush_l2()
+        ctx.sync()
         D.barrier()
         t1 = time.perf_counter()
-        dq.copy_(torch.from_numpy(qh.array), non_blocking=True)
-        torch.cuda.synchronize()
-        step()
-        ctx.sync()
-        torch.cuda.synchronize()
-        hout.array[:] = oi.cpu().numpy()
+        dq_raw.copy_(qh, non_blocking=True)
+        Sh.step(dq_raw, raw=True)
+        hi.copy_(Sh.oi, non_blocking=True)
+        hd.copy_(Sh.od, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
         e2e.append(time.perf_counter() - t1)
     e2e_total = D.allmax(float(np.sum(e2e)))
-    res["e2e"] = {"value": nq * args.steps / e2e_total, "unit": "queries/s",
-                  "h2d_bytes_per_step": nq * d * 4, "d2h_bytes_per_step": nq * K * 4}
+    assert np.array_equal(hi.numpy(), ids), "e2e and device-resident sharded results differ"
+    scanned = 4.0 * dims
+    peaks = measured_peaks()
+    res = {
+        "metric": METRIC, "value": nq * args.steps / (total_ms / 1e3), "unit": "queries/s", "n_gpus": W,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Gaussian mixtures with BASELINE.json's shapes; DESIGN.md §6)",
+        "config": workload_config(cfg, nprobe),
+        "parallelism": f"list-sharded x{W} (LPT on list sizes), fixed Q={nq} answered by every rank over "
+                       f"its lists, threshold all-reduce after {Sh.w} probes, NCCL all-gather + merge",
+        "e2e": {"value": nq * args.steps / e2e_total, "unit": "queries/s",
+                "h2d_bytes_per_step": nq * d * 4, "d2h_bytes_per_step": nq * K * 12,
+                "note": "per rank: every rank copies the raw queries in and the merged top-K out"},
+        # per step and rank: the rotation, 2 waves x (centring, coarse GEMM, prefilter, order
+        # key, 5 sort launches, scan) + merge_topk; the all-reduce, all-gather and the
+        # torch.where of the bound are NCCL / torch kernels
+        "gpu_launches": (1 + (2 * 10 if Sh.w else 10) + 1) * args.steps,
+        "roofline": {"bound": "hbm", "achieved": scanned / (total_ms / args.steps / 1e3) / 1e9 / W,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": scanned / (total_ms / args.steps / 1e3) / 1e9 / W / peaks["hbm_gbs"],
+                     "traffic": None, "kernel": "ivf_search_kernel (per GPU, whole step)",
+                     "peak_source": peaks["source"], "algorithmic_bytes_per_step_all_ranks": scanned},
+        "clocks": clk, "setup": S["info"],
+    }
+    if D.rank == 0 and gt is not None:
+        res["recall_at_k"] = recall_of(ids, gt, K)
+        res["recall_queries"] = min(nq, len(gt))
     return res
 
 
 # ---------------------------------------------------------------- reference arm
-def run_reference(args, D: Dist):
-    """The reference's own ivf_query (compiled from /root/reference by oracle/Makefile),
-    on this arm's config, all host threads.  Its index is the one the reference's
-    build_ivf produces (k-means reproduced bit-exactly on the GPU as untimed setup)."""
-    from paper_2303_09855_b200 import configs
-
+def run_reference(args, D):
+    """The reference's own adsann::ivf_query (oracle/_ref, compiled from /root/reference),
+    on this arm's config and metric, all host threads, rank 0 only.  Config 5 is set up
+    without the product library (see the module docstring); configs 1-3 reuse the GPU
+    engine's untimed setup (their reference k-means would take up to hours)."""
     if D.rank != 0:
         return None
     log = lambda *a: print(*a, file=sys.stderr, flush=True)  # noqa: E731
     from oracle import ref_available
 
-    cfg = config_for(args)
-    if args.nq:
-        cfg.nq = args.nq
+    configs = load_configs()
+    cfg = config_for(args, configs)
     nprobe = args.nprobe or cfg.nprobe
-    ads, ctx, base, t, q, m, idx, gt = setup(cfg, 0, 0, log)
-    ex = idx.export()
-    asg = configs.list_assignment(ex["list_off"], ex["ids_flat"])
-    cores = os.cpu_count() or 1
-    if ref_available():
-        from oracle import load_ref
-
-        h = load_ref().assemble_ivf(base, t, m.entries, ex["centroids_t"], asg, seed=cfg.seed,
-                                    split=True, d1=32)
-        kind = "reference"
-    else:
+    if not ref_available():
         return {"impl": "reference", "unavailable": "oracle/_ref/libadsann_ref.so not built"}
-    # bounded sample per step: ~args.cpu_budget / steps seconds each
-    _, _, _, s = h.query_batch(None, q[:64], cfg.K, nprobe, "ad-split", nthreads=cores, P=m.entries)
+    from oracle import load_oracle, load_ref
+
+    ref = load_ref()
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    if is_large(cfg):
+        h, q, gt, P, setup_note = reference_setup_large(cfg, configs, ref, load_oracle(), log)
+    else:
+        S = setup(cfg, D, log)
+        ex = S["idx"].export()
+        asg = configs.list_assignment(ex["list_off"], ex["ids_flat"])
+        h = ref.assemble_ivf(S["base"], S["t"], S["m"].entries, ex["centroids_t"], asg, seed=cfg.seed,
+                             split=True, d1=32)
+        q, gt, P = S["q"], S["gt"], S["m"].entries
+        setup_note = "untimed setup on the GPU engine (data, rotation, k-means reproduced bit-exactly)"
+    log(f"reference setup {time.time() - t0:.1f}s ({setup_note})")
+    # bounded sample per step: ~cpu_budget / (steps + warmup) seconds each
+    _, _, _, s = h.query_batch(None, q[:64], cfg.K, nprobe, "ad-split", nthreads=cores, P=P)
     per_q = s / 64
-    ns = int(max(64, min(nq_cap(cfg), args.cpu_budget / max(1, args.steps + args.warmup) / per_q)))
-    for w in range(args.warmup):
-        h.query_batch(None, q[:ns], cfg.K, nprobe, "ad-split", nthreads=cores, P=m.entries)
-    secs = []
-    recs = []
+    ns = int(max(64, min(cfg.nq, args.cpu_budget / max(1, args.steps + args.warmup) / per_q)))
+    for _ in range(args.warmup):
+        h.query_batch(None, q[:ns], cfg.K, nprobe, "ad-split", nthreads=cores, P=P)
+    secs, recs = [], []
     for s_ in range(args.steps):
         lo = (s_ * ns) % max(1, cfg.nq - ns + 1)
-        ids, _, _, sec = h.query_batch(None, q[lo:lo + ns], cfg.K, nprobe, "ad-split",
-                                       nthreads=cores, P=m.entries)
+        ids, _, _, sec = h.query_batch(None, q[lo:lo + ns], cfg.K, nprobe, "ad-split", nthreads=cores, P=P)
         secs.append(sec)
-        recs.append(np.mean([len(np.intersect1d(ids[i], gt[lo + i])) for i in range(ns)]) / cfg.K)
+        m_ = min(ns, max(0, len(gt) - lo))
+        if m_ > 0:
+            recs.append((recall_of(ids[:m_], gt[lo:lo + m_], cfg.K), m_))
     v = ns * args.steps / float(np.sum(secs))
-    return {"metric": "IVF++ ADSampling queries/sec at fixed recall@K", "value": v,
-            "unit": "queries/s", "n_gpus": D.world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * float(np.mean(secs)), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": dict(cfg.describe(), nprobe=nprobe, recall_at_k=float(np.mean(recs))),
-            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": kind,
-                             "sample": f"{ns} queries per step, ivf_query kAdSplit with rotation "
+    rec = (sum(r * w for r, w in recs) / sum(w for _, w in recs)) if recs else None
+    return {"metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": D.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)), "higher_is_better": True,
+            "scaling": "strong" if D.world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Gaussian mixtures with BASELINE.json's shapes; DESIGN.md §6)",
+            "impl": "reference", "config": workload_config(cfg, nprobe),
+            "parallelism": f"{cores} host threads over queries (rank 0 only)",
+            "recall_at_k": rec, "setup": setup_note,
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "reference",
+                             "sample": f"{ns} queries per step, adsann::ivf_query kAdSplit with adsann::apply "
                                        f"inside the loop (run_timed protocol), {cores} host threads"},
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def nq_cap(cfg):
-    return cfg.nq
+def reference_setup_large(cfg, configs, ref, orc, log):
+    """Config 5 for the reference arm with no product code: oracle generator, the
+    reference's apply_dataset, committed centroids, exact assignment (oracle.ref_workload),
+    kAdSplit-only reference IvfIndex."""
+    from oracle import ref_workload
+
+    if not os.path.exists(CFG5_CENTROIDS):
+        raise SystemExit("reference arm: tests/golden/cfg5_centroids.npy missing")
+    cent = np.load(CFG5_CENTROIDS)
+    P = ref.generate_orthogonal(cfg.d, cfg.seed)
+    gen = orc.synth_rows
+    rows = configs.row_source(cfg, gen=gen)
+    q = configs.generate_queries(cfg, gen=gen)
+    T = np.empty((cfg.n, cfg.d), np.float32)
+    chunk = 2_000_000
+    t0 = time.time()
+    asg = np.empty(cfg.n, np.int32)
+    # CPU: generate + rotate chunk i+1 while the GPU assigns chunk i
+    nxt = {}
+
+    def produce(lo):
+        hi = min(cfg.n, lo + chunk)
+        T[lo:hi] = ref.apply_dataset(P, rows(lo, hi - lo))
+        nxt[lo] = hi
+
+    th = threading.Thread(target=produce, args=(0,))
+    th.start()
+    for lo in range(0, cfg.n, chunk):
+        th.join()
+        hi = nxt.pop(lo)
+        if hi < cfg.n:
+            th = threading.Thread(target=produce, args=(hi,))
+            th.start()
+        asg[lo:hi] = ref_workload.exact_assign(T[lo:hi], cent)
+    log(f"reference arm: generated (oracle), rotated (reference apply_dataset) and assigned {cfg.n} rows "
+        f"in {time.time() - t0:.1f}s")
+    ng = min(cfg.extra.get("gt_queries", 100), cfg.nq)
+    gt = ref_workload.exact_knn(T, ref.apply_dataset(P, q[:ng]), cfg.K)
+    h = ref.assemble_split(T, cent, asg, seed=cfg.seed, d1=32)
+    del T
+    gc.collect()
+    return h, q, gt, P, ("no product code: oracle generator (pinned to ads_synth_rows), reference "
+                         "apply_dataset, committed sampled-k-means centroids (bit-identical to the GPU "
+                         "arm's), exact fp64 assignment and ground truth certified in PyTorch on the GPU")
 
 
 # ---------------------------------------------------------------- main
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -779,44 +802,44 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="search", choices=["search", "dco", "transform", "theory"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--nprobe", type=int, default=0)
     ap.add_argument("--nq", type=int, default=0)
     ap.add_argument("--step", type=int, default=0, help="threshold refresh interval (0: 64 x warps)")
     ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0: 4 for D <= 256, else 10)")
-    ap.add_argument("--slots", type=int, default=4, help="queries served concurrently per CTA")
     ap.add_argument("--ctas-per-sm", type=int, default=0, help="cap on resident search CTAs per SM (0: occupancy)")
     ap.add_argument("--query-order", type=int, default=2,
                     help="2: longest queries first (default), 1: L2-locality order, 0: input order")
-    ap.add_argument("--same-query", action="store_true", help="experiment: all queries = query 0")
     ap.add_argument("--sweep", action="store_true")
-    ap.add_argument("--tune", action="store_true", help="time (step, warps) variants after setup")
-    ap.add_argument("--tune-grid", default="", help="comma list of STEPxWARPS for --tune")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-3 measurement on the N=1 line")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--kmeans-init", type=int, default=-1, help="override (profiling runs: 1)")
+    ap.add_argument("--kmeans-iters", type=int, default=0)
     ap.add_argument("--shard", default="auto", choices=["auto", "lists", "replicas"],
-                    help="N>1: IVF lists partitioned across GPUs + NCCL all-gather merge, or query-sharded "
-                         "replicas; auto = lists for config 5 (the sharded config), replicas for configs that "
-                         "fit one GPU (SURVEY §8e)")
+                    help="N>1: IVF lists partitioned across GPUs (default for config 5) or query-sharded "
+                         "replicas (default for the configs that fit one GPU, SURVEY §8e)")
     ap.add_argument("--dco-n", type=int, default=10_000_000)
     ap.add_argument("--waves", type=int, default=-1,
                     help="list-sharded search: probe ranks of the first wave before the threshold "
-                         "all-reduce (-1: nprobe/8 when N > 1, else one wave; 0: one wave, no exchange)")
-    ap.add_argument("--force-shard", action="store_true",
-                    help="run the list-sharded path even at N=1 (exercises NCCL + merge)")
-    ap.add_argument("--kmeans-iters", type=int, default=0)
+                         "all-reduce (-1: nprobe/8 when N > 1; 0: one wave, no exchange)")
     ap.add_argument("--cfg-override", default="",
-                    help="calibration runs: comma list of Config fields / extra keys, e.g. sigma=0.5,gt_queries=30")
+                    help="calibration runs: comma list of Config fields / extra keys, e.g. sigma=0.5")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: spawn the N ranks ourselves (the driver may also launch us
+        # under torchrun, which sets WORLD_SIZE)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    expect = args.gpus if "WORLD_SIZE" in os.environ else None
     if args.shard == "auto":
-        from paper_2303_09855_b200 import configs as _cf
-
-        args.shard = "lists" if (args.force_shard or _cf.CONFIGS[args.config].n > 20_000_000) else "replicas"
+        args.shard = "lists" if load_configs().CONFIGS[args.config].n > 20_000_000 else "replicas"
     sharded = args.impl == "ours" and args.mode == "search" and args.shard == "lists"
-    D = Dist("nccl" if sharded else "gloo", force=sharded and args.force_shard)
+    D = Dist("nccl" if sharded else "gloo", expect=expect if args.impl == "ours" else None)
     try:
         if args.impl == "reference":
             res = run_reference(args, D)
@@ -832,11 +855,12 @@ def main():
             from bench_theory import run_theory
 
             res = run_theory(args, D)
-        elif sharded and (D.world > 1 or args.force_shard):
-            res = run_search_sharded(args, D)
+        elif sharded and D.world > 1:
+            res = run_sharded(args, D)
         else:
             res = run_search(args, D)
         if D.rank == 0 and res is not None:
+            res.pop("ids", None)
             print(json.dumps(res), flush=True)
     finally:
         D.close()

@@ -79,6 +79,11 @@ typedef struct {
     int32_t threads;    /* 0 = hardware concurrency */
 } ads_synth_desc;
 int ads_synth(const ads_synth_desc *desc, float *out, int32_t *component_out /* nullable */);
+/* Rows row_lo + i*stride (i < count) of the same n-row mixture, bit-identical to
+ * those rows of ads_synth's output (row r depends only on (desc, r)): chunked
+ * generation of config 5 and its strided k-means sample. */
+int ads_synth_rows(const ads_synth_desc *desc, int64_t row_lo, int64_t count, int64_t stride, float *out,
+                   int32_t *component_out /* nullable */);
 
 /* ------------------------------------------------------------------ device context */
 typedef struct ads_ctx ads_ctx;
@@ -219,7 +224,38 @@ int ads_ivf_build(ads_ctx *ctx, const float *raw, const float *t, int32_t n, int
 int ads_ivf_build_sampled_device(ads_ctx *ctx, const float *dT, int64_t n, int32_t d, const double *P,
                                  int32_t k, uint64_t seed, int32_t d1, int32_t max_iters, int64_t sample,
                                  ads_ivf **out);
+/* The same build fed in row chunks, for datasets generated or loaded piecewise and
+ * for list-sharded indexes: create; train (k-means with seeded sample
+ * init on the given transformed sample rows, device pointer) or set_centroids (host
+ * k x d); add_device every transformed row in order (row ids = row_lo ..); then
+ * finish, which lays out only the lists with keep[c] != 0 (keep NULL = all; ids stay
+ * global, like ads_ivf_subset) and may be called once per shard.  list_sizes gives the
+ * k list sizes of the whole dataset (for partitioning lists across GPUs).  Fed with
+ * the strided sample and every row, it is ads_ivf_build_sampled_device. */
+typedef struct ads_ivf_builder ads_ivf_builder;
+int ads_ivf_builder_create(ads_ctx *ctx, int64_t n, int32_t d, const double *P, int32_t k, uint64_t seed,
+                           int32_t d1, ads_ivf_builder **out);
+int ads_ivf_builder_train_device(ads_ivf_builder *b, const float *dS, int64_t sample, int32_t max_iters);
+int ads_ivf_builder_set_centroids(ads_ivf_builder *b, const float *centroids);
+int ads_ivf_builder_centroids(ads_ivf_builder *b, float *centroids);
+int ads_ivf_builder_add_device(ads_ivf_builder *b, const float *dT, int64_t row_lo, int64_t rows);
+int ads_ivf_builder_list_sizes(ads_ivf_builder *b, int64_t *sizes);
+/* The staged transformed rows (n x d, by row id; device memory owned by the builder,
+ * valid until destroy): e.g. for an exact ground truth before they are released. */
+int ads_ivf_builder_rows_device(ads_ivf_builder *b, const float **rows);
+int ads_ivf_builder_finish(ads_ivf_builder *b, const uint8_t *keep, ads_ivf **out);
+int ads_ivf_builder_destroy(ads_ivf_builder *b);
 int ads_ivf_destroy(ads_ivf *idx);
+/* save_ivf / load_ivf, ivf.hpp:91-92 / ivf.cpp:423-501: the reference's on-disk
+ * format (meta.txt + centroids_*.fvecs, buckets.ivecs (ragged), vec_*.fvecs and, for
+ * the split layout, a1_* / a2_*.fvecs), so a directory written by adsann::save_ivf
+ * loads here and the reverse.  An index without raw vectors (config 5) is written
+ * without the raw files, which the reference's format cannot express (its read_fvecs
+ * rejects empty files): such a directory loads into the engine only.  P (nullable) is
+ * not part of the format (the reference keeps TransformMatrix apart, save_matrix);
+ * pass it to enable on-device query rotation. */
+int ads_ivf_save(ads_ivf *idx, const char *dir);
+int ads_ivf_load(ads_ctx *ctx, const char *dir, const double *P, ads_ivf **out);
 /* meta[0..6] = n, d, k_clusters, d1, layout, seed, has_raw */
 int ads_ivf_meta(ads_ivf *idx, int64_t *meta);
 /* Copy the index back to the host (any pointer nullable). */

@@ -359,6 +359,16 @@ static double assign_points(const float *X, int32_t n, int32_t d, const float *C
     return obj;
 }
 
+/* The assignment step on its own (ivf.cpp:36-60): nearest centroid by exact fp64
+ * l2_sq, lowest id on ties; what build_ivf's buckets come from. */
+int orc_assign(const float *X, int32_t n, int32_t d, const float *C, int32_t k, int32_t *assignment) {
+    if (k < 1 || n < 0) return fail(1, "assign: bad shape");
+    double *best = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    (void)assign_points(X, n, d, C, k, assignment, best);
+    free(best);
+    return 0;
+}
+
 /* ivf.cpp:62-117: k-means++ seeding with a sequential fp64 CDF walk. */
 static void kmeanspp(const float *X, int32_t n, int32_t d, int32_t k, orc_rng *rng, float *C) {
     double *min_d2 = malloc(sizeof(double) * (size_t)n);
@@ -408,12 +418,37 @@ static void kmeanspp(const float *X, int32_t n, int32_t d, int32_t k, orc_rng *r
 }
 
 /* ivf.cpp:121-190 */
+/* The engine's "seeded sample" initialisation (ads_kmeans init 1, used for the
+ * configs whose k-means++ would take too long; not a reference algorithm): a
+ * partial Fisher-Yates shuffle of the row ids drawn from the same
+ * Rng::for_stream(seed, kKmeans) stream, centroid c = row perm[c]. */
+static void sample_init(const float *X, int32_t n, int32_t d, int32_t k, orc_rng *rng, float *C) {
+    int32_t *perm = malloc(sizeof(int32_t) * (size_t)n);
+    for (int32_t i = 0; i < n; ++i) perm[i] = i;
+    for (int32_t c = 0; c < k; ++c) {
+        const int64_t j = c + (int64_t)(orc_rng_next_u64(rng) % (uint64_t)(n - c));
+        const int32_t tmp = perm[c];
+        perm[c] = perm[j];
+        perm[j] = tmp;
+        memcpy(C + (int64_t)c * d, X + (int64_t)perm[c] * d, sizeof(float) * (size_t)d);
+    }
+    free(perm);
+}
+
 int orc_kmeans(const float *X, int32_t n, int32_t d, int32_t k, int max_iters, uint64_t seed,
                float *centroids, int32_t *assignment, double *objective, int *iterations) {
+    return orc_kmeans_init(X, n, d, k, max_iters, seed, 0, centroids, assignment, objective,
+                           iterations);
+}
+
+int orc_kmeans_init(const float *X, int32_t n, int32_t d, int32_t k, int max_iters, uint64_t seed,
+                    int init, float *centroids, int32_t *assignment, double *objective,
+                    int *iterations) {
     if (k < 1) return fail(1, "kmeans: k must be >= 1");
     if (k > n) return fail(1, "kmeans: k exceeds the number of points");
     orc_rng rng = orc_rng_for_stream(seed, TAG_KMEANS);
-    kmeanspp(X, n, d, k, &rng, centroids);
+    if (init == 1) sample_init(X, n, d, k, &rng, centroids);
+    else kmeanspp(X, n, d, k, &rng, centroids);
     double *best_d2 = malloc(sizeof(double) * (size_t)n);
     double *sums = malloc(sizeof(double) * (size_t)k * d);
     int64_t *counts = malloc(sizeof(int64_t) * (size_t)k);
@@ -843,5 +878,103 @@ int orc_verify_theory(const float *X, int32_t n, int32_t d, const float *Q, int3
     free(dist_sq);
     free(kth);
     free(reject_at);
+    return 0;
+}
+
+/* ------------------------------------------------------------ mixture generator
+ * Restatement of the engine's seeded Gaussian-mixture generator (the
+ * benchmark configs' synthetic stand-in for the paper's datasets, DESIGN.md
+ * §6), built on the reference's Rng (rng.hpp:36-97).  The bench's reference
+ * arm generates config data with it, so that arm never loads the product
+ * library; tests pin it bit-for-bit against ads_synth_rows.  Row r depends
+ * only on (desc, r): component draw = counter r of the component stream,
+ * noise = normals r*d .. r*d+d-1 of the noise stream.  Multi-threaded over
+ * output rows (results do not depend on the thread count). */
+#include <pthread.h>
+
+#define TAG_CENTERS 0x43454e5445525331ULL /* "CENTERS1" */
+#define TAG_COMP 0x434f4d504f4e5431ULL    /* "COMPONT1" */
+#define TAG_NOISE 0x4e4f495345303031ULL   /* "NOISE001" */
+
+typedef struct {
+    const orc_synth_desc *s;
+    const double *centers, *sig;
+    uint64_t role_seed;
+    int64_t row_lo, stride, lo, hi;
+    float *out;
+} synth_job;
+
+static void *synth_work(void *arg) {
+    const synth_job *j = (const synth_job *)arg;
+    const orc_synth_desc *s = j->s;
+    const int32_t d = s->d, C = s->components;
+    double *row = (double *)malloc(sizeof(double) * (size_t)d);
+    orc_rng comp = orc_rng_make(mix64(j->role_seed ^ TAG_COMP));
+    orc_rng noise = orc_rng_for_stream(j->role_seed, TAG_NOISE);
+    for (int64_t i = j->lo; i < j->hi; ++i) {
+        const int64_t r = j->row_lo + i * j->stride;
+        comp.counter = (uint64_t)r;
+        /* normal m = r*d: pair p = m/2 consumes counters 2p+1, 2p+2 */
+        const uint64_t m = (uint64_t)r * (uint64_t)d;
+        noise.counter = 2 * (m / 2);
+        noise.has_cached = 0;
+        if (m % 2) (void)orc_rng_normal(&noise);
+        int32_t c;
+        if (s->assign_mode == 1) c = (int32_t)((r * C) / (s->n > 0 ? s->n : 1));
+        else c = (int32_t)orc_rng_below(&comp, (uint64_t)C);
+        const double *cc = j->centers + (size_t)c * d;
+        double nrm = 0.0;
+        for (int32_t k = 0; k < d; ++k) {
+            double x = cc[k] + j->sig[k] * orc_rng_normal(&noise);
+            if (s->kind == 1) x = fmin(255.0, fmax(0.0, round(x)));
+            else if (s->kind == 2) x = fmin(1.0, fmax(0.0, x));
+            row[k] = x;
+            nrm += x * x;
+        }
+        float *o = j->out + (size_t)i * d;
+        if (s->kind == 3) {
+            const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+            for (int32_t k = 0; k < d; ++k) o[k] = (float)(row[k] * inv);
+        } else {
+            for (int32_t k = 0; k < d; ++k) o[k] = (float)row[k];
+        }
+    }
+    free(row);
+    return NULL;
+}
+
+int orc_synth_rows(const orc_synth_desc *s, int64_t row_lo, int64_t count, int64_t stride,
+                   int32_t threads, float *out) {
+    if (s->n < 0 || s->d < 1 || s->components < 1) return fail(1, "synth: bad shape");
+    if (!(s->sigma >= 0.0)) return fail(1, "synth: sigma must be >= 0");
+    if (count < 0 || stride < 1 || row_lo < 0 || (count > 0 && row_lo + (count - 1) * stride >= s->n))
+        return fail(1, "synth: row range outside [0, n)");
+    const int32_t d = s->d, C = s->components;
+    double *centers = (double *)malloc(sizeof(double) * (size_t)C * d);
+    double *sig = (double *)malloc(sizeof(double) * (size_t)d);
+    orc_rng rng = orc_rng_for_stream(s->seed, TAG_CENTERS);
+    for (size_t e = 0; e < (size_t)C * d; ++e) {
+        if (s->kind == 1 || s->kind == 2)
+            centers[e] = s->center_lo + (s->center_hi - s->center_lo) * orc_rng_uniform(&rng);
+        else
+            centers[e] = s->center_scale * orc_rng_normal(&rng);
+    }
+    for (int32_t k = 0; k < d; ++k)
+        sig[k] = s->decay ? s->sigma / sqrt(1.0 + (double)k / 32.0) : s->sigma;
+    const uint64_t role_seed = mix64(s->seed ^ (s->role * 0x9E3779B97F4A7C15ULL + 1));
+    int32_t nt = threads < 1 ? 1 : (threads > 256 ? 256 : threads);
+    if (count < 4096) nt = 1;
+    synth_job jobs[256];
+    pthread_t th[256];
+    for (int32_t t = 0; t < nt; ++t) {
+        synth_job j = {s, centers, sig, role_seed, row_lo, stride, count * t / nt,
+                       count * (t + 1) / nt, out};
+        jobs[t] = j;
+    }
+    for (int32_t t = 1; t < nt; ++t) pthread_create(&th[t], NULL, synth_work, &jobs[t]);
+    synth_work(&jobs[0]);
+    for (int32_t t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+    free(centers);
+    free(sig);
     return 0;
 }

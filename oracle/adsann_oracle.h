@@ -72,6 +72,13 @@ int orc_ad_scan_pairs(const float *X, const float *Q, int32_t dim, int64_t npair
 /* ivf.cpp:36-190 */
 int orc_kmeans(const float *X, int32_t n, int32_t d, int32_t k, int max_iters, uint64_t seed,
                float *centroids, int32_t *assignment, double *objective, int *iterations);
+/* nearest centroid per row (ivf.cpp:36-60 assignment; lowest id on ties) */
+int orc_assign(const float *X, int32_t n, int32_t d, const float *C, int32_t k, int32_t *assignment);
+/* init 0: k-means++ (the reference, ivf.cpp:62-117); 1: the engine's seeded-sample
+ * init (ads_kmeans init 1; config 3/5 builds), followed by the same Lloyd loop. */
+int orc_kmeans_init(const float *X, int32_t n, int32_t d, int32_t k, int max_iters, uint64_t seed,
+                    int init, float *centroids, int32_t *assignment, double *objective,
+                    int *iterations);
 
 /* bench.cpp:31-61 */
 int orc_brute_force_knn(const float *base, int32_t n, int32_t d, const float *queries,
@@ -139,6 +146,20 @@ int orc_probe_order(const float *centroids, int32_t L, int32_t d, const float *q
 int orc_verify_theory(const float *X, int32_t n, int32_t d, const float *Q, int32_t nq, int32_t K,
                       const double *grid, int32_t G, double *eps_sorted, uint64_t *dims,
                       uint64_t *failures, uint64_t *positives);
+
+/* The benchmark configs' seeded Gaussian-mixture generator (restated from the
+ * engine's ads_synth_rows; same field meaning as ads_synth_desc): rows
+ * row_lo + i*stride, i < count, on `threads` host threads. */
+typedef struct {
+    int64_t n;
+    int32_t d, components;
+    uint64_t seed, role;
+    int32_t kind;
+    double center_scale, center_lo, center_hi, sigma;
+    int32_t decay, assign_mode, threads;
+} orc_synth_desc;
+int orc_synth_rows(const orc_synth_desc *s, int64_t row_lo, int64_t count, int64_t stride,
+                   int32_t threads, float *out);
 
 #ifdef __cplusplus
 }

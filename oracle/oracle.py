@@ -180,6 +180,13 @@ class _Common:
         return ids
 
 
+class _SynthDesc(C.Structure):
+    _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("components", C.c_int32), ("seed", C.c_uint64),
+                ("role", C.c_uint64), ("kind", C.c_int32), ("center_scale", C.c_double),
+                ("center_lo", C.c_double), ("center_hi", C.c_double), ("sigma", C.c_double),
+                ("decay", C.c_int32), ("assign_mode", C.c_int32), ("threads", C.c_int32)]
+
+
 class Oracle(_Common):
     """The plain-C restatement (oracle/adsann_oracle.c)."""
 
@@ -187,6 +194,15 @@ class Oracle(_Common):
 
     def __init__(self, path=ORACLE_SO):
         super().__init__(path)
+        self.lib.orc_synth_rows.argtypes = [C.POINTER(_SynthDesc), C.c_int64, C.c_int64, C.c_int64,
+                                            C.c_int32, C.c_void_p]
+        self.lib.orc_synth_rows.restype = C.c_int
+        self.lib.orc_kmeans_init.argtypes = [_f32p, C.c_int32, C.c_int32, C.c_int32, C.c_int, C.c_uint64,
+                                             C.c_int, _f32p, _i32p, C.POINTER(C.c_double),
+                                             C.POINTER(C.c_int)]
+        self.lib.orc_kmeans_init.restype = C.c_int
+        self.lib.orc_assign.argtypes = [_f32p, C.c_int32, C.c_int32, _f32p, C.c_int32, _i32p]
+        self.lib.orc_assign.restype = C.c_int
         self._fn("orc_ivf_layout", [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int, _f64p,
                                     _f32p, _i32p, _f32p, _f32p, _i64p, _i32p, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _vp])
@@ -206,6 +222,38 @@ class Oracle(_Common):
         self._fn("orc_ivf_query_waves", [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int, C.c_double,
                                          C.c_int32, _i32p, C.c_int32, _i32p, _f64p,
                                          C.POINTER(C.c_int32), _u64p])
+
+    def synth_rows(self, n, d, components, seed, role, row_lo, count, stride=1, kind=0,
+                   center_scale=1.0, center_lo=0.0, center_hi=1.0, sigma=1.0, decay=False,
+                   assign_mode=0, threads=0, out=None):
+        """Rows row_lo + i*stride of the benchmark mixture (restated generator)."""
+        desc = _SynthDesc(n, d, components, seed, role, kind, center_scale, center_lo, center_hi,
+                          sigma, int(decay), assign_mode, 0)
+        if out is None:
+            out = np.empty((count, d), np.float32)
+        threads = threads or (os.cpu_count() or 1)
+        self._check(self.lib.orc_synth_rows(C.byref(desc), row_lo, count, stride, threads,
+                                            out.ctypes.data))
+        return out
+
+    def assign(self, X, centroids):
+        """Nearest centroid per row (exact fp64, lowest id on ties)."""
+        X = _f32(X)
+        Cn = _f32(centroids)
+        out = np.empty(X.shape[0], np.int32)
+        self._check(self.lib.orc_assign(X, X.shape[0], X.shape[1], Cn, Cn.shape[0], out))
+        return out
+
+    def kmeans_init(self, X, k, max_iters, seed, init):
+        """orc_kmeans_init: init 0 k-means++ (reference), 1 the engine's seeded sample."""
+        X = _f32(X)
+        n, d = X.shape
+        cent = np.empty((max(k, 1), d), np.float32)
+        asg = np.empty(n, np.int32)
+        obj, it = C.c_double(), C.c_int()
+        self._check(self.lib.orc_kmeans_init(X, n, d, k, max_iters, seed, init, cent, asg,
+                                             C.byref(obj), C.byref(it)))
+        return cent, asg, obj.value, it.value
 
     def ivf_layout(self, raw, t, P, centroids_t, assignment, k, d1=32, split=True):
         """ivf.cpp:211-256 layout from a clustering → dict of host arrays."""
@@ -375,6 +423,10 @@ class RefLib(_Common):
                                    C.c_uint64, C.c_int, C.c_int32], _vp)
         self._fn("ref_ivf_assemble", [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int,
                                       C.c_uint64, _f64p, _f32p, _i32p, _f32p, _f32p], _vp)
+        self._fn("ref_ivf_assemble_split", [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
+                                            _f32p, _i32p, _f32p], _vp)
+        self._fn("ref_ivf_from_split_layout", [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
+                                               _f32p, _i64p, _i32p, _f32p, _f32p], _vp)
         self._fn("ref_ivf_free", [_vp], None)
         self._fn("ref_ivf_meta", [_vp, _i64p])
         self._fn("ref_ivf_export", [_vp] + [_vp] * 10)
@@ -408,6 +460,25 @@ class RefLib(_Common):
         return self._handle(self._ivf_assemble(n, d, cent.shape[0], d1, int(split), seed, _f64(P),
                                                cent, np.ascontiguousarray(assignment, np.int32),
                                                raw, _f32(t)))
+
+    def assemble_split(self, t, centroids_t, assignment, seed=0, d1=32):
+        """kAdSplit-only reference IvfIndex (centroids_t, buckets, ids_flat, a1_t, a2_t)
+        from transformed rows by id and their list assignment."""
+        t = _f32(t)
+        n, d = t.shape
+        k = centroids_t.shape[0]
+        return self._handle(self._ivf_assemble_split(n, d, k, d1, seed, _f32(centroids_t),
+                                                     np.ascontiguousarray(assignment, np.int32), t))
+
+    def from_split_layout(self, centroids_t, list_off, ids_flat, a1_t, a2_t, seed=0):
+        """kAdSplit-only reference IvfIndex from a bucket-major split layout."""
+        a1_t, a2_t = _f32(a1_t), _f32(a2_t)
+        n, d1 = a1_t.shape
+        d = d1 + a2_t.shape[1]
+        k = centroids_t.shape[0]
+        return self._handle(self._ivf_from_split_layout(
+            n, d, k, d1, seed, _f32(centroids_t), np.ascontiguousarray(list_off, np.int64),
+            np.ascontiguousarray(ids_flat, np.int32), a1_t, a2_t))
 
     def load_ivf(self, path):
         return self._handle(self._load_ivf(str(path).encode()))

@@ -9,6 +9,8 @@
 //
 // Status codes: 0 ok, 1 std::invalid_argument, 2 std::runtime_error / other.
 
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -290,6 +292,73 @@ void* ref_ivf_assemble(std::int32_t n, std::int32_t d, std::int32_t k, std::int3
     return rc == 0 ? idx : nullptr;
 }
 
+// The IVF++ (kAdSplit) subset of that index: ivf_query in kAdSplit reads only
+// centroids_t, buckets, ids_flat, a1_t and a2_t (ivf.cpp:296-419), so for
+// config 5 (1e8 x 96) only those are built (~39 GB instead of six full copies).
+// Other modes must not be run on it.  t holds the transformed rows by id.
+void* ref_ivf_assemble_split(std::int32_t n, std::int32_t d, std::int32_t k, std::int32_t d1,
+                             std::uint64_t seed, const float* centroids_t,
+                             const std::int32_t* assignment, const float* t) {
+    IvfIndex* idx = nullptr;
+    const int rc = guard([&] {
+        if (d1 < 1 || d1 >= d) throw std::invalid_argument("assemble: bad d1");
+        auto* x = new IvfIndex();
+        x->n = n;
+        x->d = d;
+        x->k_clusters = k;
+        x->d1 = d1;
+        x->layout = IvfLayout::kSplit;
+        x->seed = seed;
+        x->centroids_t = make_ds(centroids_t, k, d);
+        x->buckets.assign(k, {});
+        for (std::int32_t i = 0; i < n; ++i) x->buckets.at(assignment[i]).push_back(i);
+        const std::int32_t d2 = d - d1;
+        x->ids_flat.reserve(n);
+        x->a1_t.resize(static_cast<std::size_t>(n) * d1);
+        x->a2_t.resize(static_cast<std::size_t>(n) * d2);
+        std::size_t p = 0;
+        for (std::int32_t c = 0; c < k; ++c)
+            for (const std::int32_t id : x->buckets[c]) {
+                x->ids_flat.push_back(id);
+                const float* row = t + static_cast<std::size_t>(id) * d;
+                std::memcpy(&x->a1_t[p * d1], row, d1 * 4);
+                std::memcpy(&x->a2_t[p * d2], row + d1, d2 * 4);
+                ++p;
+            }
+        idx = x;
+    });
+    return rc == 0 ? idx : nullptr;
+}
+
+// The same from an existing bucket-major split layout (e.g. one exported from the
+// GPU engine): list_off (k+1), ids_flat, a1_t (n x d1), a2_t (n x (d-d1)).
+void* ref_ivf_from_split_layout(std::int32_t n, std::int32_t d, std::int32_t k, std::int32_t d1,
+                                std::uint64_t seed, const float* centroids_t,
+                                const std::int64_t* list_off, const std::int32_t* ids_flat,
+                                const float* a1_t, const float* a2_t) {
+    IvfIndex* idx = nullptr;
+    const int rc = guard([&] {
+        if (d1 < 1 || d1 >= d) throw std::invalid_argument("assemble: bad d1");
+        if (list_off[0] != 0 || list_off[k] != n) throw std::invalid_argument("assemble: bad list_off");
+        auto* x = new IvfIndex();
+        x->n = n;
+        x->d = d;
+        x->k_clusters = k;
+        x->d1 = d1;
+        x->layout = IvfLayout::kSplit;
+        x->seed = seed;
+        x->centroids_t = make_ds(centroids_t, k, d);
+        x->buckets.assign(k, {});
+        for (std::int32_t c = 0; c < k; ++c)
+            x->buckets[c].assign(ids_flat + list_off[c], ids_flat + list_off[c + 1]);
+        x->ids_flat.assign(ids_flat, ids_flat + n);
+        x->a1_t.assign(a1_t, a1_t + static_cast<std::size_t>(n) * d1);
+        x->a2_t.assign(a2_t, a2_t + static_cast<std::size_t>(n) * (d - d1));
+        idx = x;
+    });
+    return rc == 0 ? idx : nullptr;
+}
+
 void ref_ivf_free(void* h) { delete static_cast<IvfIndex*>(h); }
 
 // meta[0..5] = n, d, k_clusters, d1, layout, seed
@@ -402,12 +471,18 @@ int ref_ivf_query_batch(void* h, const double* P, int rotate, const float* Qt, c
         if (nthreads <= 1) {
             work(0, 0, nq);
         } else {
+            // dynamic scheduling: threads take queries from a shared counter in
+            // blocks of 4, so uneven per-query costs do not idle the other threads
+            std::atomic<std::int32_t> next{0};
             std::vector<std::thread> th;
-            for (int t = 0; t < nthreads; ++t) {
-                const std::int32_t lo = static_cast<std::int32_t>(static_cast<std::int64_t>(nq) * t / nthreads);
-                const std::int32_t hi = static_cast<std::int32_t>(static_cast<std::int64_t>(nq) * (t + 1) / nthreads);
-                th.emplace_back(work, t, lo, hi);
-            }
+            for (int t = 0; t < nthreads; ++t)
+                th.emplace_back([&, t] {
+                    for (;;) {
+                        const std::int32_t lo = next.fetch_add(4);
+                        if (lo >= nq) break;
+                        work(t, lo, std::min<std::int32_t>(nq, lo + 4));
+                    }
+                });
             for (auto& x : th) x.join();
         }
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -70,6 +70,7 @@ ads_generate_orthogonal = _sig("ads_generate_orthogonal", [i32, u64, vp])
 ads_threshold_multiplier = _sig("ads_threshold_multiplier", [i32, f64, pf64])
 ads_ad_context = _sig("ads_ad_context", [f64, i32, i32, vp])
 ads_synth = _sig("ads_synth", [C.POINTER(SynthDesc), vp, vp])
+ads_synth_rows = _sig("ads_synth_rows", [C.POINTER(SynthDesc), i64, i64, i64, vp, vp])
 ads_ctx_create = _sig("ads_ctx_create", [i32, C.POINTER(vp)])
 ads_ctx_destroy = _sig("ads_ctx_destroy", [vp])
 ads_ctx_sync = _sig("ads_ctx_sync", [vp])
@@ -104,6 +105,8 @@ ads_ivf_build = _sig("ads_ivf_build", [vp, vp, vp, i32, i32, vp, i32, u64, i32, 
                                        C.POINTER(vp)])
 ads_ivf_destroy = _sig("ads_ivf_destroy", [vp])
 ads_ivf_meta = _sig("ads_ivf_meta", [vp, vp])
+ads_ivf_save = _sig("ads_ivf_save", [vp, C.c_char_p])
+ads_ivf_load = _sig("ads_ivf_load", [vp, C.c_char_p, vp, C.POINTER(vp)])
 ads_ivf_export = _sig("ads_ivf_export", [vp] * 9)
 ads_search_opts_default = _sig("ads_search_opts_default", [C.POINTER(SearchOpts)], None)
 ads_ivf_search = _sig("ads_ivf_search", [vp, vp, vp, i32, i32, i32, i32, f64, i32,
@@ -114,6 +117,15 @@ ads_ivf_probe_order = _sig("ads_ivf_probe_order", [vp, vp, i32, i32, i32, vp])
 ads_ivf_last_timings = _sig("ads_ivf_last_timings", [vp, vp])
 ads_ivf_coarse_stats = _sig("ads_ivf_coarse_stats", [vp, vp])
 ads_ivf_build_sampled_device = _sig("ads_ivf_build_sampled_device", [vp, vp, i64, i32, vp, i32, u64, i32, i32, i64, C.POINTER(vp)])
+ads_ivf_builder_create = _sig("ads_ivf_builder_create", [vp, i64, i32, vp, i32, u64, i32, C.POINTER(vp)])
+ads_ivf_builder_train_device = _sig("ads_ivf_builder_train_device", [vp, vp, i64, i32])
+ads_ivf_builder_set_centroids = _sig("ads_ivf_builder_set_centroids", [vp, vp])
+ads_ivf_builder_centroids = _sig("ads_ivf_builder_centroids", [vp, vp])
+ads_ivf_builder_add_device = _sig("ads_ivf_builder_add_device", [vp, vp, i64, i64])
+ads_ivf_builder_rows_device = _sig("ads_ivf_builder_rows_device", [vp, C.POINTER(vp)])
+ads_ivf_builder_list_sizes = _sig("ads_ivf_builder_list_sizes", [vp, vp])
+ads_ivf_builder_finish = _sig("ads_ivf_builder_finish", [vp, vp, C.POINTER(vp)])
+ads_ivf_builder_destroy = _sig("ads_ivf_builder_destroy", [vp])
 ads_ivf_subset = _sig("ads_ivf_subset", [vp, vp, C.POINTER(vp)])
 ads_merge_topk = _sig("ads_merge_topk", [vp, vp, vp, i32, i32, i32, vp, vp, vp])
 ads_merge_topk_device = _sig("ads_merge_topk_device", [vp, vp, vp, i32, i32, i32, vp, vp, vp])

@@ -254,6 +254,22 @@ def synth(n: int, d: int, components: int, seed: int, role: int, kind: int = 0,
     return (out, comp) if with_components else out
 
 
+def synth_rows(n: int, d: int, components: int, seed: int, role: int, row_lo: int, count: int,
+               stride: int = 1, out: Optional[np.ndarray] = None, kind: int = 0,
+               center_scale: float = 1.0, center_lo: float = 0.0, center_hi: float = 1.0,
+               sigma: float = 1.0, decay: bool = False, assign_mode: int = 0,
+               threads: int = 0) -> np.ndarray:
+    """Rows row_lo + i*stride (i < count) of synth(n, ...), bit-identical to them."""
+    desc = L.SynthDesc(n, d, components, seed, role, kind, center_scale, center_lo, center_hi,
+                       sigma, int(decay), assign_mode, threads)
+    if out is None:
+        out = np.empty((count, d), np.float32)
+    if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < count * d:
+        raise ValueError("synth_rows: out must be a contiguous float32 array of count x d")
+    check(L.ads_synth_rows(C.byref(desc), row_lo, count, stride, out.ctypes.data, None))
+    return out
+
+
 # ---------------------------------------------------------------- transform (GPU)
 
 
@@ -612,6 +628,20 @@ class IvfIndex:
         return {"queries": int(v[0]), "rescored": int(v[1]), "fallbacks": int(v[2])}
 
 
+def save_ivf(idx: IvfIndex, path) -> None:  # ivf.hpp:91, ivf.cpp:423-440
+    """The reference's on-disk index format (meta.txt + fvecs / ragged ivecs)."""
+    check(L.ads_ivf_save(idx.h, str(path).encode()))
+
+
+def load_ivf(path, m: Optional[TransformMatrix] = None, ctx: Optional[Context] = None) -> IvfIndex:
+    """ivf.hpp:92, ivf.cpp:442-501.  m (optional) enables on-device query rotation."""
+    ctx = ctx or Context.default()
+    P = None if m is None else np.ascontiguousarray(m.entries, np.float64)
+    h = C.c_void_p()
+    check(L.ads_ivf_load(ctx.h, str(path).encode(), _ptr(P), C.byref(h)))
+    return IvfIndex(h, ctx)
+
+
 def build_ivf(ds_raw: np.ndarray, ds_transformed: np.ndarray, m: TransformMatrix, k_clusters: int,
               seed: int, layout: IvfLayout = IvfLayout.kContiguous, d1: int = 32,
               max_iters: int = 25, init: int = 0, ctx: Optional[Context] = None) -> IvfIndex:
@@ -646,6 +676,137 @@ def build_ivf_sampled_device(dT: "DeviceArray", m: TransformMatrix, k_clusters: 
     check(L.ads_ivf_build_sampled_device(ctx.h, C.c_void_p(dT.ptr), n, d, P.ctypes.data, k_clusters, seed, d1,
                                          max_iters, min(sample, n), C.byref(h)))
     return IvfIndex(h, ctx)
+
+
+class IvfBuilder:
+    """build_ivf fed in row chunks (ads_ivf_builder; ivf.cpp:192-258): k-means on a
+    sample (or given centroids), every row assigned by the certified exact argmin,
+    and the bucket layout of the lists a shard keeps."""
+
+    def __init__(self, n: int, d: int, m: TransformMatrix, k_clusters: int, seed: int, d1: int = 32,
+                 ctx: Optional[Context] = None):
+        if m.dim != d:
+            raise ValueError("build_ivf: matrix dimension does not match the data")
+        self.ctx = ctx or Context.default()
+        self.n, self.d, self.k_clusters = n, d, k_clusters
+        P = np.ascontiguousarray(m.entries, np.float64)
+        self.h = C.c_void_p()
+        check(L.ads_ivf_builder_create(self.ctx.h, n, d, P.ctypes.data, k_clusters, seed, d1,
+                                       C.byref(self.h)))
+
+    def __del__(self):
+        try:
+            if self.h:
+                L.ads_ivf_builder_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def close(self):
+        self.__del__()
+
+    def train_device(self, dS: "DeviceArray", max_iters: int) -> None:
+        check(L.ads_ivf_builder_train_device(self.h, C.c_void_p(dS.ptr), dS.shape[0], max_iters))
+
+    def set_centroids(self, centroids: np.ndarray) -> None:
+        c = _f32(centroids)
+        if c.shape != (self.k_clusters, self.d):
+            raise ValueError("build_ivf: centroids must be k x d")
+        check(L.ads_ivf_builder_set_centroids(self.h, c.ctypes.data))
+
+    def centroids(self) -> np.ndarray:
+        out = np.empty((self.k_clusters, self.d), np.float32)
+        check(L.ads_ivf_builder_centroids(self.h, out.ctypes.data))
+        return out
+
+    def add_device(self, dT: "DeviceArray", row_lo: int, rows: Optional[int] = None) -> None:
+        rows = dT.shape[0] if rows is None else rows
+        check(L.ads_ivf_builder_add_device(self.h, C.c_void_p(dT.ptr), row_lo, rows))
+
+    def rows_device(self) -> int:
+        """Device pointer of the staged transformed rows (n x d by id), valid until close()."""
+        p = C.c_void_p()
+        check(L.ads_ivf_builder_rows_device(self.h, C.byref(p)))
+        return p.value
+
+    def list_sizes(self) -> np.ndarray:
+        out = np.empty(self.k_clusters, np.int64)
+        check(L.ads_ivf_builder_list_sizes(self.h, out.ctypes.data))
+        return out
+
+    def finish(self, keep: Optional[np.ndarray] = None) -> IvfIndex:
+        h = C.c_void_p()
+        kp = None if keep is None else np.ascontiguousarray(keep, np.uint8)
+        if kp is not None and kp.shape != (self.k_clusters,):
+            raise ValueError("build_ivf: keep must have one entry per list")
+        check(L.ads_ivf_builder_finish(self.h, _ptr(kp), C.byref(h)))
+        return IvfIndex(h, self.ctx)
+
+
+def build_ivf_streamed(rows, n: int, d: int, m: TransformMatrix, k_clusters: int, seed: int,
+                       d1: int = 32, max_iters: int = 10, sample: int = 2_000_000, chunk: int = 4_000_000,
+                       owner=None, rank: int = 0, centroids: Optional[np.ndarray] = None,
+                       on_rows=None, ctx: Optional[Context] = None):
+    """build_ivf over raw rows produced piecewise by rows(row_lo, count, stride) -> float32
+    (count x d host array): the sample rows (every n // sample-th) are rotated on the device
+    and clustered (or `centroids` are used), then every chunk is generated on a host thread
+    while the previous one is rotated (exact fp64 apply) and assigned on the GPU.  owner:
+    callable(list_sizes) -> owner rank per list (list sharding; None keeps every list).
+    on_rows(ptr): called with the device pointer of all n transformed rows (by id) before
+    they are released (e.g. for an exact ground truth).  Returns (index, list_sizes,
+    centroids)."""
+    import threading as _th
+
+    ctx = ctx or Context.default()
+    tr = Transform(m, ctx)
+    b = IvfBuilder(n, d, m, k_clusters, seed, d1, ctx)
+    try:
+        if centroids is None:
+            sample = min(sample, n)
+            stride = n // sample
+            xs = rows(0, sample, stride)
+            dS = DeviceArray.from_host(ctx, xs)
+            dSt = DeviceArray(ctx, (sample, d), np.float32)
+            tr.apply_dataset_device(dS, dSt)
+            del xs
+            dS.free()
+            b.train_device(dSt, max_iters)
+            dSt.free()
+        else:
+            b.set_centroids(centroids)
+        chunk = max(1, min(chunk, n))
+        dX = DeviceArray(ctx, (chunk, d), np.float32)
+        dY = DeviceArray(ctx, (chunk, d), np.float32)
+        nxt = {}
+
+        def produce(lo):
+            nxt[lo] = rows(lo, min(chunk, n - lo), 1)
+
+        th = _th.Thread(target=produce, args=(0,))
+        th.start()
+        for lo in range(0, n, chunk):
+            th.join()
+            host = nxt.pop(lo)
+            if lo + chunk < n:
+                th = _th.Thread(target=produce, args=(lo + chunk,))
+                th.start()
+            cnt = host.shape[0]
+            check(L.ads_memcpy_h2d(ctx.h, C.c_void_p(dX.ptr), host.ctypes.data, host.nbytes))
+            check(L.ads_apply_dataset_device(tr.h, C.c_void_p(dX.ptr), cnt, C.c_void_p(dY.ptr)))
+            b.add_device(dY, lo, cnt)
+        ctx.sync()
+        dX.free()
+        dY.free()
+        sizes = b.list_sizes()
+        if on_rows is not None:
+            on_rows(b.rows_device())
+        keep = None
+        if owner is not None:
+            keep = (np.asarray(owner(sizes)) == rank).astype(np.uint8)
+        cent = b.centroids()
+        return b.finish(keep), sizes, cent
+    finally:
+        b.close()
 
 
 @dataclass

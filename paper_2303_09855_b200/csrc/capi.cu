@@ -22,6 +22,8 @@
 
 namespace ads {
 void synth(const ads_synth_desc& s, float* out, int32_t* comp_out);
+void synth_rows(const ads_synth_desc& s, int64_t row_lo, int64_t count, int64_t stride, float* out,
+                int32_t* comp_out);
 
 int num_sms() {
     int dev = 0;
@@ -60,6 +62,14 @@ int guard(F&& f) {
     }
 }
 
+}  // namespace
+
+namespace ads {
+// for the host-only translation units (ivf_io.cpp) that report through ads_last_error
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace ads
+
+namespace {
 void require(bool ok, const char* msg) {
     if (!ok) throw std::invalid_argument(msg);
 }
@@ -220,6 +230,11 @@ int ads_ad_context(double eps0, int32_t delta_d, int32_t dim, double* factor_out
 
 int ads_synth(const ads_synth_desc* desc, float* out, int32_t* comp_out) {
     return guard([&] { synth(*desc, out, comp_out); });
+}
+
+int ads_synth_rows(const ads_synth_desc* desc, int64_t row_lo, int64_t count, int64_t stride, float* out,
+                   int32_t* comp_out) {
+    return guard([&] { synth_rows(*desc, row_lo, count, stride, out, comp_out); });
 }
 
 // ------------------------------------------------------------------ context
@@ -957,54 +972,210 @@ int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int
     });
 }
 
-int ads_ivf_build_sampled_device(ads_ctx* ctx, const float* dT, int64_t n, int32_t d, const double* P, int32_t k,
-                                 uint64_t seed, int32_t d1, int32_t max_iters, int64_t sample, ads_ivf** out) {
+// ------------------------------------------------------------------ streamed build
+// build_ivf (ivf.cpp:192-258) for data that arrives in row chunks (config 5):
+// k-means on a sample (train) or given centroids, every added row assigned to its
+// nearest centroid by the certified coarse prefilter at nprobe = 1 (the exact fp64
+// argmin, lowest id on ties, as kmeans assigns), and at finish the bucket layout of
+// the lists a shard keeps (ascending ids per list, split at d1).
+struct ads_ivf_builder {
+    ads_ctx* ctx = nullptr;
+    int64_t n = 0, added = 0;
+    int d = 0, k = 0, d1 = 0;
+    uint64_t seed = 0;
+    std::vector<double> P;
+    float* cent = nullptr;  // k x d, device
+    bool trained = false;
+    DevBuf rows, asg;       // staged rows (n x d) and their lists (n)
+    CoarseCentroids cc;
+    CoarseScratch coarse;
+    ~ads_ivf_builder() {
+        if (cent) cudaFree(cent);
+        cc.release();
+    }
+};
+
+static void builder_prefilter(ads_ivf_builder* b) {
+    b->cc.release();
+    centroid_prefilter(b->cent, b->k, b->d, b->cc, b->ctx->stream);
+    b->trained = true;
+}
+
+int ads_ivf_builder_create(ads_ctx* ctx, int64_t n, int32_t d, const double* P, int32_t k, uint64_t seed,
+                           int32_t d1, ads_ivf_builder** out) {
     return guard([&] {
         require(n >= 1 && n <= 0x7fffffff && d >= 1, "build_ivf: bad shape");
         require(P != nullptr, "build_ivf: matrix dimension does not match the data");
         require(d1 >= 1 && d1 < d, "build_ivf: split layout needs 1 <= d1 < D");
-        require(k >= 1 && sample >= k && sample <= n, "build_ivf: need 1 <= k <= sample <= n");
+        require(k >= 1 && k <= n, "kmeans: k exceeds the number of points");
+        ctx->use();
+        auto b = std::make_unique<ads_ivf_builder>();
+        b->ctx = ctx;
+        b->n = n;
+        b->d = d;
+        b->k = k;
+        b->d1 = d1;
+        b->seed = seed;
+        b->P.assign(P, P + static_cast<size_t>(d) * d);
+        ADS_CUDA(cudaMalloc(&b->cent, sizeof(float) * k * static_cast<size_t>(d)));
+        *out = b.release();
+    });
+}
+
+int ads_ivf_builder_train_device(ads_ivf_builder* b, const float* dS, int64_t sample, int32_t max_iters) {
+    return guard([&] {
+        require(sample >= b->k && sample <= b->n, "build_ivf: need 1 <= k <= sample <= n");
+        b->ctx->use();
+        DevBuf dsa;
+        (void)run_kmeans(dS, sample, b->d, b->k, max_iters, b->seed, 1, b->cent, dsa.get<int32_t>(sample),
+                         b->ctx->stream);
+        builder_prefilter(b);
+        ADS_CUDA(cudaStreamSynchronize(b->ctx->stream));
+    });
+}
+
+int ads_ivf_builder_set_centroids(ads_ivf_builder* b, const float* centroids) {
+    return guard([&] {
+        b->ctx->use();
+        ADS_CUDA(cudaMemcpyAsync(b->cent, centroids, sizeof(float) * b->k * static_cast<size_t>(b->d),
+                                 cudaMemcpyHostToDevice, b->ctx->stream));
+        builder_prefilter(b);
+        ADS_CUDA(cudaStreamSynchronize(b->ctx->stream));
+    });
+}
+
+int ads_ivf_builder_centroids(ads_ivf_builder* b, float* centroids) {
+    return guard([&] {
+        require(b->trained, "build_ivf: no centroids yet (train or set them first)");
+        b->ctx->use();
+        ADS_CUDA(cudaMemcpyAsync(centroids, b->cent, sizeof(float) * b->k * static_cast<size_t>(b->d),
+                                 cudaMemcpyDeviceToHost, b->ctx->stream));
+        ADS_CUDA(cudaStreamSynchronize(b->ctx->stream));
+    });
+}
+
+int ads_ivf_builder_add_device(ads_ivf_builder* b, const float* dT, int64_t row_lo, int64_t rows) {
+    return guard([&] {
+        require(b->trained, "build_ivf: no centroids yet (train or set them first)");
+        require(row_lo == b->added && rows >= 0 && row_lo + rows <= b->n,
+                "build_ivf: rows must be added in order, without gaps, inside [0, n)");
+        b->ctx->use();
+        cudaStream_t st = b->ctx->stream;
+        const size_t D = b->d;
+        float* R = b->rows.get<float>(static_cast<size_t>(b->n) * D);
+        int32_t* A = b->asg.get<int32_t>(static_cast<size_t>(b->n));
+        ADS_CUDA(cudaMemcpyAsync(R + row_lo * D, dT, sizeof(float) * rows * D, cudaMemcpyDeviceToDevice, st));
+        const int64_t chunk = 65536;
+        for (int64_t r = 0; r < rows; r += chunk) {
+            const int m = static_cast<int>(rows - r < chunk ? rows - r : chunk);
+            launch_coarse_probes_fast(dT + r * D, m, b->cent, b->k, b->d, 1, b->cc, b->coarse, A + row_lo + r, 0,
+                                      st);
+        }
+        b->added += rows;
+    });
+}
+
+int ads_ivf_builder_rows_device(ads_ivf_builder* b, const float** rows) {
+    return guard([&] {
+        require(b->added == b->n, "build_ivf: not every row has been added");
+        *rows = static_cast<const float*>(b->rows.p);
+    });
+}
+
+int ads_ivf_builder_list_sizes(ads_ivf_builder* b, int64_t* sizes) {
+    return guard([&] {
+        require(b->added == b->n, "build_ivf: not every row has been added");
+        b->ctx->use();
+        cudaStream_t st = b->ctx->stream;
+        DevBuf off, ids;
+        int64_t* o = off.get<int64_t>(b->k + 1);
+        build_lists(static_cast<int32_t*>(b->asg.p), b->n, b->k, o, ids.get<int32_t>(b->n), st);
+        std::vector<int64_t> h(static_cast<size_t>(b->k) + 1);
+        ADS_CUDA(cudaMemcpyAsync(h.data(), o, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        for (int c = 0; c < b->k; ++c) sizes[c] = h[c + 1] - h[c];
+    });
+}
+
+int ads_ivf_builder_finish(ads_ivf_builder* b, const uint8_t* keep, ads_ivf** out) {
+    return guard([&] {
+        require(b->added == b->n, "build_ivf: not every row has been added");
+        ads_ctx* ctx = b->ctx;
         ctx->use();
         cudaStream_t st = ctx->stream;
+        const int k = b->k, d = b->d, d1 = b->d1;
         auto x = std::make_unique<ads_ivf>();
         x->ctx = ctx;
-        x->n = static_cast<int>(n);
         x->d = d;
         x->k = k;
         x->d1 = d1;
         x->layout = 1;
-        x->seed = seed;
-        ivf_alloc_common(x.get());
+        x->seed = b->seed;
         x->d1p = d1;
-        const size_t N = static_cast<size_t>(n);
-        x->P = dev_upload(P, static_cast<size_t>(d) * d, st);
+        ivf_alloc_common(x.get());
+        x->P = dev_upload(b->P.data(), b->P.size(), st);
         ADS_CUDA(cudaMalloc(&x->cent_t, sizeof(float) * k * static_cast<size_t>(d)));
-        // k-means on every (n / sample)-th row (seeded sample init, Lloyd iterations)
-        const int64_t stride = n / sample;
-        DevBuf ds, dsa, dasg;
-        float* S = ds.get<float>(static_cast<size_t>(sample) * d);
-        ADS_CUDA(cudaMemcpy2DAsync(S, sizeof(float) * d, dT, sizeof(float) * d * stride, sizeof(float) * d,
-                                   static_cast<size_t>(sample), cudaMemcpyDeviceToDevice, st));
-        (void)run_kmeans(S, sample, d, k, max_iters, seed, 1, x->cent_t, dsa.get<int32_t>(sample), st);
-        ds.release();
-        // every row to its nearest centroid: the certified coarse prefilter at
-        // nprobe = 1 (exact fp64 argmin, lowest id on ties, as kmeans assigns)
-        centroid_prefilter(x->cent_t, k, d, x->cc_t, st);
-        int32_t* asg = dasg.get<int32_t>(N);
-        const int64_t chunk = 65536;
-        for (int64_t r = 0; r < n; r += chunk) {
-            const int rows = static_cast<int>(n - r < chunk ? n - r : chunk);
-            launch_coarse_probes_fast(dT + r * d, rows, x->cent_t, k, d, 1, x->cc_t, x->coarse, asg + r, 0, st);
+        ADS_CUDA(cudaMemcpyAsync(x->cent_t, b->cent, sizeof(float) * k * static_cast<size_t>(d),
+                                 cudaMemcpyDeviceToDevice, st));
+        const int32_t* A = static_cast<int32_t*>(b->asg.p);
+        DevBuf masked, kd, off, ids;
+        int kk = k;
+        if (keep) {  // lists this shard does not own go to bucket k, after every owned row
+            std::vector<uint8_t> hk(keep, keep + k);
+            int32_t* M = masked.get<int32_t>(b->n);
+            mask_assignment(A, b->n, buf_upload(kd, hk.data(), hk.size(), st), k, M, st);
+            A = M;
+            kk = k + 1;
         }
-        ADS_CUDA(cudaMalloc(&x->list_off, sizeof(int64_t) * (k + 1)));
-        ADS_CUDA(cudaMalloc(&x->ids, sizeof(int32_t) * N));
-        build_lists(asg, n, k, x->list_off, x->ids, st);
-        alloc_split_pair(N, d1, d - d1, &x->a1_t, &x->a2_t);
-        gather_split(dT, x->ids, n, d, d1, x->a1_t, x->a2_t, st);
-        x->coarse.release();  // the assignment-sized scratch
+        int64_t* o = off.get<int64_t>(kk + 1);
+        int32_t* I = ids.get<int32_t>(b->n);
+        build_lists(A, b->n, kk, o, I, st);
+        std::vector<int64_t> h(static_cast<size_t>(kk) + 1);
+        ADS_CUDA(cudaMemcpyAsync(h.data(), o, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        const int64_t m = h[k];  // rows in kept lists
+        x->n = static_cast<int>(m);
+        x->list_off = dev_upload(h.data(), static_cast<size_t>(k) + 1, st);
+        const size_t mm = static_cast<size_t>(m > 0 ? m : 1);
+        ADS_CUDA(cudaMalloc(&x->ids, sizeof(int32_t) * mm));
+        ADS_CUDA(cudaMemcpyAsync(x->ids, I, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, st));
+        alloc_split_pair(mm, d1, d - d1, &x->a1_t, &x->a2_t);
+        gather_split(static_cast<float*>(b->rows.p), I, m, d, d1, x->a1_t, x->a2_t, st);
+        ivf_finish_coarse(x.get(), st);
         ADS_CUDA(cudaStreamSynchronize(st));
         *out = x.release();
     });
+}
+
+int ads_ivf_builder_destroy(ads_ivf_builder* b) {
+    return guard([&] {
+        if (!b) return;
+        b->ctx->use();
+        cudaStreamSynchronize(b->ctx->stream);
+        delete b;
+    });
+}
+
+int ads_ivf_build_sampled_device(ads_ctx* ctx, const float* dT, int64_t n, int32_t d, const double* P, int32_t k,
+                                 uint64_t seed, int32_t d1, int32_t max_iters, int64_t sample, ads_ivf** out) {
+    // The streamed builder fed in one piece: k-means on every (n / sample)-th row.
+    ads_ivf_builder* b = nullptr;
+    int rc = guard([&] { require(sample >= k && sample <= n, "build_ivf: need 1 <= k <= sample <= n"); });
+    if (!rc) rc = ads_ivf_builder_create(ctx, n, d, P, k, seed, d1, &b);
+    if (rc) return rc;
+    DevBuf ds;
+    rc = guard([&] {
+        const int64_t stride = n / sample;
+        float* S = ds.get<float>(static_cast<size_t>(sample) * d);
+        ADS_CUDA(cudaMemcpy2DAsync(S, sizeof(float) * d, dT, sizeof(float) * d * stride, sizeof(float) * d,
+                                   static_cast<size_t>(sample), cudaMemcpyDeviceToDevice, ctx->stream));
+    });
+    if (!rc) rc = ads_ivf_builder_train_device(b, static_cast<float*>(ds.p), sample, max_iters);
+    ds.release();
+    if (!rc) rc = ads_ivf_builder_add_device(b, dT, 0, n);
+    if (!rc) rc = ads_ivf_builder_finish(b, nullptr, out);
+    ads_ivf_builder_destroy(b);
+    return rc;
 }
 
 int ads_ivf_destroy(ads_ivf* idx) {

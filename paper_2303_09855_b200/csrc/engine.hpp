@@ -239,6 +239,9 @@ void build_lists(const int32_t* dAssign, int64_t n, int k, int64_t* dListOff, in
                  cudaStream_t st);
 void gather_split(const float* src, const int32_t* dIds, int64_t n, int D, int d1, float* a1,
                   float* a2, cudaStream_t st);
+// out[i] = keep[asg[i]] ? asg[i] : k (lists a shard does not own sort after every owned one).
+void mask_assignment(const int32_t* dAssign, int64_t n, const uint8_t* dKeep, int k, int32_t* dOut,
+                     cudaStream_t st);
 
 // Per query, K smallest (dist, id) pairs among G lists of K ([G][nq][K]).
 void launch_merge_topk(const double* dists, const int32_t* ids, int G, int nq, int K,

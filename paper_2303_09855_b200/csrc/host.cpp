@@ -154,9 +154,17 @@ constexpr uint64_t kTagNoise = 0x4e4f495345303031ULL;    // "NOISE001"
 
 namespace ads {
 
-void synth(const ads_synth_desc& s, float* out, int32_t* comp_out) {
+// Rows row_lo + i*stride (i < count) of the mixture whose full size is s.n:
+// row r's component draw is counter r of the component stream and its noise is
+// normals r*d .. r*d+d-1 of the noise stream, so any row set is reproducible
+// without generating the rows before it (config 5 is generated in chunks, and
+// its k-means sample directly).
+void synth_rows(const ads_synth_desc& s, int64_t row_lo, int64_t count, int64_t stride, float* out,
+                int32_t* comp_out) {
     if (s.n < 0 || s.d < 1 || s.components < 1) throw std::invalid_argument("synth: bad shape");
     if (!(s.sigma >= 0.0)) throw std::invalid_argument("synth: sigma must be >= 0");
+    if (count < 0 || stride < 1 || row_lo < 0 || (count > 0 && row_lo + (count - 1) * stride >= s.n))
+        throw std::invalid_argument("synth: row range outside [0, n)");
     const int d = s.d, C = s.components;
     // Centers: one sequential stream per seed (shared by every role).
     std::vector<double> centers(static_cast<size_t>(C) * d);
@@ -173,16 +181,21 @@ void synth(const ads_synth_desc& s, float* out, int32_t* comp_out) {
     const uint64_t role_seed = HostRng::mix64(s.seed ^ (s.role * 0x9E3779B97F4A7C15ULL + 1));
     int nt = s.threads > 0 ? s.threads : static_cast<int>(std::thread::hardware_concurrency());
     nt = std::max(1, std::min<int>(nt, 64));
-    if (s.n < 4096) nt = 1;
-    auto work = [&](int64_t lo, int64_t hi) {
-        // comp draws one u64 per row; noise draws d normals per row.
-        HostRng comp(HostRng::mix64(role_seed ^ kTagComp), static_cast<uint64_t>(lo));
-        HostRng noise = HostRng::for_stream(role_seed, kTagNoise);
-        noise.seek_normal(static_cast<uint64_t>(lo) * d);
+    if (count < 4096) nt = 1;
+    auto work = [&](int64_t lo, int64_t hi) {  // output slots [lo, hi)
         std::vector<double> row(d);
+        HostRng comp(HostRng::mix64(role_seed ^ kTagComp), 0);
+        HostRng noise = HostRng::for_stream(role_seed, kTagNoise);
+        int64_t next_row = -1;  // the row both streams are positioned at
         for (int64_t i = lo; i < hi; ++i) {
+            const int64_t r = row_lo + i * stride;
+            if (r != next_row) {
+                comp = HostRng(HostRng::mix64(role_seed ^ kTagComp), static_cast<uint64_t>(r));
+                noise.seek_normal(static_cast<uint64_t>(r) * d);
+            }
+            next_row = r + 1;
             int32_t c;
-            if (s.assign_mode == 1) c = static_cast<int32_t>((i * C) / (s.n > 0 ? s.n : 1));
+            if (s.assign_mode == 1) c = static_cast<int32_t>((r * C) / (s.n > 0 ? s.n : 1));
             else c = static_cast<int32_t>(comp.below(static_cast<uint64_t>(C)));
             if (comp_out) comp_out[i] = c;
             const double* cc = centers.data() + static_cast<size_t>(c) * d;
@@ -204,15 +217,17 @@ void synth(const ads_synth_desc& s, float* out, int32_t* comp_out) {
         }
     };
     if (nt == 1) {
-        work(0, s.n);
+        work(0, count);
         return;
     }
     std::vector<std::thread> th;
     for (int t = 0; t < nt; ++t) {
-        const int64_t lo = s.n * t / nt, hi = s.n * (t + 1) / nt;
+        const int64_t lo = count * t / nt, hi = count * (t + 1) / nt;
         th.emplace_back(work, lo, hi);
     }
     for (auto& x : th) x.join();
 }
+
+void synth(const ads_synth_desc& s, float* out, int32_t* comp_out) { synth_rows(s, 0, s.n, 1, out, comp_out); }
 
 }  // namespace ads

@@ -362,6 +362,23 @@ void build_lists(const int32_t* dAssign, int64_t n, int k, int64_t* dListOff, in
     ADS_LAUNCH_CHECK();
 }
 
+namespace {
+__global__ void mask_assignment_kernel(const int32_t* __restrict__ asg, int64_t n,
+                                       const uint8_t* __restrict__ keep, int k, int32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int32_t c = asg[i];
+    out[i] = keep[c] ? c : k;
+}
+}  // namespace
+
+void mask_assignment(const int32_t* dAssign, int64_t n, const uint8_t* dKeep, int k, int32_t* dOut,
+                     cudaStream_t st) {
+    if (n <= 0) return;
+    mask_assignment_kernel<<<blocks_for(n, 256), 256, 0, st>>>(dAssign, n, dKeep, k, dOut);
+    ADS_LAUNCH_CHECK();
+}
+
 void gather_split(const float* src, const int32_t* dIds, int64_t n, int D, int d1, float* a1,
                   float* a2, cudaStream_t st) {
     if (n <= 0) return;

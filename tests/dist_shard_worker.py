@@ -1,7 +1,8 @@
 """One rank of the 2-process gloo test of the list-sharded search (CPU).
 Per-rank search runs on the oracle (test infrastructure); the product pieces
 under test are the partition (shard.partition_lists), the restricted-stream
-semantics of a shard and the all-gather -> (dist, id) merge contract."""
+semantics of a shard, and the orchestration of the product's sharded step
+(shard.ShardedIvf: two waves, all-reduce of the bound, all-gather, merge)."""
 import os
 import sys
 
@@ -36,23 +37,21 @@ def run(rank, world, port, outdir):
     dist.all_gather(gd, torch.from_numpy(dists))
     all_ids = np.stack([x.numpy() for x in gi])
     all_d = np.stack([x.numpy() for x in gd])
-    # the threshold exchange (bench.py's list-sharded step for N > 1): wave 1 over probe
-    # ranks [0, w), all-reduce (min) of the K-th distances, wave 2 over [w, nprobe) from it
-    from shard_helpers import kth_distance
+    # the product's list-sharded step (shard.ShardedIvf: wave 1 over probe ranks [0, w),
+    # all-reduce (min) of the K-th distances, wave 2 over [w, nprobe) from that bound,
+    # all-gather + merge), driven here with gloo and an oracle-backed per-rank search
+    from paper_2303_09855_b200.shard import ShardedIvf
+    from shard_helpers import OracleShardSearch
 
-    w = 3
-    i1, d1, m1 = shard_search_oracle(orc, sub, qt, qr, K, w, "ad-split", K, 64)
-    R = torch.from_numpy(kth_distance(d1, K))
-    dist.all_reduce(R, op=dist.ReduceOp.MIN)
-    i2, d2, m2 = shard_search_oracle(orc, sub, qt, qr, K, nprobe, "ad-split", K, 64, probe_lo=w, r0=R.numpy())
-    wi = [torch.zeros((2,) + ids.shape, dtype=torch.int32) for _ in range(world)]
-    wd = [torch.zeros((2,) + dists.shape, dtype=torch.float64) for _ in range(world)]
-    dist.all_gather(wi, torch.from_numpy(np.stack([i1, i2])))
-    dist.all_gather(wd, torch.from_numpy(np.stack([d1, d2])))
+    be = OracleShardSearch(orc, sub, qt, qr, K, K, 64)
+    one = ShardedIvf(be, qt.shape[0], qt.shape[1], K, nprobe, world, rank, dist.group.WORLD, waves=0)
+    one.step(None)
+    two = ShardedIvf(be, qt.shape[0], qt.shape[1], K, nprobe, world, rank, dist.group.WORLD, waves=3)
+    two.step(None)
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), ids=all_ids, dists=all_d, owner=owner,
-             dims=dims, R=R.numpy(), wave_ids=np.stack([x.numpy() for x in wi]).reshape(-1, *ids.shape),
-             wave_dists=np.stack([x.numpy() for x in wd]).reshape(-1, *dists.shape),
-             wave_dims=m1 + m2)
+             dims=dims, R=two.rb.numpy(), wave_ids=two.gi.numpy(), wave_dists=two.gd.numpy(),
+             wave_dims=two.lm.numpy().sum(axis=0), one_ids=one.oi.numpy(), one_dists=one.od.numpy(),
+             two_ids=two.oi.numpy(), two_dists=two.od.numpy())
     dist.barrier()
     dist.destroy_process_group()
 

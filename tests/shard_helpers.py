@@ -50,3 +50,33 @@ def kth_distance(dists, K):
     """Per-query K-th distance of a local top-K (+inf when fewer than K were found)."""
     d = dists[:, K - 1]
     return np.where(np.isnan(d), np.inf, d)
+
+
+class OracleShardSearch:
+    """ShardedIvf backend on the CPU: the oracle's restricted searches on a numpy shard
+    and the (dist, id) reference merge (test infrastructure for the gloo tests)."""
+
+    def __init__(self, orc, lay, qt, qr, K, first, step, mode="ad-split"):
+        self.orc, self.lay, self.qt, self.qr = orc, lay, qt, qr
+        self.K, self.first, self.step, self.mode = K, first, step, mode
+
+    def search(self, dq, nq, nprobe, probe_lo, r0, out):
+        import torch
+
+        ids, dists, dims = shard_search_oracle(self.orc, self.lay, self.qt, self.qr, self.K, nprobe,
+                                               self.mode, self.first, self.step, probe_lo=probe_lo,
+                                               r0=None if r0 is None else r0.numpy())
+        o_ids, o_d, o_c, o_m, o_n = out
+        o_ids.copy_(torch.from_numpy(ids))
+        o_d.copy_(torch.from_numpy(dists))
+        o_c.copy_(torch.from_numpy((ids >= 0).sum(axis=1).astype(np.int32)))
+        o_m.copy_(torch.from_numpy(dims.astype(np.int64)))
+        o_n.zero_()
+
+    def merge(self, gd, gi, G, nq, oi, od, oc):
+        import torch
+
+        mi, md = merge_ref(gd.numpy(), gi.numpy(), self.K)
+        oi.copy_(torch.from_numpy(mi))
+        od.copy_(torch.from_numpy(md))
+        oc.copy_(torch.from_numpy((mi >= 0).sum(axis=1).astype(np.int32)))

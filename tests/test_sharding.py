@@ -70,6 +70,25 @@ def test_two_rank_gloo_sharded_search(tmp_path, orc):
     np.testing.assert_array_equal(r0["R"], r1["R"])
     np.testing.assert_array_equal(r0["wave_ids"], r1["wave_ids"])
     ex_i, ex_d = merge_ref(r0["wave_dists"], r0["wave_ids"], 10)
+    # ShardedIvf's merged outputs, identical on both ranks: one wave == the plain merge,
+    # two waves == the merge of the gathered wave lists (recomputed here from the
+    # oracle's restricted searches with the all-reduced bound)
+    for r in (r0, r1):
+        np.testing.assert_array_equal(r["one_ids"], merged_i)
+        np.testing.assert_array_equal(r["two_ids"], ex_i)
+        np.testing.assert_array_equal(np.nan_to_num(r["two_dists"], nan=-1), np.nan_to_num(ex_d, nan=-1))
+    R = np.full(qt.shape[0], np.inf)
+    for rank in range(world):
+        _, d1w, _ = shard_search_oracle(orc, numpy_subset(lay, owner, rank), qt, qr, 10, 3, "ad-split", 10, 64)
+        R = np.minimum(R, np.where(np.isnan(d1w[:, 9]), np.inf, d1w[:, 9]))
+    np.testing.assert_array_equal(r0["R"], R)
+    exp_w = []
+    for rank in range(world):
+        sub = numpy_subset(lay, owner, rank)
+        a1, b1, _ = shard_search_oracle(orc, sub, qt, qr, 10, 3, "ad-split", 10, 64)
+        a2, b2, _ = shard_search_oracle(orc, sub, qt, qr, 10, 12, "ad-split", 10, 64, probe_lo=3, r0=R)
+        exp_w += [a1, a2]
+    np.testing.assert_array_equal(r0["wave_ids"], np.stack(exp_w))
     full = ~np.isnan(ex_d[:, -1])
     assert (ex_d[full, -1] <= r0["R"][full]).all()
     assert rec(ex_i) >= rec(merged_i) - 0.02
