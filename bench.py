@@ -216,6 +216,24 @@ def workload_config(cfg, nprobe) -> dict:
                 l2=f"flushed between timed steps; index {cfg.n * cfg.d * 4 / 1e9:.2f} GB vs 126 MB L2")
 
 
+def nvtx_push(name):
+    try:
+        import torch
+
+        torch.cuda.nvtx.range_push(name)
+    except Exception:
+        pass
+
+
+def nvtx_pop():
+    try:
+        import torch
+
+        torch.cuda.nvtx.range_pop()
+    except Exception:
+        pass
+
+
 def is_large(cfg) -> bool:
     return cfg.n > 20_000_000
 
@@ -336,6 +354,7 @@ def measure(S, cfg, nprobe, args, D, log, steps):
     D.barrier()
     ctx.sync()
     clocks.start()
+    nvtx_push("timed")  # ncu --nvtx --nvtx-include timed/ captures exactly these launches
     for _ in range(steps):
         ctx.flush_l2()  # L2 flushed between timed steps (outside the events)
         ctx.timer_start()
@@ -345,6 +364,7 @@ def measure(S, cfg, nprobe, args, D, log, steps):
         stage_ms.append(st)
         scan_ms.append(float(st[3]))
     ctx.sync()
+    nvtx_pop()
     clk = clocks.stop()
     D.barrier()
     total_ms = D.allmax(float(np.sum(step_ms)))
@@ -621,6 +641,7 @@ def run_sharded(args, D):
     ctx.sync()
     clocks.start()
     ms = []
+    nvtx_push("timed")
     for _ in range(args.steps):
         ctx.flush_l2()
         ctx.sync()
@@ -628,6 +649,7 @@ def run_sharded(args, D):
         ctx.timer_start()
         Sh.step(dq, raw=True)
         ms.append(ctx.timer_stop())
+    nvtx_pop()
     clk = clocks.stop()
     total_ms = D.allmax(float(np.sum(ms)))
     dims = D.allsum(float(Sh.dims_evaluated()))

@@ -156,6 +156,14 @@ typedef struct {
 } ads_dco_batch;
 int ads_dco_fixed(ads_ctx *ctx, const ads_dco_batch *b);
 int ads_dco_fixed_device(ads_ctx *ctx, const ads_dco_batch *b);
+/* The partial squared distances every DCO kind tests, for a batch of rows against one
+ * query: dout[c * nb + t] = S_{min((t+1) delta_d, dim)} of row dcand[c] (nb =
+ * ceil(dim / delta_d)), fp64 in the reference's order (dco.hpp:122-177).  A caller whose
+ * threshold changes between comparisons (the HNSW beam search, hnsw.cpp:214-243, where
+ * r moves after every neighbour) replays ad_scan / pd_scan_kernel / l2_sq decisions
+ * from them exactly.  Device pointers, enqueued on the context's stream. */
+int ads_dco_prefix_sums_device(ads_ctx *ctx, const float *dX, int64_t n_rows, int32_t dim, const float *dq,
+                               const int64_t *dcand, int32_t nc, int32_t delta_d, double *dout);
 /* Validated single DCO: fd_scan / pd_scan / ad_sampling, dco.hpp:69-71, dco.cpp:70-110.
  * distance is NaN when the outcome is negative (std::optional empty). */
 int ads_dco(ads_ctx *ctx, int32_t kind, const float *o, int32_t n_o, const float *q, int32_t n_q,

@@ -428,6 +428,16 @@ class RefLib(_Common):
         self._fn("ref_ivf_from_split_layout", [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
                                                _f32p, _i64p, _i32p, _f32p, _f32p], _vp)
         self._fn("ref_ivf_free", [_vp], None)
+        L = self.lib
+        L.ref_hnsw_build.argtypes = [_f32p, _f32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64]
+        L.ref_hnsw_build.restype = _vp
+        L.ref_hnsw_load.argtypes = [C.c_char_p, _f32p, _f32p, C.c_int32, C.c_int32]
+        L.ref_hnsw_load.restype = _vp
+        L.ref_hnsw_save.argtypes = [_vp, C.c_char_p]
+        L.ref_hnsw_free.argtypes = [_vp]
+        L.ref_hnsw_free.restype = None
+        L.ref_hnsw_query.argtypes = [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int, C.c_double, C.c_int32, _i32p,
+                                     _f64p, C.POINTER(C.c_int32), _u64p]
         self._fn("ref_ivf_meta", [_vp, _i64p])
         self._fn("ref_ivf_export", [_vp] + [_vp] * 10)
         self._fn("ref_save_ivf", [_vp, C.c_char_p])
@@ -460,6 +470,37 @@ class RefLib(_Common):
         return self._handle(self._ivf_assemble(n, d, cent.shape[0], d1, int(split), seed, _f64(P),
                                                cent, np.ascontiguousarray(assignment, np.int32),
                                                raw, _f32(t)))
+
+    def hnsw_build(self, raw, t, M, ef, seed):
+        raw, t = _f32(raw), _f32(t)
+        h = self.lib.ref_hnsw_build(raw, t, raw.shape[0], raw.shape[1], M, ef, seed)
+        if not h:
+            self._check(2)
+        return h
+
+    def hnsw_load(self, path, raw, t):
+        raw, t = _f32(raw), _f32(t)
+        h = self.lib.ref_hnsw_load(str(path).encode(), raw, t, raw.shape[0], raw.shape[1])
+        if not h:
+            self._check(2)
+        return h
+
+    def hnsw_save(self, h, path):
+        self._check(self.lib.ref_hnsw_save(h, str(path).encode()))
+
+    def hnsw_free(self, h):
+        self.lib.ref_hnsw_free(h)
+
+    def hnsw_query(self, h, q_t, q_raw, K, nef, mode, eps0=2.1, delta_d=32):
+        """mode 0 plain, 1 pd, 2 plus, 3 plusplus -> (ids, dists, [dims, dco, hops, cand])."""
+        ids = np.empty(K, np.int32)
+        dists = np.empty(K, np.float64)
+        cnt = C.c_int32()
+        st = np.zeros(4, np.uint64)
+        self._check(self.lib.ref_hnsw_query(h, _nullable(None if q_t is None else _f32(q_t)),
+                                            _nullable(None if q_raw is None else _f32(q_raw)), K, nef, mode,
+                                            eps0, delta_d, ids, dists, C.byref(cnt), st))
+        return ids[:cnt.value].copy(), dists[:cnt.value].copy(), st
 
     def assemble_split(self, t, centroids_t, assignment, seed=0, d1=32):
         """kAdSplit-only reference IvfIndex (centroids_t, buckets, ids_flat, a1_t, a2_t)

@@ -22,6 +22,7 @@
 
 #include "adsann/bench.hpp"
 #include "adsann/dco.hpp"
+#include "adsann/hnsw.hpp"
 #include "adsann/ivf.hpp"
 #include "adsann/rng.hpp"
 #include "adsann/transform.hpp"
@@ -488,6 +489,45 @@ int ref_ivf_query_batch(void* h, const double* P, int rotate, const float* Qt, c
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         for (const auto& e : errs)
             if (!e.empty()) throw std::invalid_argument(e);
+    });
+}
+
+// ---- HNSW (hnsw.hpp:44-105): build / save / load / query, for the facade parity test.
+void* ref_hnsw_build(const float* raw, const float* t, std::int32_t n, std::int32_t d, std::int32_t M,
+                     std::int32_t ef, std::uint64_t seed) {
+    HnswGraph* g = nullptr;
+    const int rc = guard([&] { g = new HnswGraph(build_hnsw(make_ds(raw, n, d), make_ds(t, n, d), M, ef, seed)); });
+    return rc == 0 ? g : nullptr;
+}
+
+void* ref_hnsw_load(const char* dir, const float* raw, const float* t, std::int32_t n, std::int32_t d) {
+    HnswGraph* g = nullptr;
+    const int rc = guard([&] { g = new HnswGraph(load_hnsw(dir, make_ds(raw, n, d), make_ds(t, n, d))); });
+    return rc == 0 ? g : nullptr;
+}
+
+int ref_hnsw_save(void* g, const char* dir) {
+    return guard([&] { save_hnsw(*static_cast<const HnswGraph*>(g), dir); });
+}
+
+void ref_hnsw_free(void* g) { delete static_cast<HnswGraph*>(g); }
+
+// stats[0..3] = dims_evaluated, dco_count, hops, candidates
+int ref_hnsw_query(void* g, const float* q_t, const float* q_raw, std::int32_t K, std::int32_t nef, int mode,
+                   double eps0, std::int32_t delta_d, std::int32_t* ids, double* dists, std::int32_t* count,
+                   std::uint64_t* stats) {
+    return guard([&] {
+        const KnnResult r = hnsw_query(*static_cast<const HnswGraph*>(g), q_t, q_raw, K, nef,
+                                       static_cast<HnswMode>(mode), DcoConfig{eps0, delta_d});
+        *count = static_cast<std::int32_t>(r.ids.size());
+        for (std::size_t j = 0; j < r.ids.size(); ++j) {
+            ids[j] = r.ids[j];
+            dists[j] = r.dists[j];
+        }
+        stats[0] = r.stats.dims_evaluated;
+        stats[1] = r.stats.dco_count;
+        stats[2] = r.stats.hops;
+        stats[3] = r.stats.candidates;
     });
 }
 

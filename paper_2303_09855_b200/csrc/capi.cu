@@ -615,6 +615,16 @@ int ads_dco_fixed(ads_ctx* ctx, const ads_dco_batch* hb) {
     });
 }
 
+int ads_dco_prefix_sums_device(ads_ctx* ctx, const float* dX, int64_t n_rows, int32_t dim, const float* dq,
+                               const int64_t* dcand, int32_t nc, int32_t delta_d, double* dout) {
+    return guard([&] {
+        require(dim >= 1 && n_rows >= 0 && nc >= 0, "dco: bad shape");
+        require(delta_d >= 1 && delta_d <= dim, "DcoConfig: delta_d must be in [1, dim]");
+        ctx->use();
+        launch_prefix_sums(dX, dim, dq, dcand, nc, delta_d, dout, ctx->stream);
+    });
+}
+
 int ads_dco(ads_ctx* ctx, int32_t kind, const float* o, int32_t n_o, const float* q, int32_t n_q,
             double r, double eps0, int32_t delta_d, int32_t* positive, double* distance,
             double* observed, int32_t* dims_used) {

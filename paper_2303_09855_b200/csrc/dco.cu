@@ -132,7 +132,34 @@ __global__ void __launch_bounds__(kDcoWarps * 32) dco_fixed_kernel(DcoLaunch a) 
     }
 }
 
+// Partial squared distances at every Δd boundary and at D for rows cand[0..nc)
+// against one query (the sums ad_scan / pd_scan_kernel test, dco.hpp:122-177,
+// in their order: fp64, index order, separate roundings).  One thread per row;
+// the graph search (HNSW) replays the reference's decisions from them with the
+// threshold in force at each comparison.
+__global__ void prefix_sums_kernel(const float* __restrict__ X, int D, const float* __restrict__ q,
+                                   const int64_t* __restrict__ cand, int nc, int dd, int nb,
+                                   double* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const float* x = X + cand[c] * static_cast<int64_t>(D);
+    double s = 0.0;
+    int t = 0;
+    for (int j = 0; j < D; ++j) {
+        s = sq_diff_acc(s, x[j], static_cast<double>(q[j]));
+        if ((j + 1) % dd == 0 || j + 1 == D) out[static_cast<int64_t>(c) * nb + t++] = s;
+    }
+}
+
 }  // namespace
+
+void launch_prefix_sums(const float* X, int D, const float* q, const int64_t* cand, int nc, int dd,
+                        double* out, cudaStream_t st) {
+    if (nc <= 0) return;
+    const int nb = (D + dd - 1) / dd;
+    prefix_sums_kernel<<<(nc + 127) / 128, 128, 0, st>>>(X, D, q, cand, nc, dd, nb, out);
+    ADS_LAUNCH_CHECK();
+}
 
 void launch_dco_fixed(const DcoLaunch& a, cudaStream_t st) {
     const size_t smem = sizeof(float) * kDcoWarps * 1024 + sizeof(double) * a.nseg * kQPitch +

@@ -68,6 +68,9 @@ struct DcoLaunch {
     unsigned long long* counter;  // device scratch, zeroed by the launcher
 };
 void launch_dco_fixed(const DcoLaunch& a, cudaStream_t st);
+// out[c * ceil(D/dd) + t] = S at min((t+1)dd, D) for row cand[c] (dco.cu).
+void launch_prefix_sums(const float* X, int D, const float* q, const int64_t* cand, int nc, int dd,
+                        double* out, cudaStream_t st);
 
 struct SearchLaunch {
     const float* a1;

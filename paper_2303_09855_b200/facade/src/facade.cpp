@@ -110,6 +110,12 @@ void emit_records(const std::filesystem::path& p, std::int32_t n, std::int32_t d
 
 }  // namespace
 
+namespace adsann::detail {
+// shared with the other facade translation units (facade_hnsw.cpp, facade_bench.cpp)
+ads_ctx* engine_ctx() { return engine(); }
+void check_rc(int rc) { check(rc); }
+}  // namespace adsann::detail
+
 namespace adsann {
 
 // ------------------------------------------------------------------ vecio
@@ -638,3 +644,14 @@ std::optional<double> avg_distance_ratio(std::span<const double> result_dists, s
 }
 
 }  // namespace adsann
+
+namespace adsann::detail {
+ads_ivf* ivf_handle(const IvfIndex& idx) {
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!idx.device) idx.device = std::make_shared<DeviceIvf>();
+    }
+    return device_of(idx);
+}
+ads_transform* transform_handle(const TransformMatrix& m) { return g_transforms.get(m); }
+}  // namespace adsann::detail

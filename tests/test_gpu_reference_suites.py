@@ -1,11 +1,12 @@
 """The REFERENCE's own doctest suites (test_dco.cpp, test_ivf.cpp,
-test_transform.cpp, test_vecio.cpp from /root/reference/proj/tests), compiled
-unchanged against the adsann C++ facade of the B200 engine (tests/cpp/Makefile,
-doctest shim tests/cpp/doctest.h), run on the GPU.  Every DCO, transform,
-k-means, build_ivf, ivf_query and brute_force_knn call in them executes on the
-B200 through include/adsann_b200.h.  facade_theory_test is this repo's own
-doctest file for the facade's verify_theory (the reference's test_bench.cpp
-also needs its HNSW builders, which are out of scope)."""
+test_transform.cpp, test_vecio.cpp, test_bench.cpp, test_hnsw.cpp from
+/root/reference/proj/tests), compiled unchanged against the adsann C++ facade of
+the B200 engine (tests/cpp/Makefile, doctest shim tests/cpp/doctest.h), run on
+the GPU.  Every DCO, transform, k-means, build_ivf, ivf_query, brute_force_knn,
+sweep_ivf and hnsw_query comparison in them executes on the B200 through
+include/adsann_b200.h (HNSW: graph build and walk on the host, every query-time
+DCO batched per hop on the GPU).  facade_theory_test is this repo's own doctest
+file for the facade's verify_theory."""
 import os
 import subprocess
 
@@ -16,8 +17,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "cpp", "_bin")
 
 
-@pytest.mark.parametrize("suite", ["test_dco", "test_transform", "test_vecio", "test_ivf",
-                                   "facade_theory_test"])
+@pytest.mark.parametrize("suite", ["test_dco", "test_transform", "test_vecio", "test_ivf", "test_bench",
+                                   "test_hnsw", "facade_theory_test"])
 def test_reference_suite_passes_on_b200(eng, suite):
     exe = os.path.join(BIN, suite)
     if not os.path.exists(exe):
