@@ -415,7 +415,7 @@ def measure(S, cfg, nprobe, args, D, log, steps):
         # per step: rotation, query centring, coarse GEMM (tcgen05), prefilter, scan, plus the
         # longest-first order when the batch exceeds one wave of resident CTAs (key kernel +
         # radix sort) (ncu launch lists: profiles/)
-        "gpu_launches": (11 if order_sorted(args, nq, d) else 5) * steps,
+        "gpu_launches": (7 if order_sorted(args, nq, d) else 5) * steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "frac_vs_nominal_8000": achieved / 8000.0,
                      "traffic": ncu_traffic(cfg.key),

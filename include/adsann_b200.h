@@ -270,23 +270,19 @@ int ads_ivf_meta(ads_ivf *idx, int64_t *meta);
 int ads_ivf_export(ads_ivf *idx, float *centroids_t, float *centroids_raw, int64_t *list_off,
                    int32_t *ids_flat, float *a1_t, float *a2_t, float *a1_raw, float *a2_raw);
 
-/* Threshold refresh schedule and launch knobs.
- * scheduler 0 (query-major, one CTA per query): the running K-th distance r is
- *   re-read before candidate i of a query's probe-ordered stream when i = 0,
- *   first, first+step, ...; first = step = 1 is the reference's per-candidate
- *   refresh (ivf.cpp:331, 391), larger values batch it.
- * scheduler 1 (list-major waves): r is re-read at probe-rank boundaries
- *   0, first, first+step, ... (first/step count probed LISTS; defaults 1 and
- *   step as given); each list is read once per wave for all its queries. */
+/* Threshold refresh schedule and launch knobs.  The running K-th distance r is
+ * re-read before candidate i of a query's probe-ordered stream when i = 0,
+ * first, first+step, ...; first = step = 1 is the reference's per-candidate
+ * refresh (ivf.cpp:331, 391), larger values batch it. */
 typedef struct {
-    int64_t first;         /* default K (scheduler 0) / 1 list (scheduler 1) */
-    int64_t step;          /* 0 (default): 64 * warps_per_cta candidates (scheduler 0), 1 list (scheduler 1) */
-    int32_t warps_per_cta; /* 0 (default): 4 for D <= 256, else 10 (scheduler 0); 8 (scheduler 1) */
+    int64_t first;         /* default K */
+    int64_t step;          /* 0 (default): 64 * warps_per_cta candidates */
+    int32_t warps_per_cta; /* 0 (default): 4 for D <= 256, else 10 */
     int32_t queries_per_cta; /* reserved: the query-major kernel serves one query per CTA */
     int32_t ctas_per_sm;   /* 0 = occupancy maximum */
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */
-    int32_t scheduler;     /* 0 query-major (default), 1 list-major waves (16-byte-aligned layouts) */
-    int32_t tile;          /* list-major: candidates staged per shared-memory tile (default 64) */
+    int32_t scheduler;     /* must be 0 (query-major, one CTA per query) */
+    int32_t tile;          /* reserved */
     int32_t query_order;   /* order in which the batch's queries are served; results do not
                               depend on it.  2 (default): longest first (descending candidate
                               count), which shortens the tail of the persistent scan grid;
@@ -301,9 +297,9 @@ typedef struct {
     int32_t rotate_mode;   /* when the queries come untransformed (Q_t == NULL): 0 (default) exact
                               fp64 rotation, bit-identical to apply(); 1 the 3xTF32 tensor-core
                               rotation of ads_apply_dataset_tc (~1e-6 |q|; D % 4 == 0, D >= 32) */
-    int32_t probe_lo;      /* scheduler 0: scan only the lists at probe ranks probe_lo .. n_probe-1
+    int32_t probe_lo;      /* scan only the lists at probe ranks probe_lo .. n_probe-1
                               (default 0) */
-    const double *r0;      /* scheduler 0, nullable: per-query initial radius (a distance); r starts
+    const double *r0;      /* nullable: per-query initial radius (a distance); r starts
                               at r0[q] and is min(r0[q], heap threshold) at every refresh.  Host
                               memory for ads_ivf_search, device memory for ads_ivf_search_device.
                               With probe_lo this is the second wave of the sharded search: probe

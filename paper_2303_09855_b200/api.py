@@ -523,8 +523,8 @@ def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_p
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
                 tile: int = 64, query_order: int = 2, coarse_mode: int = 0,
                 rotate_mode: int = 0, probe_lo: int = 0, r0=None) -> L.SearchOpts:
-    """scheduler 0: query-major, first/step in candidates; scheduler 1: list-major
-    waves, first/step in probed lists (see include/adsann_b200.h)."""
+    """Search options (ads_search_opts, include/adsann_b200.h): first/step set the
+    threshold refresh schedule in candidates; scheduler must be 0."""
     o = L.SearchOpts()
     L.ads_search_opts_default(C.byref(o))
     o.first, o.step, o.warps_per_cta, o.queries_per_cta, o.ctas_per_sm, o.time_stages = (

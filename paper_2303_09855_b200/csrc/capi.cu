@@ -153,7 +153,6 @@ struct ads_ivf {
     DevBuf ph, pl, qh, ql;  // rotate_mode 1: P and the queries as TF32 hi/lo pairs
     DevBuf r0buf;           // host-API copy of opts.r0
     bool p_split = false;
-    ListMajorScratch lm;
     int32_t* chain_rank = nullptr;  // L2-locality rank of each list (host chain over centroids)
     DevBuf order, order_tmp;
     // coarse prefilter state per centroid space (transformed / raw)
@@ -1303,11 +1302,11 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     // auto launch shape: CTAs of 4 warps for D <= 256; wider CTAs amortise the
     // larger per-query shared state (staged query, chunk slots) at high D.
     // The refresh interval follows the CTA: 64 candidates per warp.
-    if (o.warps_per_cta <= 0) o.warps_per_cta = o.scheduler == 1 ? 8 : (x->d <= 256 ? 4 : 10);
-    if (o.step <= 0) o.step = o.scheduler == 1 ? 1 : 64 * static_cast<int64_t>(o.warps_per_cta);
+    require(o.scheduler == 0, "search: scheduler must be 0 (query-major; the list-major scheduler was removed)");
+    if (o.warps_per_cta <= 0) o.warps_per_cta = x->d <= 256 ? 4 : 10;
+    if (o.step <= 0) o.step = 64 * static_cast<int64_t>(o.warps_per_cta);
     require(o.warps_per_cta >= 1 && o.warps_per_cta <= 32, "search: warps_per_cta in [1, 32]");
     require(o.probe_lo >= 0 && o.probe_lo <= nprobe, "ivf_query: probe_lo must be in [0, n_probe]");
-    require(o.scheduler == 0 || (o.probe_lo == 0 && !o.r0), "search: probe_lo / r0 need scheduler 0");
     require(o.queries_per_cta >= 1 && o.queries_per_cta <= 16, "search: queries_per_cta in [1, 16]");
     cudaStream_t st = x->ctx->stream;
     const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
@@ -1404,39 +1403,7 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
         launch_query_order(probes, nq, nprobe, x->chain_rank, x->k, x->order_tmp, ord, st);
         a.order = ord;
     }
-    if (o.scheduler == 1 && a.vec == 4) {
-        ListMajorLaunch m{};
-        m.a1 = a.a1;
-        m.a2 = a.a2;
-        m.d1 = a.d1;
-        m.D = D;
-        m.ids = a.ids;
-        m.list_off = a.list_off;
-        m.L = x->k;
-        m.Q = Qs;
-        m.nq = nq;
-        m.probes = probes;
-        m.nprobe = nprobe;
-        m.K = K;
-        m.final_fd = a.final_fd;
-        m.segs = a.segs;
-        m.tfac = a.tfac;
-        m.nseg = a.nseg;
-        m.ntest = a.ntest;
-        m.first_lists = static_cast<int>(opts && opts->first > 0 ? opts->first : 1);
-        m.step_lists = static_cast<int>(o.step);
-        m.tile = o.tile;
-        m.warps = o.warps_per_cta;
-        m.qgroup = o.queries_per_cta;
-        m.out_ids = dids;
-        m.out_dists = ddists;
-        m.out_cnt = dcnt;
-        m.out_dims = reinterpret_cast<unsigned long long*>(ddims);
-        m.out_cand = reinterpret_cast<unsigned long long*>(dcand);
-        launch_listmajor_search(m, x->lm, st);
-    } else {
-        launch_ivf_search(a, st);
-    }
+    launch_ivf_search(a, st);
     if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[4], st));
 }
 

@@ -136,36 +136,6 @@ struct DevBuf {
     }
 };
 
-// List-major wave search (listmajor.cu).
-struct ListMajorLaunch {
-    const float* a1;
-    const float* a2;
-    int d1, D;
-    const int32_t* ids;
-    const int64_t* list_off;
-    int L;
-    const float* Q;
-    int nq;
-    const int32_t* probes;
-    int nprobe, K, final_fd;
-    const Seg* segs;
-    const double* tfac;
-    int nseg, ntest;
-    int first_lists, step_lists;  // wave sizes in probed lists
-    int tile, warps, qgroup;
-    int32_t* out_ids;
-    double* out_dists;
-    int32_t* out_cnt;
-    unsigned long long* out_dims;
-    unsigned long long* out_cand;
-};
-struct ListMajorScratch {
-    DevBuf pre, heap_d, heap_i, heap_c, rr, thr, dims, wcnt, wbase, lcnt, loff, fill, pairs, counter,
-        flag, pdist, pid, tmp;
-};
-void launch_listmajor_search(const ListMajorLaunch& a, ListMajorScratch& s, cudaStream_t st);
-size_t listmajor_scan_smem(int tile, int d1, int D, int nseg, int ntest, int qgroup);
-
 // Certified coarse quantizer (coarse.cu): fp32 prefilter + exact fp64 rescoring.
 struct CoarseScratch {
     DevBuf approx, qc, qn2, qnrm;

@@ -17,8 +17,6 @@
 //                        then thr[t] = factor[d_t] * r^2 is rebuilt.
 #include <cfloat>
 
-#include <cub/cub.cuh>
-
 #include "engine.hpp"
 #include "scan_engine.cuh"
 
@@ -722,36 +720,26 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
 }  // namespace
 
 namespace {
+// Queries ordered by a 32-bit key (ties by query index): one CTA bitonic-sorts a
+// tile of kOrderTile packed (key << 32 | q) words in shared memory, so a batch of
+// up to kOrderTile queries is fully ordered and larger ones are ordered per tile.
+// Results never depend on the order (each query is searched independently); it
+// only shapes the persistent scan grid's tail.
+constexpr int kOrderTile = 16384;
+constexpr int kOrderThreads = 1024;
+
 __global__ void order_keys_kernel(const int32_t* probes, int nq, int nprobe, const int32_t* rank,
-                                  int32_t* keys, int32_t* vals) {
+                                  unsigned long long* words) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
-    keys[q] = rank[probes[static_cast<int64_t>(q) * nprobe]];
-    vals[q] = q;
-}
-}  // namespace
-
-void launch_query_order(const int32_t* probes, int nq, int nprobe, const int32_t* rank, int k,
-                        DevBuf& scratch, int32_t* order, cudaStream_t st) {
-    int bits = 1;
-    while ((1 << bits) < k) ++bits;
-    int32_t* kin = scratch.get<int32_t>(static_cast<size_t>(nq) * 3 + 64);
-    int32_t* kout = kin + nq;
-    int32_t* vin = kout + nq;
-    order_keys_kernel<<<(nq + 255) / 256, 256, 0, st>>>(probes, nq, nprobe, rank, kin, vin);
-    ADS_LAUNCH_CHECK();
-    size_t tmp = 0;
-    ADS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, order, nq, 0, bits, st));
-    static thread_local DevBuf tmpbuf;
-    void* t = tmpbuf.get<unsigned char>(tmp);
-    ADS_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, order, nq, 0, bits, st));
+    const uint32_t key = static_cast<uint32_t>(rank[probes[static_cast<int64_t>(q) * nprobe]]);
+    words[q] = (static_cast<unsigned long long>(key) << 32) | static_cast<uint32_t>(q);
 }
 
-namespace {
-// key = 2^24 - 1 - (candidates the query will stream) / 4, so an ascending
-// sort puts the longest queries first
+// key = 2^32 - 1 - (candidates the query will stream), so ascending order puts the
+// longest queries first
 __global__ void work_keys_kernel(const int32_t* probes, int nq, int nprobe, int probe_lo,
-                                 const int64_t* list_off, uint32_t* keys, int32_t* vals) {
+                                 const int64_t* list_off, unsigned long long* words) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     int64_t tot = 0;
@@ -759,25 +747,64 @@ __global__ void work_keys_kernel(const int32_t* probes, int nq, int nprobe, int 
         const int p = probes[static_cast<int64_t>(q) * nprobe + i];
         tot += list_off[p + 1] - list_off[p];
     }
-    // 24-bit key (three radix passes): candidates / 4, saturating at 2^26
-    const int64_t v = tot >> 2;
-    keys[q] = 0xFFFFFFu - static_cast<uint32_t>(v < 0xFFFFFF ? v : 0xFFFFFF);
-    vals[q] = q;
+    const uint32_t key = 0xFFFFFFFFu - static_cast<uint32_t>(tot < 0xFFFFFFFF ? tot : 0xFFFFFFFF);
+    words[q] = (static_cast<unsigned long long>(key) << 32) | static_cast<uint32_t>(q);
+}
+
+__global__ void __launch_bounds__(kOrderThreads) order_sort_kernel(const unsigned long long* words, int nq,
+                                                                   int32_t* order) {
+    extern __shared__ unsigned long long tile[];
+    const int base = blockIdx.x * kOrderTile;
+    const int n = min(kOrderTile, nq - base);
+    int P2 = 1;
+    while (P2 < n) P2 <<= 1;
+    for (int i = threadIdx.x; i < P2; i += blockDim.x) tile[i] = i < n ? words[base + i] : ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= P2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P2 / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long x = tile[lo], y = tile[hi];
+                if ((x > y) == up) {
+                    tile[lo] = y;
+                    tile[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) order[base + i] = static_cast<int32_t>(tile[i] & 0xffffffffu);
+}
+
+void sort_order(const unsigned long long* words, int nq, int32_t* order, cudaStream_t st) {
+    const int tiles = (nq + kOrderTile - 1) / kOrderTile;
+    int P2 = 1;
+    while (P2 < (nq < kOrderTile ? nq : kOrderTile)) P2 <<= 1;
+    const size_t smem = sizeof(unsigned long long) * static_cast<size_t>(P2);
+    ADS_CUDA(cudaFuncSetAttribute(order_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(unsigned long long) * kOrderTile)));
+    order_sort_kernel<<<tiles, kOrderThreads, smem, st>>>(words, nq, order);
+    ADS_LAUNCH_CHECK();
 }
 }  // namespace
 
+void launch_query_order(const int32_t* probes, int nq, int nprobe, const int32_t* rank, int k,
+                        DevBuf& scratch, int32_t* order, cudaStream_t st) {
+    (void)k;
+    if (nq <= 0) return;
+    unsigned long long* w = scratch.get<unsigned long long>(static_cast<size_t>(nq));
+    order_keys_kernel<<<(nq + 255) / 256, 256, 0, st>>>(probes, nq, nprobe, rank, w);
+    ADS_LAUNCH_CHECK();
+    sort_order(w, nq, order, st);
+}
+
 void launch_query_order_work(const int32_t* probes, int nq, int nprobe, int probe_lo, const int64_t* list_off,
                              DevBuf& scratch, int32_t* order, cudaStream_t st) {
-    uint32_t* kin = scratch.get<uint32_t>(static_cast<size_t>(nq) * 3 + 64);
-    uint32_t* kout = kin + nq;
-    int32_t* vin = reinterpret_cast<int32_t*>(kout + nq);
-    work_keys_kernel<<<(nq + 255) / 256, 256, 0, st>>>(probes, nq, nprobe, probe_lo, list_off, kin, vin);
+    if (nq <= 0) return;
+    unsigned long long* w = scratch.get<unsigned long long>(static_cast<size_t>(nq));
+    work_keys_kernel<<<(nq + 255) / 256, 256, 0, st>>>(probes, nq, nprobe, probe_lo, list_off, w);
     ADS_LAUNCH_CHECK();
-    size_t tmp = 0;
-    ADS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, order, nq, 0, 24, st));
-    static thread_local DevBuf tmpbuf;
-    void* t = tmpbuf.get<unsigned char>(tmp);
-    ADS_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, order, nq, 0, 24, st));
+    sort_order(w, nq, order, st);
 }
 
 void launch_coarse_dist(const float* Q, int nq, const float* C, int L, int D, double* out,

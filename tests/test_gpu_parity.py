@@ -294,56 +294,13 @@ def test_brute_force_knn_bitexact(eng, orc, n, d, nq, K):
         eng.brute_force_knn(base, q, n + 1)
 
 
-# ------------------------------------------------------------------ list-major wave scheduler
-def _waves(nprobe, b0, B):
-    w = [0]
-    r = b0
-    while r < nprobe:
-        w.append(r)
-        r += B
-    return w
-
-
-@pytest.mark.parametrize("case", [(4000, 64, 16, 50, 32, 32, 10), (3000, 128, 32, 40, 32, 32, 20),
-                                  (2000, 96, 8, 30, 32, 32, 7), (1500, 48, 8, 20, 16, 16, 5)])
-@pytest.mark.parametrize("b0,B,qg", [(1, 1, 1), (1, 4, 8), (2, 3, 3), (1, 100, 16)])
-def test_ivf_listmajor_waves_bitexact(eng, orc, case, b0, B, qg):
-    """scheduler 1 (lists read once per wave for all their queries) == the oracle
-    with the threshold refreshed at the same probe-rank boundaries."""
-    n, d, blobs, k, d1, dd, K = case
-    raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 40, 77 + d)
-    lay = oracle_index(orc, raw, t, P, k, 79, d1=d1)
+def test_ivf_scheduler_1_is_rejected(eng, orc):
+    """The list-major scheduler was removed (slower than query-major)."""
+    raw, t, qr, qt, P = make_fixture(orc, 500, 32, 4, 4, 5)
+    lay = oracle_index(orc, raw, t, P, 8, 6, d1=16)
     idx = gpu_index(eng, lay, P)
-    cfg = eng.DcoConfig(2.1, dd)
-    for mode in MODES:
-        for nprobe in (1, 6, k):
-            o = eng.search_opts(first=b0, step=B, scheduler=1, warps_per_cta=4, tile=64,
-                                queries_per_cta=qg)
-            res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg, opts=o)
-            w = _waves(nprobe, b0, B)
-            for qi in range(qt.shape[0]):
-                ids, dists, stats = orc.ivf_query(lay, qt[qi], qr[qi], K, nprobe, mode, 2.1, dd, waves=w)
-                c = int(res.counts[qi])
-                assert c == len(ids), (mode, nprobe, qi)
-                np.testing.assert_array_equal(res.ids[qi, :c], ids, err_msg=f"{mode} np={nprobe} q={qi}")
-                np.testing.assert_array_equal(res.dists[qi, :c], dists)
-                assert int(res.dims[qi]) == int(stats[0]), (mode, nprobe, qi)
-                assert int(res.candidates[qi]) == int(stats[2])
-
-
-def test_ivf_listmajor_tiles_smaller_than_lists(eng, orc):
-    """Lists longer than the shared-memory tile are staged in several tiles."""
-    raw, t, qr, qt, P = make_fixture(orc, 6000, 64, 4, 30, 5)
-    lay = oracle_index(orc, raw, t, P, 8, 6, d1=32)
-    assert np.diff(lay["list_off"]).max() > 64
-    idx = gpu_index(eng, lay, P)
-    for tile, qg in ((16, 2), (32, 5), (64, 8), (128, 1)):
-        o = eng.search_opts(first=1, step=2, scheduler=1, tile=tile, warps_per_cta=8, queries_per_cta=qg)
-        res = eng.ivf_query_batch(idx, qt, qr, 10, 5, eng.IvfMode.kAdSplit, opts=o)
-        for qi in range(qt.shape[0]):
-            ids, dists, stats = orc.ivf_query(lay, qt[qi], qr[qi], 10, 5, "ad-split", waves=[0, 1, 3])
-            np.testing.assert_array_equal(res.ids[qi, :len(ids)], ids)
-            assert int(res.dims[qi]) == int(stats[0])
+    with pytest.raises(ValueError):
+        eng.ivf_query_batch(idx, qt, qr, 5, 2, eng.IvfMode.kAdSplit, opts=eng.search_opts(scheduler=1))
 
 
 def test_coarse_prefilter_adversarial_ties(eng, orc):
