@@ -330,7 +330,8 @@ def measure(S, cfg, nprobe, args, D, log, steps):
     K, nq, d = cfg.K, cfg.nq, cfg.d
     mode = ads.IvfMode.kAdSplit
     opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True,
-                           query_order=args.query_order, ctas_per_sm=args.ctas_per_sm)
+                           query_order=args.query_order, ctas_per_sm=args.ctas_per_sm,
+                           tile=-1 if getattr(args, "no_dense", False) else 64)
     dq = ads.DeviceArray.from_host(ctx, q)
     outs = {nm: ads.DeviceArray(ctx, shape, dt) for nm, shape, dt in (
         ("ids", (nq, K), np.int32), ("dists", (nq, K), np.float64), ("cnt", (nq,), np.int32),
@@ -406,6 +407,9 @@ def measure(S, cfg, nprobe, args, D, log, steps):
     achieved = scanned / (scan_avg / 1e3) / 1e9
     stage = np.mean(np.array(stage_ms), axis=0)
     world_q = nq * D.world * steps
+    traffic = ncu_traffic(cfg.key)
+    dram = {} if not traffic else {  # ncu DRAM bytes of the scan launch over its live time
+        "dram_gbs": traffic / (scan_avg / 1e3), "dram_frac": traffic / (scan_avg / 1e3) / peaks["hbm_gbs"]}
     return {
         "value": world_q / (total_ms / 1e3), "ms_per_step": total_ms / steps,
         "recall_at_k": recall_of(ids, gt, K) if gt is not None else None,
@@ -418,11 +422,11 @@ def measure(S, cfg, nprobe, args, D, log, steps):
         "gpu_launches": (7 if order_sorted(args, nq, d) else 5) * steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "frac_vs_nominal_8000": achieved / 8000.0,
-                     "traffic": ncu_traffic(cfg.key),
+                     "traffic": traffic,
                      "traffic_unit": "GB per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
                      "kernel": "ivf_search_kernel", "peak_source": peaks["source"] + ", copy (burst)",
                      "algorithmic_bytes_per_launch": scanned,
-                     "scanned_gbs_whole_step": scanned / (float(np.mean(step_ms)) / 1e3) / 1e9},
+                     "scanned_gbs_whole_step": scanned / (float(np.mean(step_ms)) / 1e3) / 1e9, **dram},
         "stages_ms": {"rotate": float(stage[0]), "coarse": float(stage[1]), "select": float(stage[2]),
                       "scan": float(stage[3])},
         "dims_per_query": float(dims.mean()),
@@ -833,6 +837,8 @@ def main():
     ap.add_argument("--query-order", type=int, default=2,
                     help="2: longest queries first (default), 1: L2-locality order, 0: input order")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-dense", action="store_true",
+                    help="A/B: the lane walk gathers A1 too (no dense prefix phase)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the config-3 measurement on the N=1 line")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

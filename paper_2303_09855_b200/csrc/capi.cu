@@ -147,6 +147,7 @@ struct ads_ivf {
     int64_t* list_off = nullptr;
     int32_t* ids = nullptr;
     float *a1_t = nullptr, *a2_t = nullptr, *a1_raw = nullptr, *a2_raw = nullptr;
+    float* a1i_t = nullptr;  // A1 interleaved by 32-row groups (dense prefix phase of the scan)
     double* P = nullptr;
     std::map<PlanKey, std::unique_ptr<DevSegPlan>> plans;
     DevBuf dist, probes, qrot, qin_t, qin_raw, o_ids, o_dists, o_cnt, o_dims, o_cand;
@@ -165,7 +166,7 @@ struct ads_ivf {
         for (void* p : {static_cast<void*>(cent_t), static_cast<void*>(cent_raw),
                         static_cast<void*>(list_off), static_cast<void*>(ids),
                         static_cast<void*>(a1_t), static_cast<void*>(a1_raw),  // a2_* live inside
-                        static_cast<void*>(P), static_cast<void*>(chain_rank)})
+                        static_cast<void*>(P), static_cast<void*>(chain_rank), static_cast<void*>(a1i_t)})
             if (p) cudaFree(p);
         cc_t.release();
         cc_raw.release();
@@ -848,6 +849,16 @@ static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& o
     out.cmax = m * (1.0 + 1e-12) + 1e-300;
 }
 
+// The interleaved A1 copy the scan's dense prefix phase reads (ivf.cu); call once the
+// index's A1 holds its final rows.
+static void ivf_finish_dense(ads_ivf* x, cudaStream_t st) {
+    if (x->layout == 1 && x->d1p == 32 && x->a1_t && !x->a1i_t) {
+        const size_t groups = (static_cast<size_t>(x->n) + 31) / 32;
+        ADS_CUDA(cudaMalloc(&x->a1i_t, sizeof(float) * 1024 * (groups > 0 ? groups : 1)));
+        interleave_a1(x->a1_t, x->n, x->a1i_t, st);
+    }
+}
+
 static void ivf_finish_coarse(ads_ivf* x, cudaStream_t st) {
     centroid_prefilter(x->cent_t, x->k, x->d, x->cc_t, st);
     if (x->cent_raw) centroid_prefilter(x->cent_raw, x->k, x->d, x->cc_raw, st);
@@ -904,6 +915,7 @@ int ads_ivf_create(ads_ctx* ctx, const ads_ivf_desc* desc, ads_ivf** out) {
             x->chain_rank = dev_upload(rk.data(), rk.size(), st);
         }
         ivf_finish_coarse(x.get(), st);
+        ivf_finish_dense(x.get(), st);
         ADS_CUDA(cudaStreamSynchronize(st));
         *out = x.release();
     });
@@ -966,6 +978,7 @@ int ads_ivf_build(ads_ctx* ctx, const float* raw, const float* t, int32_t n, int
             const std::vector<int32_t> rk = centroid_chain_rank(hc.data(), k, d);
             x->chain_rank = dev_upload(rk.data(), rk.size(), st);
             ivf_finish_coarse(x.get(), st);
+            ivf_finish_dense(x.get(), st);
             ADS_CUDA(cudaStreamSynchronize(st));
         } catch (...) {
             cudaStreamSynchronize(st);
@@ -1151,6 +1164,7 @@ int ads_ivf_builder_finish(ads_ivf_builder* b, const uint8_t* keep, ads_ivf** ou
         alloc_split_pair(mm, d1, d - d1, &x->a1_t, &x->a2_t);
         gather_split(static_cast<float*>(b->rows.p), I, m, d, d1, x->a1_t, x->a2_t, st);
         ivf_finish_coarse(x.get(), st);
+        ivf_finish_dense(x.get(), st);
         ADS_CUDA(cudaStreamSynchronize(st));
         *out = x.release();
     });
@@ -1393,6 +1407,9 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.out_cand = reinterpret_cast<unsigned long long*>(dcand);
     a.counter = x->ctx->counter;
     a.order = nullptr;
+    // dense prefix phase (ivf.cu): IVF++ on the transformed split layout with a 32-float
+    // A1 whose end is the first test point; opts.tile = -1 turns it off (A/B runs)
+    a.a1i = (mode == ADS_MODE_AD_SPLIT && x->a1i_t && a.vec == 4 && o.tile >= 0) ? x->a1i_t : nullptr;
     // longest queries first; pointless when the whole batch is resident at once
     if (o.query_order == 2 && nq > 1 && nq > search_resident_ctas(a)) {
         int32_t* ord = x->order.get<int32_t>(nq);
@@ -1573,6 +1590,7 @@ int ads_ivf_subset(ads_ivf* src, const uint8_t* keep, ads_ivf** out) {
             }
             c = e;
         }
+        ivf_finish_dense(x.get(), st);
         ADS_CUDA(cudaStreamSynchronize(st));
         *out = x.release();
     });

@@ -103,6 +103,7 @@ struct SearchLaunch {
     unsigned long long* out_cand;
     unsigned long long* counter;
     const int32_t* order;  // nullable: work item w searches query order[w]
+    const float* a1i;      // nullable: the interleaved A1 copy (d1 == 32, split, AD): dense prefix phase
 };
 void launch_ivf_search(const SearchLaunch& a, cudaStream_t st);
 // CTAs of the search grid resident at once (num_sms x occupancy for this launch shape).
@@ -212,6 +213,9 @@ void build_lists(const int32_t* dAssign, int64_t n, int k, int64_t* dListOff, in
                  cudaStream_t st);
 void gather_split(const float* src, const int32_t* dIds, int64_t n, int D, int d1, float* a1,
                   float* a2, cudaStream_t st);
+// The A1 prefix (32 floats per row) re-blocked by 32-row position groups and
+// 16-byte chunks (dense coalesced reads of a list run's prefixes, ivf.cu).
+void interleave_a1(const float* a1, int64_t n, float* a1i, cudaStream_t st);
 // out[i] = keep[asg[i]] ? asg[i] : k (lists a shard does not own sort after every owned one).
 void mask_assignment(const int32_t* dAssign, int64_t n, const uint8_t* dKeep, int k, int32_t* dOut,
                      cudaStream_t st);

@@ -233,6 +233,7 @@ struct SearchShared {
     double r, r_sq;
     int q, stop, total, next, cnt, pnext;
     int pcount[2];
+    int nsurv;  // DENSE: candidates of the chunk that passed the test at d1
     unsigned long long dims;
 };
 
@@ -435,12 +436,25 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
     return true;
 }
 
+#ifndef DENSE_PARTS
+#define DENSE_PARTS 1  // the prefix phase loads its 8 chunks in this many rounds (1: all in flight)
+#endif
 #ifdef ADS_MAXNREG
 #define ADS_SCAN_REGS __maxnreg__(ADS_MAXNREG)
 #else
 #define ADS_SCAN_REGS
 #endif
-template <int VEC, bool FULL>
+// Dense prefix phase (DENSE, IVF++ with a 32-float A1 over the transformed split
+// layout).  The reference computes every candidate's A1 prefix before any test
+// (ivf.cpp:366-386); no decision depends on those sums, and within a chunk the
+// threshold is fixed, so at each chunk start the CTA computes all the chunk's
+// prefixes from the interleaved A1 copy (a1i: a warp reads 32 consecutive rows of
+// one list with eight contiguous 512-byte loads straight into registers, no
+// gather, no shared-memory staging), applies the test at d1 (dco.hpp:129), and
+// hands only the survivors to the lane walk, which resumes them at the first A2
+// segment with the carried prefix.  Sums and decisions are the same operations
+// in the same order, so results are unchanged bit for bit.
+template <int VEC, bool FULL, bool DENSE>
 __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SearchShared sh;
@@ -548,19 +562,80 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
             const int64_t span = lo == 0 ? a.first : a.step;
             const int hi = static_cast<int>(lo + span < total ? lo + span : total);
             const int nhi = static_cast<int>(hi + a.step < total ? hi + a.step : total);  // next chunk [hi, nhi)
-            double* pre_cur = pre_s + (j & 1) * chunk_cap;
+            double* pre_cur = DENSE ? pre_s : pre_s + (j & 1) * chunk_cap;
             double* pend_d = pre_cur;
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
+            int32_t* surv = reinterpret_cast<int32_t*>(pre_s + chunk_cap);  // DENSE: the idle half
             for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) cpos[sl] = locate(lo + sl);
             if (threadIdx.x == 0) {
-                sh.next = lo;
+                sh.next = DENSE ? 0 : lo;
                 sh.pnext = 0;
+                sh.nsurv = 0;
             }
             for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
             __syncthreads();
             const double r = sh.r, r_sq = sh.r_sq;
-            const int pc = sh.pcount[j & 1];  // [lo, lo + pc) carry their prefix in pre_cur
-            const bool can_pre = nseg0 > 0 && nhi > hi;
+            const int pc = DENSE ? 0 : sh.pcount[j & 1];  // [lo, lo + pc) carry their prefix in pre_cur
+            const bool can_pre = !DENSE && nseg0 > 0 && nhi > hi;
+            if constexpr (DENSE) {
+                // tasks = (probed list, 32-row position group) pairs covering the chunk
+                auto list_of = [&](int i) {
+                    int l = 0, h = nl - 1;
+                    while (l < h) {
+                        const int mid = (l + h + 1) >> 1;
+                        if (pre[mid] <= i) l = mid;
+                        else h = mid - 1;
+                    }
+                    return l;
+                };
+                const int l0 = list_of(lo), l1 = list_of(hi - 1);
+                const double t1 = thr[segs[0].test];
+                const double2* q2 = reinterpret_cast<const double2*>(qseg);
+                int t = 0;
+                for (int l = l0; l <= l1; ++l) {
+                    const int as = max(lo, pre[l]), bs = min(hi, pre[l + 1]);
+                    if (as >= bs) continue;
+                    const int pa = lstart[l] + (as - pre[l]), pb = pa + (bs - as);
+                    const int g0 = pa >> 5, g1 = (pb - 1) >> 5;
+                    const int tw = t + ((warp - t) % nwarps + nwarps) % nwarps;  // this warp's first task here
+                    for (int g = g0 + (tw - t); g <= g1; g += nwarps) {
+                        const int p = (g << 5) + static_cast<int>(lane);
+                        const bool act = p >= pa && p < pb;
+                        const float4* src = reinterpret_cast<const float4*>(a.a1i) + static_cast<int64_t>(g) * 256 + lane;
+                        double sa = 0.0;
+#pragma unroll
+                        for (int h = 0; h < DENSE_PARTS; ++h) {
+                            constexpr int PC = 8 / DENSE_PARTS;
+                            float4 v[PC];
+#pragma unroll
+                            for (int c = 0; c < PC; ++c)
+                                v[c] = act ? __ldg(src + (h * PC + c) * 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                            for (int c = 0; c < PC; ++c) {
+                                const double2 qa = q2[(h * PC + c) * 2], qb = q2[(h * PC + c) * 2 + 1];
+                                sa = sq_diff_acc(sa, v[c].x, qa.x);
+                                sa = sq_diff_acc(sa, v[c].y, qa.y);
+                                sa = sq_diff_acc(sa, v[c].z, qb.x);
+                                sa = sq_diff_acc(sa, v[c].w, qb.y);
+                            }
+                        }
+                        const bool keep = act && !(sa > t1);  // reject iff s > thr at d1 (dco.hpp:129)
+                        if (act && !keep) my_dims += static_cast<unsigned long long>(segs[0].len);
+                        const unsigned kb = __ballot_sync(kFull, keep);
+                        int base = 0;
+                        if (lane == 0 && kb) base = atomicAdd(&sh.nsurv, __popc(kb));
+                        base = __shfl_sync(kFull, base, 0);
+                        if (keep) {
+                            const int slot = as - lo + (p - pa);
+                            pre_cur[slot] = sa;
+                            surv[base + __popc(kb & ((1u << lane) - 1u))] = slot;
+                        }
+                    }
+                    t += g1 - g0 + 1;
+                }
+                __syncthreads();
+            }
+            const int nsurv = DENSE ? sh.nsurv : 0;
 
             int cand = -1, seg = 0, pos = 0;
             bool prew = false;  // lane holds a next-chunk candidate's untested prefix
@@ -573,7 +648,16 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                     base = __shfl_sync(kFull, base, 0);
                     if (cand < 0) {
                         const int i = base + __popc(need & ((1u << lane) - 1u));
-                        if (i < hi) {
+                        if constexpr (DENSE) {  // survivors of the prefix test, resumed at A2
+                            if (i < nsurv) {
+                                const int slot = surv[i];
+                                cand = lo + slot;
+                                pos = cpos[slot];
+                                prew = false;
+                                seg = 1;
+                                s = pre_cur[slot];
+                            }
+                        } else if (i < hi) {
                             cand = i;
                             pos = cpos[i - lo];
                             prew = false;
@@ -844,8 +928,11 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     SearchShape sh{};
     sh.cap = static_cast<int>(cap64);
     sh.smem = search_smem(a, sh.cap);
-    sh.kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true> : ivf_search_kernel<4, false>)
-                         : ivf_search_kernel<1, false>;
+    if (a.a1i)
+        sh.kern = a.full ? ivf_search_kernel<4, true, true> : ivf_search_kernel<4, false, true>;
+    else
+        sh.kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true, false> : ivf_search_kernel<4, false, false>)
+                             : ivf_search_kernel<1, false, false>;
     ADS_CUDA(cudaFuncSetAttribute(sh.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sh.smem)));
     ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sh.occ, sh.kern, a.warps * 32, sh.smem));

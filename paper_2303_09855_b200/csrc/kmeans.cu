@@ -372,6 +372,29 @@ __global__ void mask_assignment_kernel(const int32_t* __restrict__ asg, int64_t 
 }
 }  // namespace
 
+namespace {
+// a1i[((g * 8 + c) * 32 + r) * 4 + e] = a1[(g * 32 + r) * 32 + c * 4 + e]: position group
+// g's 32 rows interleaved by 16-byte chunk, so lane r of a warp reading chunk c of
+// rows 32g .. 32g+31 issues one contiguous 512-byte request (zeros past n).
+__global__ void interleave_a1_kernel(const float4* __restrict__ a1, int64_t n, float4* __restrict__ a1i,
+                                     int64_t groups) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= groups * 256) return;
+    const int64_t g = t >> 8;
+    const int c = static_cast<int>((t >> 5) & 7), r = static_cast<int>(t & 31);
+    const int64_t p = g * 32 + r;
+    a1i[t] = p < n ? a1[p * 8 + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+}  // namespace
+
+void interleave_a1(const float* a1, int64_t n, float* a1i, cudaStream_t st) {
+    const int64_t groups = (n + 31) / 32;
+    if (groups <= 0) return;
+    interleave_a1_kernel<<<blocks_for(groups * 256, 256), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(a1), n, reinterpret_cast<float4*>(a1i), groups);
+    ADS_LAUNCH_CHECK();
+}
+
 void mask_assignment(const int32_t* dAssign, int64_t n, const uint8_t* dKeep, int k, int32_t* dOut,
                      cudaStream_t st) {
     if (n <= 0) return;

@@ -26,7 +26,7 @@ int main(int argc, char** argv) {
             save_hnsw(g, argv[7]);
             return 0;
         }
-        if (cmd == "query" && argc == 14) {
+        if (cmd == "query" && argc == 13) {
             const Dataset raw = read_fvecs(argv[3]), t = read_fvecs(argv[4]);
             const Dataset qr = read_fvecs(argv[5]), qt = read_fvecs(argv[6]);
             const HnswGraph g = load_hnsw(argv[2], raw, t);

@@ -91,7 +91,7 @@ def test_rawless_index_roundtrip(eng, ref, tmp_path):
     b = eng.ivf_query_batch(back, None, q, 20, 8, eng.IvfMode.kAdSplit)
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dims, b.dims)
-    with pytest.raises(RuntimeError):
+    with pytest.raises((RuntimeError, ValueError)):  # "cannot open .../centroids_raw.fvecs"
         ref.load_ivf(tmp_path / "c5")
 
 

@@ -516,3 +516,25 @@ def test_ivf_probe_range_and_initial_radius(eng, orc, probe_lo, rscale):
             assert int(res.dims[i]) == int(stats[0]), (mode, i)
     with pytest.raises(ValueError):
         eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, opts=eng.search_opts(probe_lo=nprobe + 1))
+
+
+@pytest.mark.parametrize("case", [(6000, 96, 24, 40, 8), (3000, 128, 16, 30, 32), (2500, 200, 12, 20, 48),
+                                  (4000, 64, 40, 64, 16)])
+def test_ivf_dense_prefix_phase_bitexact(eng, orc, case):
+    """IVF++ with a 32-float A1: the dense prefix phase (interleaved A1 copy, default)
+    == the lane walk without it (opts.tile = -1) == the oracle, at the batched and the
+    reference schedules, with Δd below, at and above d1."""
+    n, d, blobs, k, dd = case
+    raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 24, 300 + d)
+    lay = oracle_index(orc, raw, t, P, k, 301, d1=32)
+    idx = gpu_index(eng, lay, P)
+    cfg = eng.DcoConfig(2.1, dd)
+    for first, step in ((1, 1), (10, 64), (10, 7)):
+        for nprobe in (1, 5, k):
+            a = eng.ivf_query_batch(idx, qt, qr, 10, nprobe, eng.IvfMode.kAdSplit, cfg,
+                                    opts=eng.search_opts(first=first, step=step))
+            b = eng.ivf_query_batch(idx, qt, qr, 10, nprobe, eng.IvfMode.kAdSplit, cfg,
+                                    opts=eng.search_opts(first=first, step=step, tile=-1))
+            np.testing.assert_array_equal(a.ids, b.ids)
+            np.testing.assert_array_equal(a.dims, b.dims)
+            assert_same_results(a, orc, lay, qt, qr, 10, nprobe, "ad-split", 2.1, dd, first, step)
