@@ -851,8 +851,11 @@ static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& o
 
 // The interleaved A1 copy the scan's dense prefix phase reads (ivf.cu); call once the
 // index's A1 holds its final rows.
+// Only for long lists (>= 1024 rows on average, config 5's 6 100): a chunk's rows then
+// form one or two long runs and the dense phase measured +1-2 % (tools/ab_scan.py,
+// profiles/r02/ab_dense.log); with ~244-row lists (configs 2 and 3) it measured -1 %.
 static void ivf_finish_dense(ads_ivf* x, cudaStream_t st) {
-    if (x->layout == 1 && x->d1p == 32 && x->a1_t && !x->a1i_t) {
+    if (x->layout == 1 && x->d1p == 32 && x->a1_t && !x->a1i_t && x->n >= 1024LL * x->k) {
         const size_t groups = (static_cast<size_t>(x->n) + 31) / 32;
         ADS_CUDA(cudaMalloc(&x->a1i_t, sizeof(float) * 1024 * (groups > 0 ? groups : 1)));
         interleave_a1(x->a1_t, x->n, x->a1i_t, st);

@@ -177,3 +177,52 @@ def test_sharded_step_world1_vs_oracle(eng, orc, waves):
         ei, ed, m = shard_search_oracle(orc, lay, qt, qr, K, nprobe, "ad-split", K, step)
     np.testing.assert_array_equal(S.oi.cpu().numpy(), ei)
     np.testing.assert_array_equal(np.nan_to_num(S.od.cpu().numpy(), nan=-1), np.nan_to_num(ed, nan=-1))
+
+
+@pytest.mark.parametrize("waves", [0, 3])
+def test_sharded_step_two_gpus(eng, orc, tmp_path, waves):
+    """The product's sharded step across two GPUs over NCCL (runs when a 2-GPU lease
+    exists; this pool's gpurun leases one GPU) == the oracle's per-shard restricted
+    searches, the all-reduced bound and the (dist, id) merge."""
+    import subprocess
+    import sys
+
+    from helpers import make_fixture, oracle_index
+    from paper_2303_09855_b200.shard import partition_lists
+
+    if eng.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    procs = [subprocess.Popen([sys.executable, os.path.join(root, "tests", "dist_gpu_shard_worker.py"), str(r), "2",
+                               str(port), str(tmp_path), str(waves)]) for r in range(2)]
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    g0, g1 = np.load(tmp_path / "g0.npz"), np.load(tmp_path / "g1.npz")
+    np.testing.assert_array_equal(g0["ids"], g1["ids"])
+    raw, t, qr, qt, P = make_fixture(orc, 6000, 64, 20, 40, 51)
+    lay = oracle_index(orc, raw, t, P, 64, 52, d1=32)
+    owner = partition_lists(np.diff(lay["list_off"]), 2)
+    w = int(g0["w"])
+    parts_i, parts_d, R = [], [], np.full(qt.shape[0], np.inf)
+    subs = [numpy_subset(lay, owner, r) for r in range(2)]
+    if w:
+        for sub in subs:
+            _, d1, _ = shard_search_oracle(orc, sub, qt, qr, 10, w, "ad-split", 10, 64)
+            R = np.minimum(R, kth_distance(d1, 10))
+        np.testing.assert_array_equal(g0["R"], R)
+    for sub in subs:
+        if w:
+            i1, d1, _ = shard_search_oracle(orc, sub, qt, qr, 10, w, "ad-split", 10, 64)
+            i2, d2, _ = shard_search_oracle(orc, sub, qt, qr, 10, 16, "ad-split", 10, 64, probe_lo=w, r0=R)
+            parts_i += [i1, i2]
+            parts_d += [d1, d2]
+        else:
+            i1, d1, _ = shard_search_oracle(orc, sub, qt, qr, 10, 16, "ad-split", 10, 64)
+            parts_i.append(i1)
+            parts_d.append(d1)
+    ei, ed = merge_ref(np.stack(parts_d), np.stack(parts_i), 10)
+    np.testing.assert_array_equal(g0["ids"], ei)
+    np.testing.assert_array_equal(np.nan_to_num(g0["dists"], nan=-1), np.nan_to_num(ed, nan=-1))
