@@ -599,10 +599,14 @@ def sweep(S, cfg, args):
             rf = ads.ivf_query_batch(idx, None, q, cfg.K, np_, ads.IvfMode.kFd, opts=opts)
             row.update(fd_recall=recall_of(rf.ids, gt, cfg.K),
                        dims_frac=float(r1.dims.sum()) / float(rf.dims.sum()))
-        ctx.sync()
-        ctx.timer_start()
-        ads.ivf_query_batch(idx, None, q, cfg.K, np_, ads.IvfMode.kAdSplit, opts=opts)
-        row["e2e_qps"] = cfg.nq / (ctx.timer_stop() / 1e3)
+        ms = []
+        for _ in range(3):  # through the host API (H2D queries, D2H results inside), best of 3
+            ctx.flush_l2()
+            ctx.sync()
+            ctx.timer_start()
+            ads.ivf_query_batch(idx, None, q, cfg.K, np_, ads.IvfMode.kAdSplit, opts=opts)
+            ms.append(ctx.timer_stop())
+        row["e2e_qps"] = cfg.nq / (min(ms) / 1e3)
         if href is not None:
             ids, _, _, _ = href.query_batch(None, q[:nref], cfg.K, np_, "ad-split", nthreads=os.cpu_count(),
                                             P=m.entries)

@@ -35,7 +35,11 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 // cp.async (LDGSTS): global -> shared, bypassing L1 for 16-byte copies.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+#ifdef ADS_CP_ASYNC_CA
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

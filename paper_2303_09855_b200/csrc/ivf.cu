@@ -566,7 +566,22 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
             double* pend_d = pre_cur;
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
             int32_t* surv = reinterpret_cast<int32_t*>(pre_s + chunk_cap);  // DENSE: the idle half
-            for (int sl = threadIdx.x; sl < hi - lo; sl += blockDim.x) cpos[sl] = locate(lo + sl);
+            {  // slot -> flat position: each thread maps a contiguous run of slots with one search
+                const int n = hi - lo, per = (n + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
+                const int s0 = static_cast<int>(threadIdx.x) * per, s1 = min(n, s0 + per);
+                if (s0 < s1) {
+                    int l = 0, h = nl - 1;
+                    while (l < h) {
+                        const int mid = (l + h + 1) >> 1;
+                        if (pre[mid] <= lo + s0) l = mid;
+                        else h = mid - 1;
+                    }
+                    for (int sl = s0; sl < s1; ++sl) {
+                        while (pre[l + 1] <= lo + sl) ++l;
+                        cpos[sl] = lstart[l] + (lo + sl - pre[l]);
+                    }
+                }
+            }
             if (threadIdx.x == 0) {
                 sh.next = DENSE ? 0 : lo;
                 sh.pnext = 0;
@@ -718,11 +733,12 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                         cand = -1;
                     } else if (seg == a.nseg - 1) {  // d == D (dco.hpp:145; ivf.cpp:335-338)
                         my_dims += static_cast<unsigned long long>(a.D);
-                        const double dist = __dsqrt_rn(s);
-                        const bool positive = a.final_fd ? dist <= r : s <= r_sq;
+                        // kFd decides on dist <= r (ivf.cpp:337), the scans on s <= r^2
+                        // (dco.hpp:145); the root is taken only where it is needed
+                        const bool positive = a.final_fd ? __dsqrt_rn(s) <= r : s <= r_sq;
                         if (positive) {
                             const int slot = cand - lo;
-                            pend_d[slot] = dist;
+                            pend_d[slot] = __dsqrt_rn(s);
                             pend_i[slot] = a.ids[pos];
                             atomicOr(&pflag[slot >> 5], 1u << (slot & 31));
                         }
