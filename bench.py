@@ -331,7 +331,8 @@ def measure(S, cfg, nprobe, args, D, log, steps):
     mode = ads.IvfMode.kAdSplit
     opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True,
                            query_order=args.query_order, ctas_per_sm=args.ctas_per_sm,
-                           tile=-1 if getattr(args, "no_dense", False) else 64)
+                           tile=-1 if getattr(args, "no_dense", False) else 64,
+                           rotate_mode=getattr(args, "rotate_mode", 0), walk=getattr(args, "walk", 0))
     dq = ads.DeviceArray.from_host(ctx, q)
     outs = {nm: ads.DeviceArray(ctx, shape, dt) for nm, shape, dt in (
         ("ids", (nq, K), np.int32), ("dists", (nq, K), np.float64), ("cnt", (nq,), np.int32),
@@ -561,6 +562,7 @@ def extra_config(args, D, log, cid):
 
     a = copy.copy(args)
     a.config, a.nprobe, a.nq, a.kmeans_iters, a.kmeans_init, a.cfg_override = cid, 0, 0, 0, -1, ""
+    a.rotate_mode = 0
     cfg = config_for(a)
     S = setup(cfg, D, log)
     M = measure(S, cfg, cfg.nprobe, a, D, log, max(3, args.steps // 2))
@@ -569,6 +571,14 @@ def extra_config(args, D, log, cid):
            "recall_at_k": M["recall_at_k"], "e2e": M["e2e"], "roofline": M["roofline"],
            "stages_ms": M["stages_ms"], "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
            "gpu_fd": gpu_mode_line(S, cfg, cfg.nprobe, "fd")}
+    # north-star subsystem 1 delta: the same step with the queries rotated on the tensor
+    # cores (3xTF32, rotate_mode 1) instead of the exact fp64 rotation the default keeps
+    a.rotate_mode = 1
+    T = measure(S, cfg, cfg.nprobe, a, D, log, 3)
+    out["tc_rotation"] = {"value": T["value"], "rotate_ms": T["stages_ms"]["rotate"],
+                          "exact_rotate_ms": M["stages_ms"]["rotate"], "recall_at_k": T["recall_at_k"],
+                          "ids_equal_to_exact_rotation": bool(np.array_equal(T["ids"], M["ids"])),
+                          "note": "opt-in: results then follow the tensor-core-rotated queries (~1e-7 relative)"}
     del S
     gc.collect()
     return out
@@ -841,6 +851,8 @@ def main():
     ap.add_argument("--query-order", type=int, default=2,
                     help="2: longest queries first (default), 1: L2-locality order, 0: input order")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--walk", type=int, default=0,
+                    help="lane walk: 0 engine default, 1 exact fp64, 2 certified fp32 + exact re-walk")
     ap.add_argument("--no-dense", action="store_true",
                     help="A/B: the lane walk gathers A1 too (no dense prefix phase)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -52,7 +52,7 @@ class SearchOpts(C.Structure):
     _fields_ = [("first", i64), ("step", i64), ("warps_per_cta", i32), ("queries_per_cta", i32),
                 ("ctas_per_sm", i32), ("time_stages", i32), ("scheduler", i32), ("tile", i32),
                 ("query_order", i32), ("coarse_mode", i32), ("rotate_mode", i32),
-                ("probe_lo", i32), ("r0", vp)]
+                ("probe_lo", i32), ("r0", vp), ("walk", i32)]
 
 
 def _sig(name, args, res=C.c_int):

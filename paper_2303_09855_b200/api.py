@@ -522,7 +522,7 @@ def search_shape(d: int, step: int = 0, warps_per_cta: int = 0) -> tuple:
 def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
                 tile: int = 64, query_order: int = 2, coarse_mode: int = 0,
-                rotate_mode: int = 0, probe_lo: int = 0, r0=None) -> L.SearchOpts:
+                rotate_mode: int = 0, probe_lo: int = 0, r0=None, walk: int = 0) -> L.SearchOpts:
     """Search options (ads_search_opts, include/adsann_b200.h): first/step set the
     threshold refresh schedule in candidates; scheduler must be 0."""
     o = L.SearchOpts()
@@ -532,6 +532,7 @@ def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_p
     o.scheduler, o.tile, o.query_order, o.coarse_mode = scheduler, tile, query_order, coarse_mode
     o.rotate_mode = rotate_mode
     o.probe_lo = probe_lo
+    o.walk = walk
     if r0 is not None:  # per-query initial radii (host array for the host API)
         if isinstance(r0, DeviceArray):
             o.r0 = r0.ptr

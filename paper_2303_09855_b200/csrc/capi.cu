@@ -1260,6 +1260,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->rotate_mode = 0;
     o->probe_lo = 0;
     o->r0 = nullptr;
+    o->walk = 0;
 }
 
 namespace {
@@ -1413,6 +1414,11 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     // dense prefix phase (ivf.cu): IVF++ on the transformed split layout with a 32-float
     // A1 whose end is the first test point; opts.tile = -1 turns it off (A/B runs)
     a.a1i = (mode == ADS_MODE_AD_SPLIT && x->a1i_t && a.vec == 4 && o.tile >= 0) ? x->a1i_t : nullptr;
+    // certified fp32 walk (ivf.cu): requested with walk = 2 (walk 0 keeps the exact walk)
+    require(o.walk >= 0 && o.walk <= 2, "search: walk must be 0, 1 or 2");
+    // (4-warp CTAs: the kernel is held to 9 resident CTAs per SM, __launch_bounds__(128, 9))
+    a.f32 = (o.walk == 2 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT && o.warps_per_cta <= 4) ? 1 : 0;
+    if (a.f32) a.a1i = nullptr;
     // longest queries first; pointless when the whole batch is resident at once
     if (o.query_order == 2 && nq > 1 && nq > search_resident_ctas(a)) {
         int32_t* ord = x->order.get<int32_t>(nq);

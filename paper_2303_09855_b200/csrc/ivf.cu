@@ -16,6 +16,7 @@
 //                        with the reference's strict rule (ivf.cpp:273-280),
 //                        then thr[t] = factor[d_t] * r^2 is rebuilt.
 #include <cfloat>
+#include <type_traits>
 
 #include "engine.hpp"
 #include "scan_engine.cuh"
@@ -436,6 +437,9 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
     return true;
 }
 
+#ifndef F32_MIN_CTAS
+#define F32_MIN_CTAS 9  // the fp32 walk is held to 9 resident 4-warp CTAs per SM (56 registers)
+#endif
 #ifndef DENSE_PARTS
 #define DENSE_PARTS 1  // the prefix phase loads its 8 chunks in this many rounds (1: all in flight)
 #endif
@@ -454,8 +458,16 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
 // hands only the survivors to the lane walk, which resumes them at the first A2
 // segment with the carried prefix.  Sums and decisions are the same operations
 // in the same order, so results are unchanged bit for bit.
-template <int VEC, bool FULL, bool DENSE>
-__global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+// F32: the certified fp32 walk (scan_engine.cuh): lanes walk in fp32 with a proven
+// error band; a test decides only outside the band, and the chunk's undecided and
+// possibly-positive candidates are re-walked exactly in fp64 (one thread each, the
+// reference's order) before the merge.  Decisions, dims and distances are the exact
+// walk's.  Worth it where positives are rare among the candidates (config 5: ~0.1 %).
+template <int VEC, bool FULL, bool DENSE, bool F32>
+__global__ void ADS_SCAN_REGS __launch_bounds__(F32 ? 128 : 1024, F32 ? F32_MIN_CTAS : 1)
+    ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+    static_assert(!F32 || (VEC == 4 && FULL && !DENSE), "the fp32 walk runs on full 32-float lines");
+    using acc_t = typename std::conditional<F32, float, double>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SearchShared sh;
     const int nwarps = blockDim.x >> 5;
@@ -479,11 +491,22 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     // CTA-merge compaction counts: warp 0's gather line (idle at a chunk end)
     int* wc = reinterpret_cast<int*>(wbuf_all);
     unsigned* pflag = reinterpret_cast<unsigned*>(pre + a.nprobe + 1);
+    // F32: undecided slots of the chunk; the query staged as fp32 and the per-test band
+    // factors share qseg's slot
+    unsigned* vflag = pflag + ((chunk_cap + 31) >> 5);
+    float* qsegf = reinterpret_cast<float*>(qseg);
+    double2* gband = reinterpret_cast<double2*>(qsegf + a.nseg * kQPitchF);
+    const double2 band_d = F32 ? f32_band(a.D) : make_double2(0.0, 0.0);
+    const double nabs = (a.D + 2) * 0x1p-148;
 
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     float* wbuf = wbuf_all + warp * 1024;
-    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
+    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) {
+        const Seg sg = a.segs[i];
+        segs[i] = sg;
+        if (F32 && sg.test >= 0) gband[sg.test] = f32_band(sg.col + sg.len);
+    }
     for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) tfac[i] = a.tfac[i];
     // VEC=4 line descriptor = pos * stride + column offset, 16-byte units from a.a1
     const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
@@ -526,7 +549,8 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
         __syncthreads();
         if (sh.stop) break;
         const int qi = sh.q;
-        stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        if constexpr (F32) stage_query_f32(qsegf, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        else stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
         for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = __dmul_rn(tfac[i], sh.r_sq);
         if (warp == 0) {  // probed lists -> stream prefix offsets
             int carry = 0;
@@ -582,16 +606,28 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                     }
                 }
             }
+            // F32 with no finite radius yet (r = +inf before K results): every candidate
+            // would reach d == D undecided, so the chunk goes straight to the exact re-walk
+            const bool open = F32 && !(sh.r_sq < kInf);
             if (threadIdx.x == 0) {
-                sh.next = DENSE ? 0 : lo;
+                sh.next = DENSE ? 0 : (open ? hi : lo);
                 sh.pnext = 0;
                 sh.nsurv = 0;
             }
-            for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) pflag[w] = 0;
+            for (int w = threadIdx.x; w < (hi - lo + 31) / 32; w += blockDim.x) {
+                pflag[w] = 0;
+                if constexpr (F32) {
+                    const int rem = hi - lo - w * 32;
+                    vflag[w] = open ? (rem >= 32 ? ~0u : (1u << rem) - 1u) : 0u;
+                }
+            }
             __syncthreads();
             const double r = sh.r, r_sq = sh.r_sq;
-            const int pc = DENSE ? 0 : sh.pcount[j & 1];  // [lo, lo + pc) carry their prefix in pre_cur
-            const bool can_pre = !DENSE && nseg0 > 0 && nhi > hi;
+            const int pc = (DENSE || F32) ? 0 : sh.pcount[j & 1];  // [lo, lo + pc) carry their prefix in pre_cur
+            const bool can_pre = !DENSE && !F32 && nseg0 > 0 && nhi > hi;
+            // F32 final test: certainly negative above rfin (kFd: sqrt(s) > r is certain once
+            // s > r_sq (1 + 2^-47))
+            const double rfin = a.final_fd ? __dmul_rn(r_sq, 1.0 + 0x1p-47) : r_sq;
             if constexpr (DENSE) {
                 // tasks = (probed list, 32-row position group) pairs covering the chunk
                 auto list_of = [&](int i) {
@@ -654,7 +690,7 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
 
             int cand = -1, seg = 0, pos = 0;
             bool prew = false;  // lane holds a next-chunk candidate's untested prefix
-            double s = 0.0;
+            acc_t s = 0.0;
             for (;;) {
                 unsigned need = __ballot_sync(kFull, cand < 0);
                 if (need) {
@@ -670,7 +706,7 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                                 pos = cpos[slot];
                                 prew = false;
                                 seg = 1;
-                                s = pre_cur[slot];
+                                s = static_cast<acc_t>(pre_cur[slot]);
                             }
                         } else if (i < hi) {
                             cand = i;
@@ -678,7 +714,7 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                             prew = false;
                             if (i - lo < pc) {
                                 seg = nseg0;
-                                s = pre_cur[i - lo];
+                                s = static_cast<acc_t>(pre_cur[i - lo]);
                             } else {
                                 seg = 0;
                                 s = 0.0;
@@ -720,8 +756,33 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 cp_async_wait_group<0>();
                 __syncwarp();
                 if (cand >= 0) {
-                    s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
-                    if (prew) {
+                    if constexpr (F32) s = accumulate_line_f32(wbuf, qsegf + seg * kQPitchF, s);
+                    else s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                    if constexpr (F32) {
+                        // decide only what the band proves; the rest is re-walked exactly
+                        const double sd = s;
+                        int verdict = 0;  // 1 reject, 2 undecided, 3 certainly negative at D
+                        if (sg.test >= 0) {
+                            const double t = thr[sg.test];
+                            const double2 g = gband[sg.test];
+                            if (__dmul_rn(sd - nabs, g.x) > t) verdict = 1;
+                            else if (!(__dmul_rn(sd + nabs, g.y) <= t)) verdict = 2;
+                        }
+                        if (verdict == 0 && seg == a.nseg - 1) verdict = __dmul_rn(sd - nabs, band_d.x) > rfin ? 3 : 2;
+                        if (verdict == 1) {
+                            my_dims += static_cast<unsigned long long>(sg.col + sg.len);
+                            cand = -1;
+                        } else if (verdict == 3) {
+                            my_dims += static_cast<unsigned long long>(a.D);
+                            cand = -1;
+                        } else if (verdict == 2) {
+                            const int slot = cand - lo;
+                            atomicOr(&vflag[slot >> 5], 1u << (slot & 31));
+                            cand = -1;
+                        } else {
+                            ++seg;
+                        }
+                    } else if (prew) {
                         if (seg + 1 == nseg0) {
                             pre_nxt[cand] = s;
                             cand = -1;
@@ -749,6 +810,55 @@ __global__ void ADS_SCAN_REGS ivf_search_kernel(SearchLaunch a, int chunk_cap) {
                 }
             }
             __syncthreads();
+            if constexpr (F32) {
+                // exact re-walk of the undecided slots, one thread each, in the reference's
+                // order and arithmetic (dco.hpp:130-150; split resume at d1, ivf.cpp:389-400)
+                const int nw = (hi - lo + 31) >> 5;
+                int nv = 0;
+                for (int w = 0; w < nw; ++w) nv += __popc(vflag[w]);
+                for (int k = threadIdx.x; k < nv; k += blockDim.x) {
+                    int w = 0, c = k;
+                    for (;; ++w) {
+                        const int pcnt = __popc(vflag[w]);
+                        if (c < pcnt) break;
+                        c -= pcnt;
+                    }
+                    unsigned bits = vflag[w];
+                    for (; c > 0; --c) bits &= bits - 1;
+                    const int slot = w * 32 + __ffs(bits) - 1;
+                    const int64_t pos = cpos[slot];
+                    double se = 0.0;
+                    for (int g = 0; g < a.nseg; ++g) {
+                        const Seg sg = segs[g];
+                        const float* src = sg.arr == 0 ? a.a1 + pos * a.d1 + sg.col
+                                                       : a.a2 + pos * (a.D - a.d1) + (sg.col - a.d1);
+                        const float* qq = qsegf + g * kQPitchF;
+#pragma unroll
+                        for (int c4 = 0; c4 < 8; ++c4) {
+                            const float4 v = __ldg(reinterpret_cast<const float4*>(src) + c4);
+                            const float4 qv = *reinterpret_cast<const float4*>(qq + c4 * 4);
+                            se = sq_diff_acc(se, v.x, static_cast<double>(qv.x));
+                            se = sq_diff_acc(se, v.y, static_cast<double>(qv.y));
+                            se = sq_diff_acc(se, v.z, static_cast<double>(qv.z));
+                            se = sq_diff_acc(se, v.w, static_cast<double>(qv.w));
+                        }
+                        if (sg.test >= 0 && se > thr[sg.test]) {  // dco.hpp:141
+                            my_dims += static_cast<unsigned long long>(sg.col + sg.len);
+                            break;
+                        }
+                        if (g == a.nseg - 1) {  // dco.hpp:145; ivf.cpp:335-338
+                            my_dims += static_cast<unsigned long long>(a.D);
+                            const double dist = __dsqrt_rn(se);
+                            if (a.final_fd ? dist <= r : se <= r_sq) {
+                                pend_d[slot] = dist;
+                                pend_i[slot] = a.ids[pos];
+                                atomicOr(&pflag[slot >> 5], 1u << (slot & 31));
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+            }
             // offer the chunk's positives in candidate order: few -> one warp,
             // many -> the whole CTA, ties or oversize -> one by one
             const int n = hi - lo;
@@ -813,7 +923,7 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     b += sizeof(int32_t) * (a.nprobe + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + a.nprobe + 1);
-    b += sizeof(unsigned) * ((chunk_cap + 31) / 32);
+    b += sizeof(unsigned) * ((chunk_cap + 31) / 32) * (a.f32 ? 2 : 1);
     return b;
 }
 
@@ -944,11 +1054,13 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     SearchShape sh{};
     sh.cap = static_cast<int>(cap64);
     sh.smem = search_smem(a, sh.cap);
-    if (a.a1i)
-        sh.kern = a.full ? ivf_search_kernel<4, true, true> : ivf_search_kernel<4, false, true>;
+    if (a.f32 && a.vec == 4 && a.full)
+        sh.kern = ivf_search_kernel<4, true, false, true>;
+    else if (a.a1i)
+        sh.kern = a.full ? ivf_search_kernel<4, true, true, false> : ivf_search_kernel<4, false, true, false>;
     else
-        sh.kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true, false> : ivf_search_kernel<4, false, false>)
-                             : ivf_search_kernel<1, false, false>;
+        sh.kern = a.vec == 4 ? (a.full ? ivf_search_kernel<4, true, false, false> : ivf_search_kernel<4, false, false, false>)
+                             : ivf_search_kernel<1, false, false, false>;
     ADS_CUDA(cudaFuncSetAttribute(sh.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sh.smem)));
     ADS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sh.occ, sh.kern, a.warps * 32, sh.smem));

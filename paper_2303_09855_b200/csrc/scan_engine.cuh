@@ -132,6 +132,52 @@ __device__ __forceinline__ double accumulate_line(const float* wbuf, const doubl
     return s;
 }
 
+// Certified fp32 walk (ivf.cu, F32): the same line with an fp32 difference and a
+// fused square-add.  |s32 - S| and |s64 - S| are bounded relative to the exact sum S
+// (f32_band), so a test decides only outside the band; everything inside it, and
+// every candidate that may be positive at d = D, is re-walked in fp64.
+__device__ __forceinline__ float accumulate_line_f32(const float* wbuf, const float* qq, float s) {
+    const unsigned lane = lane_id();
+    const float* row = wbuf + lane * 32;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float4 v = *reinterpret_cast<const float4*>(row + (((c + static_cast<int>(lane)) & 7) << 2));
+        const float4 q = *reinterpret_cast<const float4*>(qq + c * 4);
+        float d = __fsub_rn(v.x, q.x);
+        s = __fmaf_rn(d, d, s);
+        d = __fsub_rn(v.y, q.y);
+        s = __fmaf_rn(d, d, s);
+        d = __fsub_rn(v.z, q.z);
+        s = __fmaf_rn(d, d, s);
+        d = __fsub_rn(v.w, q.w);
+        s = __fmaf_rn(d, d, s);
+    }
+    return s;
+}
+
+constexpr int kQPitchF = 36;  // floats per segment slot of the fp32-staged query
+
+__device__ __forceinline__ void stage_query_f32(float* qseg, const Seg* segs, int nseg, const float* q) {
+    for (int i = threadIdx.x; i < nseg * 32; i += blockDim.x) {
+        const int s = i >> 5, k = i & 31;
+        const Seg sg = segs[s];
+        if (k < sg.len) qseg[s * kQPitchF + k] = q[sg.col + k];
+    }
+}
+
+// Band factors at depth d (terms accumulated): with S the exact sum,
+// |s32 - S| <= g32 S + nabs and |s64 - S| <= g64 S, g(n, u) = n u / (1 - n u),
+// n = d + 2 (difference, square, d additions), nabs covering fp32 underflow.  A
+// test is certainly passed when (s32 + nabs) * hi <= thr and certainly failed when
+// (s32 - nabs) * lo > thr; lo / hi also absorb the rounding of those two fp64
+// operations (the 1 % widening of g32 dwarfs it).
+__device__ __forceinline__ double2 f32_band(int d) {
+    const double n = d + 2;
+    const double g32 = 1.01 * n * 0x1p-24 / (1.0 - n * 0x1p-24);
+    const double g64 = 1.01 * n * 0x1p-53 / (1.0 - n * 0x1p-53);
+    return make_double2((1.0 - g64) / (1.0 + g32) * (1.0 - 0x1p-50), (1.0 + g64) / (1.0 - g32) * (1.0 + 0x1p-50));
+}
+
 // Stage query coordinates per segment: qseg[s*34 + k] = (double)q[seg.col + k].
 __device__ __forceinline__ void stage_query(double* qseg, const Seg* segs, int nseg,
                                             const float* q) {

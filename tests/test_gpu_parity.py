@@ -538,3 +538,35 @@ def test_ivf_dense_prefix_phase_bitexact(eng, orc, case):
             np.testing.assert_array_equal(a.ids, b.ids)
             np.testing.assert_array_equal(a.dims, b.dims)
             assert_same_results(a, orc, lay, qt, qr, 10, nprobe, "ad-split", 2.1, dd, first, step)
+
+
+@pytest.mark.parametrize("case", [(6000, 96, 24, 40, 32), (3000, 128, 16, 30, 32), (2500, 256, 12, 20, 32),
+                                  (4000, 64, 40, 64, 32)])
+@pytest.mark.parametrize("K", [1, 10, 100])
+def test_ivf_certified_f32_walk_bitexact(eng, orc, case, K):
+    """walk = 2 (certified fp32 walk + exact fp64 re-walk of undecided / possibly
+    positive candidates) == the exact walk == the oracle, at the reference schedule
+    and batched schedules, including the first chunk at r = +inf and an initial
+    radius r0 (the sharded second wave)."""
+    n, d, blobs, k, dd = case
+    raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 24, 400 + d)
+    lay = oracle_index(orc, raw, t, P, k, 401, d1=32)
+    idx = gpu_index(eng, lay, P)
+    cfg = eng.DcoConfig(2.1, dd)
+    for first, step in ((1, 1), (K, 64), (K, 7)):
+        for nprobe in (1, 5, k):
+            a = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, cfg,
+                                    opts=eng.search_opts(first=first, step=step, walk=2))
+            b = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, cfg,
+                                    opts=eng.search_opts(first=first, step=step, walk=1))
+            np.testing.assert_array_equal(a.ids, b.ids)
+            np.testing.assert_array_equal(a.dims, b.dims)
+            np.testing.assert_array_equal(np.nan_to_num(a.dists, nan=-1), np.nan_to_num(b.dists, nan=-1))
+            assert_same_results(a, orc, lay, qt, qr, K, nprobe, "ad-split", 2.1, dd, first, step)
+    r0 = np.full(qt.shape[0], 0.5 * float(np.median(np.linalg.norm(t[:50] - qt[0], axis=1))))
+    a = eng.ivf_query_batch(idx, qt, qr, K, k, eng.IvfMode.kAdSplit, cfg,
+                            opts=eng.search_opts(first=K, step=64, walk=2, probe_lo=2, r0=r0))
+    b = eng.ivf_query_batch(idx, qt, qr, K, k, eng.IvfMode.kAdSplit, cfg,
+                            opts=eng.search_opts(first=K, step=64, walk=1, probe_lo=2, r0=r0))
+    np.testing.assert_array_equal(a.ids, b.ids)
+    np.testing.assert_array_equal(a.dims, b.dims)

@@ -19,7 +19,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
     args = argparse.Namespace(config=a.config, nq=0, kmeans_iters=0, kmeans_init=-1, cfg_override="", step=0,
-                              warps=0, query_order=2, ctas_per_sm=0, warmup=3, no_dense=False)
+                              warps=0, query_order=2, ctas_per_sm=0, warmup=3, no_dense=False, walk=0)
     D = bench.Dist()
     log = lambda *x: print(*x, file=sys.stderr, flush=True)  # noqa: E731
     cfg = bench.config_for(args)
@@ -31,6 +31,7 @@ def main():
             args.no_dense = "nodense" in v
             args.step = int(v.split("step=")[1].split("+")[0]) if "step=" in v else 0
             args.warps = int(v.split("warps=")[1].split("+")[0]) if "warps=" in v else 0
+            args.walk = 2 if "f32" in v else (1 if "exact" in v else 0)
             M = bench.measure(S, cfg, cfg.nprobe, args, D, log, a.steps)
             row = {"variant": v, "rep": rep, "qps": M["value"], "scan_ms": M["stages_ms"]["scan"],
                    "frac": M["roofline"]["frac"], "sm_mhz": M["clocks"]["sm_mhz"],
