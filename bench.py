@@ -753,10 +753,13 @@ def run_reference(args, D):
         q, gt, P = S["q"], S["gt"], S["m"].entries
         setup_note = "untimed setup on the GPU engine (data, rotation, k-means reproduced bit-exactly)"
     log(f"reference setup {time.time() - t0:.1f}s ({setup_note})")
-    # bounded sample per step: ~cpu_budget / (steps + warmup) seconds each
+    # bounded sample per step: ~cpu_budget / (steps + warmup) seconds each, but at least ~2 s
+    # (>= 64 queries per host thread) so the thread pool's tail does not dominate a step
     _, _, _, s = h.query_batch(None, q[:64], cfg.K, nprobe, "ad-split", nthreads=cores, P=P)
     per_q = s / 64
-    ns = int(max(64, min(cfg.nq, args.cpu_budget / max(1, args.steps + args.warmup) / per_q)))
+    per_step = max(2.0, args.cpu_budget / max(1, args.steps + args.warmup))
+    ns = int(max(64 * cores, min(cfg.nq, per_step / per_q)))
+    ns = min(ns, cfg.nq)
     for _ in range(args.warmup):
         h.query_batch(None, q[:ns], cfg.K, nprobe, "ad-split", nthreads=cores, P=P)
     secs, recs = [], []

@@ -307,7 +307,7 @@ typedef struct {
                               [w, n_probe) from the global bound. */
     int32_t walk;          /* lane walk of the IVF++ scan: 1 exact fp64; 2 certified fp32 walk with an exact
                               fp64 re-walk of every undecided or possibly positive candidate (results
-                              identical to the exact walk; 4-warp CTAs, 32-float segments); 0 (default)
+                              identical to the exact walk; 32-float segments); 0 (default)
                               picks 2 when a query streams >= 100 000 candidates on average, else 1 */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);

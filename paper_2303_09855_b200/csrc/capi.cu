@@ -1416,15 +1416,14 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.a1i = (mode == ADS_MODE_AD_SPLIT && x->a1i_t && a.vec == 4 && o.tile >= 0) ? x->a1i_t : nullptr;
     // certified fp32 walk (ivf.cu): requested with walk = 2 (walk 0 keeps the exact walk)
     require(o.walk >= 0 && o.walk <= 2, "search: walk must be 0, 1 or 2");
-    // (4-warp CTAs: the kernel is held to 9 resident CTAs per SM, __launch_bounds__(128, 9)).
     // walk 0 picks it when a query streams >= 100 000 candidates on average: positives, which
     // the fp32 walk must re-walk exactly, are then a small fraction of the stream (config 5:
     // 390 000 candidates, ~0.2 % positives, +5 %; config 2: 15 600 candidates, -1 to -3 %;
     // profiles/r02/ab_f32_walk.log)
     const double cand_per_query = static_cast<double>(x->n) / x->k * (nprobe - o.probe_lo);
     const bool want_f32 = o.walk == 2 || (o.walk == 0 && cand_per_query >= 100000.0);
-    a.f32 = (want_f32 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT && o.warps_per_cta <= 4) ? 1 : 0;
-    if (a.f32) a.a1i = nullptr;
+    a.f32 = (want_f32 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT) ? 1 : 0;
+
     // longest queries first; pointless when the whole batch is resident at once
     if (o.query_order == 2 && nq > 1 && nq > search_resident_ctas(a)) {
         int32_t* ord = x->order.get<int32_t>(nq);

@@ -437,17 +437,11 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
     return true;
 }
 
-#ifndef F32_MIN_CTAS
-#define F32_MIN_CTAS 9  // the fp32 walk is held to 9 resident 4-warp CTAs per SM (56 registers)
-#endif
 #ifndef DENSE_PARTS
 #define DENSE_PARTS 1  // the prefix phase loads its 8 chunks in this many rounds (1: all in flight)
 #endif
-#ifdef ADS_MAXNREG
-#define ADS_SCAN_REGS __maxnreg__(ADS_MAXNREG)
-#else
-#define ADS_SCAN_REGS
-#endif
+// Every scan variant is held to 56 registers: 9 resident 4-warp CTAs per SM (the
+// shared-memory limit too), 3 of the 10-warp CTAs used above D = 256.
 // Dense prefix phase (DENSE, IVF++ with a 32-float A1 over the transformed split
 // layout).  The reference computes every candidate's A1 prefix before any test
 // (ivf.cpp:366-386); no decision depends on those sums, and within a chunk the
@@ -464,9 +458,8 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
 // reference's order) before the merge.  Decisions, dims and distances are the exact
 // walk's.  Worth it where positives are rare among the candidates (config 5: ~0.1 %).
 template <int VEC, bool FULL, bool DENSE, bool F32>
-__global__ void ADS_SCAN_REGS __launch_bounds__(F32 ? 128 : 1024, F32 ? F32_MIN_CTAS : 1)
-    ivf_search_kernel(SearchLaunch a, int chunk_cap) {
-    static_assert(!F32 || (VEC == 4 && FULL && !DENSE), "the fp32 walk runs on full 32-float lines");
+__global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+    static_assert(!F32 || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
     using acc_t = typename std::conditional<F32, float, double>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SearchShared sh;
@@ -512,6 +505,7 @@ __global__ void ADS_SCAN_REGS __launch_bounds__(F32 ? 128 : 1024, F32 ? F32_MIN_
     const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
     const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
     const char* gbase = lane_base16(a.a1);
+    const GatherDst gdst = gather_dst(wbuf);
     // stream index -> flat position (last probed list with pre[l] <= i)
     const int nl = a.nprobe - a.probe_lo;  // lists scanned per query
     auto locate = [&](int i) {
@@ -628,7 +622,7 @@ __global__ void ADS_SCAN_REGS __launch_bounds__(F32 ? 128 : 1024, F32 ? F32_MIN_
             // F32 final test: certainly negative above rfin (kFd: sqrt(s) > r is certain once
             // s > r_sq (1 + 2^-47))
             const double rfin = a.final_fd ? __dmul_rn(r_sq, 1.0 + 0x1p-47) : r_sq;
-            if constexpr (DENSE) {
+            if (DENSE && !open) {
                 // tasks = (probed list, 32-row position group) pairs covering the chunk
                 auto list_of = [&](int i) {
                     int l = 0, h = nl - 1;
@@ -653,7 +647,7 @@ __global__ void ADS_SCAN_REGS __launch_bounds__(F32 ? 128 : 1024, F32 ? F32_MIN_
                         const int p = (g << 5) + static_cast<int>(lane);
                         const bool act = p >= pa && p < pb;
                         const float4* src = reinterpret_cast<const float4*>(a.a1i) + static_cast<int64_t>(g) * 256 + lane;
-                        double sa = 0.0;
+                        acc_t sa = 0.0;
 #pragma unroll
                         for (int h = 0; h < DENSE_PARTS; ++h) {
                             constexpr int PC = 8 / DENSE_PARTS;
@@ -663,22 +657,47 @@ __global__ void ADS_SCAN_REGS __launch_bounds__(F32 ? 128 : 1024, F32 ? F32_MIN_
                                 v[c] = act ? __ldg(src + (h * PC + c) * 32) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                             for (int c = 0; c < PC; ++c) {
-                                const double2 qa = q2[(h * PC + c) * 2], qb = q2[(h * PC + c) * 2 + 1];
-                                sa = sq_diff_acc(sa, v[c].x, qa.x);
-                                sa = sq_diff_acc(sa, v[c].y, qa.y);
-                                sa = sq_diff_acc(sa, v[c].z, qb.x);
-                                sa = sq_diff_acc(sa, v[c].w, qb.y);
+                                if constexpr (F32) {  // the certified fp32 walk's arithmetic
+                                    const float4 qf = reinterpret_cast<const float4*>(qsegf)[h * PC + c];
+                                    float df = __fsub_rn(v[c].x, qf.x);
+                                    sa = __fmaf_rn(df, df, sa);
+                                    df = __fsub_rn(v[c].y, qf.y);
+                                    sa = __fmaf_rn(df, df, sa);
+                                    df = __fsub_rn(v[c].z, qf.z);
+                                    sa = __fmaf_rn(df, df, sa);
+                                    df = __fsub_rn(v[c].w, qf.w);
+                                    sa = __fmaf_rn(df, df, sa);
+                                } else {
+                                    const double2 qa = q2[(h * PC + c) * 2], qb = q2[(h * PC + c) * 2 + 1];
+                                    sa = sq_diff_acc(sa, v[c].x, qa.x);
+                                    sa = sq_diff_acc(sa, v[c].y, qa.y);
+                                    sa = sq_diff_acc(sa, v[c].z, qb.x);
+                                    sa = sq_diff_acc(sa, v[c].w, qb.y);
+                                }
                             }
                         }
-                        const bool keep = act && !(sa > t1);  // reject iff s > thr at d1 (dco.hpp:129)
-                        if (act && !keep) my_dims += static_cast<unsigned long long>(segs[0].len);
+                        bool keep, drop;
+                        if constexpr (F32) {  // band decision at d1; undecided -> the exact re-walk
+                            const double sd = sa;
+                            const double2 gb = gband[segs[0].test];
+                            drop = act && __dmul_rn(sd - nabs, gb.x) > t1;
+                            keep = act && !drop && __dmul_rn(sd + nabs, gb.y) <= t1;
+                            if (act && !drop && !keep) {
+                                const int slot = as - lo + (p - pa);
+                                atomicOr(&vflag[slot >> 5], 1u << (slot & 31));
+                            }
+                        } else {
+                            keep = act && !(sa > t1);  // reject iff s > thr at d1 (dco.hpp:129)
+                            drop = act && !keep;
+                        }
+                        if (drop) my_dims += static_cast<unsigned long long>(segs[0].len);
                         const unsigned kb = __ballot_sync(kFull, keep);
                         int base = 0;
                         if (lane == 0 && kb) base = atomicAdd(&sh.nsurv, __popc(kb));
                         base = __shfl_sync(kFull, base, 0);
                         if (keep) {
                             const int slot = as - lo + (p - pa);
-                            pre_cur[slot] = sa;
+                            pre_cur[slot] = static_cast<double>(sa);
                             surv[base + __popc(kb & ((1u << lane) - 1u))] = slot;
                         }
                     }
@@ -747,7 +766,7 @@ __global__ void ADS_SCAN_REGS __launch_bounds__(F32 ? 128 : 1024, F32 ? F32_MIN_
                     if (cand >= 0)
                         dsc = sg.arr == 0 ? static_cast<uint32_t>(pos) * str1 + (sg.col >> 2)
                                           : static_cast<uint32_t>(pos) * str2 + a2c + (sg.col >> 2);
-                    gather_issue16<FULL>(wbuf, gbase, dsc, sg.len >> 2);
+                    gather_issue16<FULL>(gdst, gbase, dsc, sg.len >> 2);
                 } else {
                     const float* src = sg.arr == 0 ? a.a1 + static_cast<int64_t>(pos) * a.d1 + sg.col
                                                    : a.a2 + static_cast<int64_t>(pos) * (a.D - a.d1) + (sg.col - a.d1);
@@ -1055,7 +1074,7 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     sh.cap = static_cast<int>(cap64);
     sh.smem = search_smem(a, sh.cap);
     if (a.f32 && a.vec == 4 && a.full)
-        sh.kern = ivf_search_kernel<4, true, false, true>;
+        sh.kern = a.a1i ? ivf_search_kernel<4, true, true, true> : ivf_search_kernel<4, true, false, true>;
     else if (a.a1i)
         sh.kern = a.full ? ivf_search_kernel<4, true, true, false> : ivf_search_kernel<4, false, true, false>;
     else

@@ -49,8 +49,25 @@ __device__ __forceinline__ const char* lane_base16(const float* base) {
     return reinterpret_cast<const char*>(v);
 }
 
+// Per-lane shared-memory destinations of gather_issue16: the lane copies chunk c =
+// lane & 7 of line L = 4j + (lane >> 3) (j = 0..7) to wbuf + L*32 + ((c + L) & 7)*4
+// floats.  (c + L) & 7 takes two values as j runs (L steps by 4), so the byte offsets
+// are d[j & 1] + j * 512: two registers, computed once per kernel.
+struct GatherDst {
+    unsigned d0, d1;
+};
+__device__ __forceinline__ GatherDst gather_dst(const float* wbuf) {
+    const unsigned lane = lane_id(), c = lane & 7u, l0 = lane >> 3;
+    const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(wbuf)) + l0 * 128u;
+    return {base + (((c + l0) & 7u) << 4), base + (((c + l0 + 4u) & 7u) << 4)};
+}
+
+__device__ __forceinline__ void cp_async16_s(unsigned saddr, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
+}
+
 template <bool FULL>
-__device__ __forceinline__ void gather_issue16(float* wbuf, const char* bc, uint32_t desc, int nchunk) {
+__device__ __forceinline__ void gather_issue16(const GatherDst& dst, const char* bc, uint32_t desc, int nchunk) {
     const unsigned lane = lane_id();
     const int c = static_cast<int>(lane & 7u);
 #pragma unroll
@@ -60,8 +77,8 @@ __device__ __forceinline__ void gather_issue16(float* wbuf, const char* bc, uint
         int l = 8;
         if constexpr (!FULL) l = __shfl_sync(kFull, nchunk, L);
         if (dsc != kNoLine && c < l)
-            cp_async16(wbuf + L * 32 + (((c + L) & 7) << 2),
-                       reinterpret_cast<const float*>(bc + static_cast<uint64_t>(dsc) * 16u));
+            cp_async16_s(((j & 1) ? dst.d1 : dst.d0) + j * 512u,
+                         reinterpret_cast<const float*>(bc + static_cast<uint64_t>(dsc) * 16u));
     }
     cp_async_commit();
 }

@@ -570,3 +570,37 @@ def test_ivf_certified_f32_walk_bitexact(eng, orc, case, K):
                             opts=eng.search_opts(first=K, step=64, walk=1, probe_lo=2, r0=r0))
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dims, b.dims)
+
+
+def test_ivf_long_lists_default_path_bitexact(eng, orc):
+    """The default path at config 5's shape of work: 6 250-row lists (the interleaved A1
+    copy and its dense prefix phase) and 100 000 candidates per query (the certified fp32
+    walk), both picked automatically, == the exact walk without the dense phase == the
+    oracle on the exported index, at the batched schedule."""
+    n, d, k, nq, K, nprobe = 400_000, 96, 64, 24, 100, 16
+    m = eng.generate_orthogonal(d, 7)
+
+    def rows(lo, count, stride=1):
+        return eng.synth_rows(n, d, 256, 7, 1, lo, count, stride, kind=3, sigma=1.4)
+
+    idx, _, _ = eng.build_ivf_streamed(rows, n, d, m, k, 7, 32, 4, 40_000, chunk=100_000)
+    q = eng.synth_rows(1000, d, 256, 7, 2, 0, nq, 1, kind=3, sigma=1.4)
+    qt = eng.apply_dataset(m, q)
+    a = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit)
+    b = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit,
+                            opts=eng.search_opts(walk=1, tile=-1))
+    assert float(a.candidates.mean()) >= 100_000
+    np.testing.assert_array_equal(a.ids, b.ids)
+    np.testing.assert_array_equal(a.dims, b.dims)
+    np.testing.assert_array_equal(a.dists, b.dists)
+    ex = idx.export()
+    lay = {"n": idx.n, "d": d, "k": k, "d1": 32, "split": True, "centroids_t": ex["centroids_t"],
+           "centroids_raw": ex["centroids_t"], "list_off": ex["list_off"], "ids_flat": ex["ids_flat"],
+           "a1_t": ex["a1_t"], "a2_t": ex["a2_t"], "a1_raw": ex["a1_t"], "a2_raw": ex["a2_t"],
+           "vec_t": None, "vec_raw": None}
+    step = eng.search_shape(d)[0]
+    for i in range(nq):
+        ids, dists, stats = orc.ivf_query(lay, qt[i], qt[i], K, nprobe, "ad-split", 2.1, 32, K, step)
+        np.testing.assert_array_equal(a.ids[i], ids, err_msg=f"q={i}")
+        np.testing.assert_array_equal(a.dists[i], dists, err_msg=f"q={i}")
+        assert int(a.dims[i]) == int(stats[0]), i
