@@ -141,6 +141,7 @@ static void alloc_split_pair(size_t n, int d1p, int d2p, float** a1, float** a2)
 struct ads_ivf {
     ads_ctx* ctx = nullptr;
     int n = 0, d = 0, k = 0, d1 = 0, layout = 0, d1p = 0;
+    int nonempty = 0;  // lists holding rows (a shard's own lists): the scan heuristics' list length
     uint64_t seed = 0;
     bool has_raw = false;
     float *cent_t = nullptr, *cent_raw = nullptr;
@@ -855,7 +856,14 @@ static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& o
 // form one or two long runs and the dense phase measured +1-2 % (tools/ab_scan.py,
 // profiles/r02/ab_dense.log); with ~244-row lists (configs 2 and 3) it measured -1 %.
 static void ivf_finish_dense(ads_ivf* x, cudaStream_t st) {
-    if (x->layout == 1 && x->d1p == 32 && x->a1_t && !x->a1i_t && x->n >= 1024LL * x->k) {
+    {
+        std::vector<int64_t> off(static_cast<size_t>(x->k) + 1);
+        ADS_CUDA(cudaMemcpyAsync(off.data(), x->list_off, sizeof(int64_t) * off.size(), cudaMemcpyDeviceToHost, st));
+        ADS_CUDA(cudaStreamSynchronize(st));
+        x->nonempty = 0;
+        for (int c = 0; c < x->k; ++c) x->nonempty += off[c + 1] > off[c];
+    }
+    if (x->layout == 1 && x->d1p == 32 && x->a1_t && !x->a1i_t && x->n >= 1024LL * std::max(1, x->nonempty)) {
         const size_t groups = (static_cast<size_t>(x->n) + 31) / 32;
         ADS_CUDA(cudaMalloc(&x->a1i_t, sizeof(float) * 1024 * (groups > 0 ? groups : 1)));
         interleave_a1(x->a1_t, x->n, x->a1i_t, st);
@@ -1420,6 +1428,7 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     // the fp32 walk must re-walk exactly, are then a small fraction of the stream (config 5:
     // 390 000 candidates, ~0.2 % positives, +5 %; config 2: 15 600 candidates, -1 to -3 %;
     // profiles/r02/ab_f32_walk.log)
+    // (for a shard: its rows over all k lists, i.e. the candidates this rank streams)
     const double cand_per_query = static_cast<double>(x->n) / x->k * (nprobe - o.probe_lo);
     const bool want_f32 = o.walk == 2 || (o.walk == 0 && cand_per_query >= 100000.0);
     a.f32 = (want_f32 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT) ? 1 : 0;

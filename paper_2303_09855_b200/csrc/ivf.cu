@@ -489,6 +489,10 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
     unsigned* vflag = pflag + ((chunk_cap + 31) >> 5);
     float* qsegf = reinterpret_cast<float*>(qseg);
     double2* gband = reinterpret_cast<double2*>(qsegf + a.nseg * kQPitchF);
+    // F32: per-test fp32 decision thresholds (rebuilt with thr): s32 > rej32[t] is a
+    // certain rejection, s32 <= pas32[t] a certain pass (directed roundings, f32_cuts)
+    float* rej32 = reinterpret_cast<float*>(gband + (a.ntest > 0 ? a.ntest : 1));
+    float* pas32 = rej32 + (a.ntest > 0 ? a.ntest : 1);
     const double2 band_d = F32 ? f32_band(a.D) : make_double2(0.0, 0.0);
     const double nabs = (a.D + 2) * 0x1p-148;
 
@@ -505,7 +509,7 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
     const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
     const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
     const char* gbase = lane_base16(a.a1);
-    const GatherDst gdst = gather_dst(wbuf);
+    const GatherDst gdst = F32 ? gather_dst(wbuf) : GatherDst{0u, 0u};
     // stream index -> flat position (last probed list with pre[l] <= i)
     const int nl = a.nprobe - a.probe_lo;  // lists scanned per query
     auto locate = [&](int i) {
@@ -545,7 +549,10 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
         const int qi = sh.q;
         if constexpr (F32) stage_query_f32(qsegf, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
         else stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
-        for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) thr[i] = __dmul_rn(tfac[i], sh.r_sq);
+        for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) {
+            thr[i] = __dmul_rn(tfac[i], sh.r_sq);
+            if constexpr (F32) f32_cuts(thr[i], gband[i], nabs, rej32[i], pas32[i]);
+        }
         if (warp == 0) {  // probed lists -> stream prefix offsets
             int carry = 0;
             for (int base = 0; base < nl; base += 32) {  // probe ranks probe_lo .. nprobe-1
@@ -622,6 +629,8 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
             // F32 final test: certainly negative above rfin (kFd: sqrt(s) > r is certain once
             // s > r_sq (1 + 2^-47))
             const double rfin = a.final_fd ? __dmul_rn(r_sq, 1.0 + 0x1p-47) : r_sq;
+            float fin32 = 0.f, unused32 = 0.f;  // s32 > fin32: certainly negative at d = D
+            if constexpr (F32) f32_cuts(rfin, band_d, nabs, fin32, unused32);
             if (DENSE && !open) {
                 // tasks = (probed list, 32-row position group) pairs covering the chunk
                 auto list_of = [&](int i) {
@@ -678,10 +687,8 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
                         }
                         bool keep, drop;
                         if constexpr (F32) {  // band decision at d1; undecided -> the exact re-walk
-                            const double sd = sa;
-                            const double2 gb = gband[segs[0].test];
-                            drop = act && __dmul_rn(sd - nabs, gb.x) > t1;
-                            keep = act && !drop && __dmul_rn(sd + nabs, gb.y) <= t1;
+                            drop = act && sa > rej32[segs[0].test];
+                            keep = act && !drop && sa <= pas32[segs[0].test];
                             if (act && !drop && !keep) {
                                 const int slot = as - lo + (p - pa);
                                 atomicOr(&vflag[slot >> 5], 1u << (slot & 31));
@@ -766,7 +773,8 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
                     if (cand >= 0)
                         dsc = sg.arr == 0 ? static_cast<uint32_t>(pos) * str1 + (sg.col >> 2)
                                           : static_cast<uint32_t>(pos) * str2 + a2c + (sg.col >> 2);
-                    gather_issue16<FULL>(gdst, gbase, dsc, sg.len >> 2);
+                    if constexpr (F32) gather_issue16<FULL>(gdst, gbase, dsc, sg.len >> 2);
+                    else gather_issue16<FULL>(wbuf, gbase, dsc, sg.len >> 2);
                 } else {
                     const float* src = sg.arr == 0 ? a.a1 + static_cast<int64_t>(pos) * a.d1 + sg.col
                                                    : a.a2 + static_cast<int64_t>(pos) * (a.D - a.d1) + (sg.col - a.d1);
@@ -779,15 +787,12 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
                     else s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
                     if constexpr (F32) {
                         // decide only what the band proves; the rest is re-walked exactly
-                        const double sd = s;
                         int verdict = 0;  // 1 reject, 2 undecided, 3 certainly negative at D
                         if (sg.test >= 0) {
-                            const double t = thr[sg.test];
-                            const double2 g = gband[sg.test];
-                            if (__dmul_rn(sd - nabs, g.x) > t) verdict = 1;
-                            else if (!(__dmul_rn(sd + nabs, g.y) <= t)) verdict = 2;
+                            if (s > rej32[sg.test]) verdict = 1;
+                            else if (!(s <= pas32[sg.test])) verdict = 2;
                         }
-                        if (verdict == 0 && seg == a.nseg - 1) verdict = __dmul_rn(sd - nabs, band_d.x) > rfin ? 3 : 2;
+                        if (verdict == 0 && seg == a.nseg - 1) verdict = s > fin32 ? 3 : 2;
                         if (verdict == 1) {
                             my_dims += static_cast<unsigned long long>(sg.col + sg.len);
                             cand = -1;
@@ -906,7 +911,10 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
                 if (sh.cnt == a.K) {  // ivf.cpp:268-270; dco.hpp:125
                     const double rn = topd[a.K - 1];
                     const double rsq = __dmul_rn(rn, rn);
-                    for (int i = static_cast<int>(lane); i < a.ntest; i += 32) thr[i] = __dmul_rn(tfac[i], rsq);
+                    for (int i = static_cast<int>(lane); i < a.ntest; i += 32) {
+                        thr[i] = __dmul_rn(tfac[i], rsq);
+                        if constexpr (F32) f32_cuts(thr[i], gband[i], nabs, rej32[i], pas32[i]);
+                    }
                     if (lane == 0) {
                         sh.r = rn;
                         sh.r_sq = rsq;

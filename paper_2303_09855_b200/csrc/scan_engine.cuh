@@ -66,6 +66,25 @@ __device__ __forceinline__ void cp_async16_s(unsigned saddr, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
 }
 
+// The same with the destinations computed per copy (fewer live registers: the exact
+// walk of configs 2 / 3 measured 2 % faster this way, the fp32 walk 3 % slower).
+template <bool FULL>
+__device__ __forceinline__ void gather_issue16(float* wbuf, const char* bc, uint32_t desc, int nchunk) {
+    const unsigned lane = lane_id();
+    const int c = static_cast<int>(lane & 7u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int L = j * 4 + static_cast<int>(lane >> 3);
+        const uint32_t dsc = __shfl_sync(kFull, desc, L);
+        int l = 8;
+        if constexpr (!FULL) l = __shfl_sync(kFull, nchunk, L);
+        if (dsc != kNoLine && c < l)
+            cp_async16(wbuf + L * 32 + (((c + L) & 7) << 2),
+                       reinterpret_cast<const float*>(bc + static_cast<uint64_t>(dsc) * 16u));
+    }
+    cp_async_commit();
+}
+
 template <bool FULL>
 __device__ __forceinline__ void gather_issue16(const GatherDst& dst, const char* bc, uint32_t desc, int nchunk) {
     const unsigned lane = lane_id();
@@ -193,6 +212,15 @@ __device__ __forceinline__ double2 f32_band(int d) {
     const double g32 = 1.01 * n * 0x1p-24 / (1.0 - n * 0x1p-24);
     const double g64 = 1.01 * n * 0x1p-53 / (1.0 - n * 0x1p-53);
     return make_double2((1.0 - g64) / (1.0 + g32) * (1.0 - 0x1p-50), (1.0 + g64) / (1.0 - g32) * (1.0 + 0x1p-50));
+}
+
+// fp32 cut points of one test (threshold t, band g): a rejection is certain when
+// (s - nabs) g.x > t, i.e. s > t / g.x + nabs, and a pass when (s + nabs) g.y <= t, i.e.
+// s <= t / g.y - nabs.  rej / pas round those bounds outwards (up / down, fp64 then
+// fp32), so the two fp32 comparisons s32 > rej and s32 <= pas imply the exact ones.
+__device__ __forceinline__ void f32_cuts(double t, double2 g, double nabs, float& rej, float& pas) {
+    rej = __double2float_ru(__dadd_ru(__ddiv_ru(t, g.x), nabs));
+    pas = __double2float_rd(__dsub_rd(__ddiv_rd(t, g.y), nabs));
 }
 
 // Stage query coordinates per segment: qseg[s*34 + k] = (double)q[seg.col + k].
