@@ -282,7 +282,10 @@ typedef struct {
     int32_t ctas_per_sm;   /* 0 = occupancy maximum */
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */
     int32_t scheduler;     /* must be 0 (query-major, one CTA per query) */
-    int32_t tile;          /* reserved */
+    int32_t tile;          /* -1: no dense prefix phase (lane walk only); >= 0 (default 64): the
+                              IVF++ scan's dense A1 prefix phase where the index holds the
+                              interleaved A1 copy (long lists, d1 = 32).  Results do not depend
+                              on it. */
     int32_t query_order;   /* order in which the batch's queries are served; results do not
                               depend on it.  2 (default): longest first (descending candidate
                               count), which shortens the tail of the persistent scan grid;

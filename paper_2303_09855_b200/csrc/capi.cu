@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -855,6 +856,7 @@ static void centroid_prefilter(const float* dC, int k, int D, CoarseCentroids& o
 // Only for long lists (>= 1024 rows on average, config 5's 6 100): a chunk's rows then
 // form one or two long runs and the dense phase measured +1-2 % (tools/ab_scan.py,
 // profiles/r02/ab_dense.log); with ~244-row lists (configs 2 and 3) it measured -1 %.
+// ADS_DENSE_MIN_LIST overrides the 1024 (tests: 0 builds the copy for short lists too).
 static void ivf_finish_dense(ads_ivf* x, cudaStream_t st) {
     {
         std::vector<int64_t> off(static_cast<size_t>(x->k) + 1);
@@ -863,10 +865,12 @@ static void ivf_finish_dense(ads_ivf* x, cudaStream_t st) {
         x->nonempty = 0;
         for (int c = 0; c < x->k; ++c) x->nonempty += off[c + 1] > off[c];
     }
-    if (x->layout == 1 && x->d1p == 32 && x->a1_t && !x->a1i_t && x->n >= 1024LL * std::max(1, x->nonempty)) {
+    int64_t min_list = 1024;
+    if (const char* e = std::getenv("ADS_DENSE_MIN_LIST")) min_list = std::atoll(e);
+    if (x->layout == 1 && x->d1p == 32 && x->a1_t && !x->a1i_t && x->n >= min_list * std::max(1, x->nonempty)) {
         const size_t groups = (static_cast<size_t>(x->n) + 31) / 32;
         ADS_CUDA(cudaMalloc(&x->a1i_t, sizeof(float) * 1024 * (groups > 0 ? groups : 1)));
-        interleave_a1(x->a1_t, x->n, x->a1i_t, st);
+        interleave_rows(x->a1_t, x->n, 32, x->a1i_t, st);
     }
 }
 

@@ -21,10 +21,11 @@ struct DcoSmem {
 
 template <int VEC>
 __global__ void __launch_bounds__(kDcoWarps * 32) dco_fixed_kernel(DcoLaunch a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];  // gather rows: 128-byte aligned (swizzle)
     __shared__ DcoSmem sh;
     // dynamic smem: wbuf [warps*1024 floats] | qseg [nseg*33 doubles] | thr [ntest] | segs [nseg]
     float* wbuf_all = reinterpret_cast<float*>(smem_raw);
+    if (threadIdx.x == 0 && (__cvta_generic_to_shared(smem_raw) & 127u)) __trap();  // swizzle needs 128-B rows
     double* qseg = reinterpret_cast<double*>(wbuf_all + kDcoWarps * 1024);
     double* thr = qseg + a.nseg * kQPitch;
     Seg* segs = reinterpret_cast<Seg*>(thr + (a.ntest > 0 ? a.ntest : 1));

@@ -216,7 +216,9 @@ void gather_split(const float* src, const int32_t* dIds, int64_t n, int D, int d
                   float* a2, cudaStream_t st);
 // The A1 prefix (32 floats per row) re-blocked by 32-row position groups and
 // 16-byte chunks (dense coalesced reads of a list run's prefixes, ivf.cu).
-void interleave_a1(const float* a1, int64_t n, float* a1i, cudaStream_t st);
+// Rows of `width` floats (a multiple of 32) interleaved by 32-row position groups, 16-byte
+// chunk by chunk within each 32-float segment (the scan's dense phases, ivf.cu).
+void interleave_rows(const float* in, int64_t n, int width, float* out, cudaStream_t st);
 // out[i] = keep[asg[i]] ? asg[i] : k (lists a shard does not own sort after every owned one).
 void mask_assignment(const int32_t* dAssign, int64_t n, const uint8_t* dKeep, int k, int32_t* dOut,
                      cudaStream_t st);

@@ -16,6 +16,7 @@
 //                        with the reference's strict rule (ivf.cpp:273-280),
 //                        then thr[t] = factor[d_t] * r^2 is rebuilt.
 #include <cfloat>
+#include <climits>
 #include <type_traits>
 
 #include "engine.hpp"
@@ -458,15 +459,19 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
 // reference's order) before the merge.  Decisions, dims and distances are the exact
 // walk's.  Worth it where positives are rare among the candidates (config 5: ~0.1 %).
 template <int VEC, bool FULL, bool DENSE, bool F32>
-__global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+#ifndef SCAN_MAXNREG
+#define SCAN_MAXNREG 56
+#endif
+__global__ void __maxnreg__(SCAN_MAXNREG) ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     static_assert(!F32 || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
     using acc_t = typename std::conditional<F32, float, double>::type;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];  // gather rows: 128-byte aligned (swizzle)
     __shared__ SearchShared sh;
     const int nwarps = blockDim.x >> 5;
     // dynamic layout (8-byte items first)
     float* wbuf_all = reinterpret_cast<float*>(smem_raw);
     double* qseg = reinterpret_cast<double*>(wbuf_all + nwarps * 1024);
+    if (threadIdx.x == 0 && (__cvta_generic_to_shared(smem_raw) & 127u)) __trap();  // swizzle needs 128-B rows
     double* thr = qseg + a.nseg * kQPitch;
     double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
     double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
@@ -591,7 +596,12 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
             double* pend_d = pre_cur;
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
             int32_t* surv = reinterpret_cast<int32_t*>(pre_s + chunk_cap);  // DENSE: the idle half
-            {  // slot -> flat position: each thread maps a contiguous run of slots with one search
+            // F32 with no finite radius yet (r = +inf before K results): every candidate
+            // would reach d == D undecided, so the chunk goes straight to the exact re-walk
+            const bool open = F32 && !(sh.r_sq < kInf);
+            // slot -> flat position.  The dense prefix phase writes it for the rows it visits
+            // (every row of the chunk), so only the lane walks need this pass.
+            if (!DENSE || open) {  // each thread maps a contiguous run of slots with one search
                 const int n = hi - lo, per = (n + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
                 const int s0 = static_cast<int>(threadIdx.x) * per, s1 = min(n, s0 + per);
                 if (s0 < s1) {
@@ -607,9 +617,6 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
                     }
                 }
             }
-            // F32 with no finite radius yet (r = +inf before K results): every candidate
-            // would reach d == D undecided, so the chunk goes straight to the exact re-walk
-            const bool open = F32 && !(sh.r_sq < kInf);
             if (threadIdx.x == 0) {
                 sh.next = DENSE ? 0 : (open ? hi : lo);
                 sh.pnext = 0;
@@ -633,28 +640,30 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
             if constexpr (F32) f32_cuts(rfin, band_d, nabs, fin32, unused32);
             if (DENSE && !open) {
                 // tasks = (probed list, 32-row position group) pairs covering the chunk
-                auto list_of = [&](int i) {
-                    int l = 0, h = nl - 1;
-                    while (l < h) {
-                        const int mid = (l + h + 1) >> 1;
-                        if (pre[mid] <= i) l = mid;
-                        else h = mid - 1;
-                    }
-                    return l;
-                };
-                const int l0 = list_of(lo), l1 = list_of(hi - 1);
+                // probed lists holding the chunk's first and last rows (last l with
+                // pre[l] <= i; pre is non-decreasing): one ballot per 32 lists
+                int l0 = -1, l1 = -1;
+                for (int b = 0; b < nl; b += 32) {
+                    const int i = b + static_cast<int>(lane);
+                    const int pv = i < nl ? pre[i] : INT_MAX;
+                    l0 += __popc(__ballot_sync(kFull, pv <= lo));
+                    l1 += __popc(__ballot_sync(kFull, pv <= hi - 1));
+                }
                 const double t1 = thr[segs[0].test];
                 const double2* q2 = reinterpret_cast<const double2*>(qseg);
-                int t = 0;
+                // tasks = (probed list, 32-row position group) pairs in order, dealt round
+                // robin to the warps; off = this warp's first task within the next list
+                int off = warp;
                 for (int l = l0; l <= l1; ++l) {
                     const int as = max(lo, pre[l]), bs = min(hi, pre[l + 1]);
                     if (as >= bs) continue;
                     const int pa = lstart[l] + (as - pre[l]), pb = pa + (bs - as);
                     const int g0 = pa >> 5, g1 = (pb - 1) >> 5;
-                    const int tw = t + ((warp - t) % nwarps + nwarps) % nwarps;  // this warp's first task here
-                    for (int g = g0 + (tw - t); g <= g1; g += nwarps) {
+                    int g = g0 + off;
+                    for (; g <= g1; g += nwarps) {
                         const int p = (g << 5) + static_cast<int>(lane);
                         const bool act = p >= pa && p < pb;
+                        if (act) cpos[as - lo + (p - pa)] = p;  // the lane walk / exact re-walk read it
                         const float4* src = reinterpret_cast<const float4*>(a.a1i) + static_cast<int64_t>(g) * 256 + lane;
                         acc_t sa = 0.0;
 #pragma unroll
@@ -708,7 +717,7 @@ __global__ void __maxnreg__(56) ivf_search_kernel(SearchLaunch a, int chunk_cap)
                             surv[base + __popc(kb & ((1u << lane) - 1u))] = slot;
                         }
                     }
-                    t += g1 - g0 + 1;
+                    off = g - g1 - 1;
                 }
                 __syncthreads();
             }

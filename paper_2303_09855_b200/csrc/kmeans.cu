@@ -373,25 +373,30 @@ __global__ void mask_assignment_kernel(const int32_t* __restrict__ asg, int64_t 
 }  // namespace
 
 namespace {
-// a1i[((g * 8 + c) * 32 + r) * 4 + e] = a1[(g * 32 + r) * 32 + c * 4 + e]: position group
-// g's 32 rows interleaved by 16-byte chunk, so lane r of a warp reading chunk c of
-// rows 32g .. 32g+31 issues one contiguous 512-byte request (zeros past n).
-__global__ void interleave_a1_kernel(const float4* __restrict__ a1, int64_t n, float4* __restrict__ a1i,
-                                     int64_t groups) {
+// out[(((g * S + s) * 8 + c) * 32 + r) * 4 + e] = in[(g * 32 + r) * 32 S + s * 32 + c * 4 + e]
+// (rows of 32 S floats, S = 32-float segments per row): position group g's 32 rows
+// interleaved by 16-byte chunk, segment by segment, so lane r of a warp reading chunk c
+// of segment s of rows 32g .. 32g+31 issues one contiguous 512-byte request (zeros past n).
+__global__ void interleave_rows_kernel(const float4* __restrict__ in, int64_t n, int S,
+                                       float4* __restrict__ out, int64_t groups) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t >= groups * 256) return;
-    const int64_t g = t >> 8;
+    if (t >= groups * S * 256) return;
+    const int64_t gs = t >> 8;  // g * S + s
+    const int64_t g = gs / S;
+    const int s = static_cast<int>(gs - g * S);
     const int c = static_cast<int>((t >> 5) & 7), r = static_cast<int>(t & 31);
     const int64_t p = g * 32 + r;
-    a1i[t] = p < n ? a1[p * 8 + c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    out[t] = p < n ? in[(p * S + s) * 8 + c] : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 }  // namespace
 
-void interleave_a1(const float* a1, int64_t n, float* a1i, cudaStream_t st) {
+void interleave_rows(const float* in, int64_t n, int width, float* out, cudaStream_t st) {
     const int64_t groups = (n + 31) / 32;
-    if (groups <= 0) return;
-    interleave_a1_kernel<<<blocks_for(groups * 256, 256), 256, 0, st>>>(
-        reinterpret_cast<const float4*>(a1), n, reinterpret_cast<float4*>(a1i), groups);
+    if (groups <= 0 || width <= 0) return;
+    if (width % 32) throw std::invalid_argument("interleave_rows: width must be a multiple of 32");
+    const int S = width / 32;
+    interleave_rows_kernel<<<blocks_for(groups * S * 256, 256), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(in), n, S, reinterpret_cast<float4*>(out), groups);
     ADS_LAUNCH_CHECK();
 }
 

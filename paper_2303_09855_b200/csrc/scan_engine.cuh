@@ -7,8 +7,9 @@
 //      line for Δd = 32) are copied HBM -> shared memory with cp.async; eight
 //      lanes cover one line, so every load instruction reads four whole lines
 //      (coalesced, no sector is wasted).  Lines land in a per-warp 32 x 32-float
-//      buffer with a lane-rotated 16-byte chunk order so the per-lane reads
-//      below are bank-conflict free.  Gathers are asynchronous (one cp.async
+//      buffer (128-byte aligned) with an XOR-swizzled 16-byte chunk order (chunk c
+//      of line L at slot c ^ (L & 7)) so the per-lane reads below are bank-conflict
+//      free and each costs one LOP3 on the lane's row address.  Gathers are asynchronous (one cp.async
 //      group per buffer) so a warp can keep two buffers in flight.
 //   2. accumulate: each lane adds its segment in index order in fp64
 //      (sq_diff_acc), against the query stored per segment (34-double pitch).
@@ -50,16 +51,29 @@ __device__ __forceinline__ const char* lane_base16(const float* base) {
 }
 
 // Per-lane shared-memory destinations of gather_issue16: the lane copies chunk c =
-// lane & 7 of line L = 4j + (lane >> 3) (j = 0..7) to wbuf + L*32 + ((c + L) & 7)*4
-// floats.  (c + L) & 7 takes two values as j runs (L steps by 4), so the byte offsets
-// are d[j & 1] + j * 512: two registers, computed once per kernel.
+// lane & 7 of line L = 4j + (lane >> 3) (j = 0..7) to wbuf + L*32 + (c ^ (L & 7))*4
+// floats.  L & 7 = (lane >> 3) ^ 4 (j & 1), so the byte offsets are d[j & 1] + j * 512:
+// two registers, computed once per kernel.
 struct GatherDst {
     unsigned d0, d1;
 };
 __device__ __forceinline__ GatherDst gather_dst(const float* wbuf) {
     const unsigned lane = lane_id(), c = lane & 7u, l0 = lane >> 3;
     const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(wbuf)) + l0 * 128u;
-    return {base + (((c + l0) & 7u) << 4), base + (((c + l0 + 4u) & 7u) << 4)};
+    return {base + ((c ^ l0) << 4), base + ((c ^ l0 ^ 4u) << 4)};
+}
+
+// Shared address of the lane's row in the 128-byte-aligned gather buffer with the
+// swizzle key folded in: chunk c of the row is at row_key ^ (c << 4).
+__device__ __forceinline__ unsigned row_key(const float* wbuf) {
+    const unsigned lane = lane_id();
+    return static_cast<unsigned>(__cvta_generic_to_shared(wbuf)) + lane * 128u + ((lane & 7u) << 4);
+}
+
+__device__ __forceinline__ float4 lds128(unsigned addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
 }
 
 __device__ __forceinline__ void cp_async16_s(unsigned saddr, const void* gmem) {
@@ -79,7 +93,7 @@ __device__ __forceinline__ void gather_issue16(float* wbuf, const char* bc, uint
         int l = 8;
         if constexpr (!FULL) l = __shfl_sync(kFull, nchunk, L);
         if (dsc != kNoLine && c < l)
-            cp_async16(wbuf + L * 32 + (((c + L) & 7) << 2),
+            cp_async16(wbuf + L * 32 + ((c ^ (L & 7)) << 2),
                        reinterpret_cast<const float*>(bc + static_cast<uint64_t>(dsc) * 16u));
     }
     cp_async_commit();
@@ -126,7 +140,7 @@ __device__ __forceinline__ void gather_lines(float* wbuf, const float* src, int 
             const float* s = reinterpret_cast<const float*>(
                 __shfl_sync(kFull, reinterpret_cast<unsigned long long>(src), L));
             const int l = __shfl_sync(kFull, len, L);
-            if (c * 4 < l) cp_async16(wbuf + L * 32 + (((c + L) & 7) << 2), s + c * 4);
+            if (c * 4 < l) cp_async16(wbuf + L * 32 + ((c ^ (L & 7)) << 2), s + c * 4);
         }
     } else {
         for (int L = 0; L < 32; ++L) {
@@ -149,11 +163,11 @@ __device__ __forceinline__ double accumulate_line(const float* wbuf, const doubl
     const float* row = wbuf + lane * 32;
     if constexpr (VEC == 4) {
         const int nc = FULL ? 8 : len >> 2;
+        const unsigned rk = row_key(wbuf);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             if (FULL || c < nc) {
-                const float4 v =
-                    *reinterpret_cast<const float4*>(row + (((c + static_cast<int>(lane)) & 7) << 2));
+                const float4 v = lds128(rk ^ (static_cast<unsigned>(c) << 4));
                 const double2 q0 = *reinterpret_cast<const double2*>(qq + c * 4);
                 const double2 q1 = *reinterpret_cast<const double2*>(qq + c * 4 + 2);
                 s = sq_diff_acc(s, v.x, q0.x);
@@ -173,11 +187,10 @@ __device__ __forceinline__ double accumulate_line(const float* wbuf, const doubl
 // (f32_band), so a test decides only outside the band; everything inside it, and
 // every candidate that may be positive at d = D, is re-walked in fp64.
 __device__ __forceinline__ float accumulate_line_f32(const float* wbuf, const float* qq, float s) {
-    const unsigned lane = lane_id();
-    const float* row = wbuf + lane * 32;
+    const unsigned rk = row_key(wbuf);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-        const float4 v = *reinterpret_cast<const float4*>(row + (((c + static_cast<int>(lane)) & 7) << 2));
+        const float4 v = lds128(rk ^ (static_cast<unsigned>(c) << 4));
         const float4 q = *reinterpret_cast<const float4*>(qq + c * 4);
         float d = __fsub_rn(v.x, q.x);
         s = __fmaf_rn(d, d, s);

@@ -519,11 +519,13 @@ def test_ivf_probe_range_and_initial_radius(eng, orc, probe_lo, rscale):
 
 
 @pytest.mark.parametrize("case", [(6000, 96, 24, 40, 8), (3000, 128, 16, 30, 32), (2500, 200, 12, 20, 48),
-                                  (4000, 64, 40, 64, 16)])
-def test_ivf_dense_prefix_phase_bitexact(eng, orc, case):
-    """IVF++ with a 32-float A1: the dense prefix phase (interleaved A1 copy, default)
-    == the lane walk without it (opts.tile = -1) == the oracle, at the batched and the
-    reference schedules, with Δd below, at and above d1."""
+                                  (4000, 64, 40, 64, 16), (5000, 192, 16, 24, 32)])
+def test_ivf_dense_prefix_phase_bitexact(eng, orc, case, monkeypatch):
+    """IVF++ with a 32-float A1: the dense prefix phase (interleaved A1 copy, built here
+    for short lists with ADS_DENSE_MIN_LIST=0; default opts) == the lane walk without it
+    (opts.tile = -1) == the oracle, at the batched and the reference schedules, with Δd
+    below, at and above d1."""
+    monkeypatch.setenv("ADS_DENSE_MIN_LIST", "0")
     n, d, blobs, k, dd = case
     raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 24, 300 + d)
     lay = oracle_index(orc, raw, t, P, k, 301, d1=32)
@@ -531,23 +533,27 @@ def test_ivf_dense_prefix_phase_bitexact(eng, orc, case):
     cfg = eng.DcoConfig(2.1, dd)
     for first, step in ((1, 1), (10, 64), (10, 7)):
         for nprobe in (1, 5, k):
-            a = eng.ivf_query_batch(idx, qt, qr, 10, nprobe, eng.IvfMode.kAdSplit, cfg,
-                                    opts=eng.search_opts(first=first, step=step))
             b = eng.ivf_query_batch(idx, qt, qr, 10, nprobe, eng.IvfMode.kAdSplit, cfg,
                                     opts=eng.search_opts(first=first, step=step, tile=-1))
-            np.testing.assert_array_equal(a.ids, b.ids)
-            np.testing.assert_array_equal(a.dims, b.dims)
-            assert_same_results(a, orc, lay, qt, qr, 10, nprobe, "ad-split", 2.1, dd, first, step)
+            for tile in (64,):
+                a = eng.ivf_query_batch(idx, qt, qr, 10, nprobe, eng.IvfMode.kAdSplit, cfg,
+                                        opts=eng.search_opts(first=first, step=step, tile=tile))
+                np.testing.assert_array_equal(a.ids, b.ids)
+                np.testing.assert_array_equal(a.dims, b.dims)
+                np.testing.assert_array_equal(np.nan_to_num(a.dists, nan=-1), np.nan_to_num(b.dists, nan=-1))
+            assert_same_results(b, orc, lay, qt, qr, 10, nprobe, "ad-split", 2.1, dd, first, step)
 
 
 @pytest.mark.parametrize("case", [(6000, 96, 24, 40, 32), (3000, 128, 16, 30, 32), (2500, 256, 12, 20, 32),
                                   (4000, 64, 40, 64, 32)])
 @pytest.mark.parametrize("K", [1, 10, 100])
-def test_ivf_certified_f32_walk_bitexact(eng, orc, case, K):
+def test_ivf_certified_f32_walk_bitexact(eng, orc, case, K, monkeypatch):
     """walk = 2 (certified fp32 walk + exact fp64 re-walk of undecided / possibly
     positive candidates) == the exact walk == the oracle, at the reference schedule
     and batched schedules, including the first chunk at r = +inf and an initial
-    radius r0 (the sharded second wave)."""
+    radius r0 (the sharded second wave); with and without the dense prefix phase (the
+    interleaved A1 copy built with ADS_DENSE_MIN_LIST=0)."""
+    monkeypatch.setenv("ADS_DENSE_MIN_LIST", "0")
     n, d, blobs, k, dd = case
     raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 24, 400 + d)
     lay = oracle_index(orc, raw, t, P, k, 401, d1=32)
@@ -555,14 +561,15 @@ def test_ivf_certified_f32_walk_bitexact(eng, orc, case, K):
     cfg = eng.DcoConfig(2.1, dd)
     for first, step in ((1, 1), (K, 64), (K, 7)):
         for nprobe in (1, 5, k):
-            a = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, cfg,
-                                    opts=eng.search_opts(first=first, step=step, walk=2))
             b = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, cfg,
-                                    opts=eng.search_opts(first=first, step=step, walk=1))
-            np.testing.assert_array_equal(a.ids, b.ids)
-            np.testing.assert_array_equal(a.dims, b.dims)
-            np.testing.assert_array_equal(np.nan_to_num(a.dists, nan=-1), np.nan_to_num(b.dists, nan=-1))
-            assert_same_results(a, orc, lay, qt, qr, K, nprobe, "ad-split", 2.1, dd, first, step)
+                                    opts=eng.search_opts(first=first, step=step, walk=1, tile=-1))
+            for tile in (-1, 64):
+                a = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode.kAdSplit, cfg,
+                                        opts=eng.search_opts(first=first, step=step, walk=2, tile=tile))
+                np.testing.assert_array_equal(a.ids, b.ids)
+                np.testing.assert_array_equal(a.dims, b.dims)
+                np.testing.assert_array_equal(np.nan_to_num(a.dists, nan=-1), np.nan_to_num(b.dists, nan=-1))
+            assert_same_results(b, orc, lay, qt, qr, K, nprobe, "ad-split", 2.1, dd, first, step)
     r0 = np.full(qt.shape[0], 0.5 * float(np.median(np.linalg.norm(t[:50] - qt[0], axis=1))))
     a = eng.ivf_query_batch(idx, qt, qr, K, k, eng.IvfMode.kAdSplit, cfg,
                             opts=eng.search_opts(first=K, step=64, walk=2, probe_lo=2, r0=r0))
@@ -593,6 +600,12 @@ def test_ivf_long_lists_default_path_bitexact(eng, orc):
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dims, b.dims)
     np.testing.assert_array_equal(a.dists, b.dists)
+    for walk, tile in ((1, 64), (2, -1)):  # the dense phase with the exact walk, the fp32 walk alone
+        c = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit,
+                                opts=eng.search_opts(walk=walk, tile=tile))
+        np.testing.assert_array_equal(c.ids, b.ids)
+        np.testing.assert_array_equal(c.dims, b.dims)
+        np.testing.assert_array_equal(c.dists, b.dists)
     ex = idx.export()
     lay = {"n": idx.n, "d": d, "k": k, "d1": 32, "split": True, "centroids_t": ex["centroids_t"],
            "centroids_raw": ex["centroids_t"], "list_off": ex["list_off"], "ids_flat": ex["ids_flat"],
