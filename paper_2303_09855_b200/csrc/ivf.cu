@@ -441,8 +441,6 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
 #ifndef DENSE_PARTS
 #define DENSE_PARTS 1  // the prefix phase loads its 8 chunks in this many rounds (1: all in flight)
 #endif
-// Every scan variant is held to 56 registers: 9 resident 4-warp CTAs per SM (the
-// shared-memory limit too), 3 of the 10-warp CTAs used above D = 256.
 // Dense prefix phase (DENSE, IVF++ with a 32-float A1 over the transformed split
 // layout).  The reference computes every candidate's A1 prefix before any test
 // (ivf.cpp:366-386); no decision depends on those sums, and within a chunk the
@@ -459,10 +457,10 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
 // reference's order) before the merge.  Decisions, dims and distances are the exact
 // walk's.  Worth it where positives are rare among the candidates (config 5: ~0.1 %).
 template <int VEC, bool FULL, bool DENSE, bool F32>
-#ifndef SCAN_MAXNREG
-#define SCAN_MAXNREG 56
-#endif
-__global__ void __maxnreg__(SCAN_MAXNREG) ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+// Register caps (same-box A/B, profiles/r02/ab_regs.log): the certified fp32 walk at 56
+// (9 resident 4-warp CTAs per SM; 64 measured -2.5 % on config 5), the exact walk at 64
+// (8 CTAs; +3 to +4 % on configs 2 and 3, where the fp64 chains need the registers).
+__global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     static_assert(!F32 || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
     using acc_t = typename std::conditional<F32, float, double>::type;
     extern __shared__ __align__(128) unsigned char smem_raw[];  // gather rows: 128-byte aligned (swizzle)
