@@ -333,6 +333,7 @@ def measure(S, cfg, nprobe, args, D, log, steps):
                            query_order=args.query_order, ctas_per_sm=args.ctas_per_sm,
                            tile=-1 if getattr(args, "no_dense", False) else 64,
                            rotate_mode=getattr(args, "rotate_mode", 0), walk=getattr(args, "walk", 0))
+    plan = ads.search_plan(idx, K, nprobe, mode, opts=opts)
     dq = ads.DeviceArray.from_host(ctx, q)
     outs = {nm: ads.DeviceArray(ctx, shape, dt) for nm, shape, dt in (
         ("ids", (nq, K), np.int32), ("dists", (nq, K), np.float64), ("cnt", (nq,), np.int32),
@@ -433,8 +434,8 @@ def measure(S, cfg, nprobe, args, D, log, steps):
         "dims_per_query": float(dims.mean()),
         "dims_fraction": float(dims.mean()) / (float(cand.mean()) * d),
         "clocks": clk, "ids": ids,
-        "threshold_refresh": {"first": K, "step": ads.search_shape(d, args.step, args.warps)[0]},
-        "warps_per_cta": ads.search_shape(d, args.step, args.warps)[1],
+        "threshold_refresh": {"first": plan["first"], "step": plan["step"]},
+        "warps_per_cta": plan["warps_per_cta"], "walk": plan["walk"], "dense_prefix": plan["dense"],
     }
 
 

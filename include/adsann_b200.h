@@ -330,6 +330,13 @@ int ads_ivf_search_device(ads_ivf *idx, const float *dQ_t, const float *dQ_raw, 
                           int32_t delta_d, const ads_search_opts *opts, int32_t *dids,
                           double *ddists, int32_t *dcounts, uint64_t *ddims,
                           uint64_t *dcandidates);
+/* The scan schedule ads_ivf_search would use for these arguments (no search runs):
+ * the threshold refresh schedule (first, step: the oracle replays it), the CTA width,
+ * the lane walk (1 exact fp64, 2 certified fp32 + exact re-walk) and whether the dense
+ * A1 prefix phase runs.  Results depend on (first, step) only. */
+int ads_ivf_search_plan(ads_ivf *idx, int32_t K, int32_t nprobe, int32_t mode, double epsilon0,
+                        int32_t delta_d, const ads_search_opts *opts, int64_t *first, int64_t *step,
+                        int32_t *warps_per_cta, int32_t *walk, int32_t *dense);
 /* probe_order, ivf.cpp:283-292, batched: nprobe list ids per query. */
 int ads_ivf_probe_order(ads_ivf *idx, const float *Q, int32_t nq, int32_t nprobe,
                         int32_t transformed, int32_t *probes);

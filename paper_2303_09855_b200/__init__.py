@@ -11,5 +11,5 @@ from .api import (  # noqa: F401
     ad_context_factor, ad_sampling, apply, apply_dataset, apply_prefix, apply_transpose,
     brute_force_knn, build_ivf, dco_fixed, device_count, fd_scan, generate_orthogonal,
     ivf_mode_from_name, ivf_mode_name, ivf_query, ivf_query_batch, kmeans, pd_scan, recall,
-    recall_batch, rng_draw, search_opts, synth, synth_rows, threshold_multiplier, TheoryRow, verify_theory,
+    recall_batch, rng_draw, search_opts, search_plan, synth, synth_rows, threshold_multiplier, TheoryRow, verify_theory,
 )

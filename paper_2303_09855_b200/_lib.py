@@ -113,6 +113,8 @@ ads_ivf_search = _sig("ads_ivf_search", [vp, vp, vp, i32, i32, i32, i32, f64, i3
                                          C.POINTER(SearchOpts), vp, vp, vp, vp, vp])
 ads_ivf_search_device = _sig("ads_ivf_search_device", [vp, vp, vp, i32, i32, i32, i32, f64, i32,
                                                        C.POINTER(SearchOpts), vp, vp, vp, vp, vp])
+ads_ivf_search_plan = _sig("ads_ivf_search_plan", [vp, i32, i32, i32, f64, i32, C.POINTER(SearchOpts),
+                                                   vp, vp, vp, vp, vp])
 ads_ivf_probe_order = _sig("ads_ivf_probe_order", [vp, vp, i32, i32, i32, vp])
 ads_ivf_last_timings = _sig("ads_ivf_last_timings", [vp, vp])
 ads_ivf_coarse_stats = _sig("ads_ivf_coarse_stats", [vp, vp])

@@ -512,11 +512,19 @@ def recall_batch(ids: np.ndarray, gt: np.ndarray, K: int) -> float:
 # ---------------------------------------------------------------- IVF (GPU)
 
 
-def search_shape(d: int, step: int = 0, warps_per_cta: int = 0) -> tuple:
-    """The (step, warps_per_cta) the engine uses for scheduler 0 at dimension d
-    (0 = auto, as ads_search_opts documents)."""
-    w = warps_per_cta if warps_per_cta > 0 else (4 if d <= 256 else 10)
-    return (step if step > 0 else 64 * w), w
+def search_plan(idx: "IvfIndex", K: int, n_probe: int, mode: "IvfMode", cfg: "DcoConfig" = None,
+                opts: Optional[L.SearchOpts] = None) -> dict:
+    """The scan schedule a search with these arguments uses (ads_ivf_search_plan): the
+    threshold refresh schedule (first, step), warps_per_cta, walk (1 exact, 2 certified
+    fp32) and dense (the A1 prefix phase).  Results depend on (first, step) only."""
+    cfg = cfg or DcoConfig()
+    o = opts or search_opts()
+    first, step = C.c_int64(), C.c_int64()
+    warps, walk, dense = C.c_int32(), C.c_int32(), C.c_int32()
+    check(L.ads_ivf_search_plan(idx.h, K, n_probe, int(mode), cfg.epsilon0, cfg.delta_d, C.byref(o),
+                                C.byref(first), C.byref(step), C.byref(warps), C.byref(walk), C.byref(dense)))
+    return {"first": first.value, "step": step.value, "warps_per_cta": warps.value, "walk": walk.value,
+            "dense": bool(dense.value)}
 
 
 def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,

@@ -1322,22 +1322,83 @@ void validate_search(ads_ivf* x, bool has_qt, bool has_qraw, int32_t K, int32_t 
     }
 }
 
-void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq, int32_t K,
-                   int32_t nprobe, int32_t mode, double eps0, int32_t dd, const ads_search_opts* opts,
-                   int32_t* dids, double* ddists, int32_t* dcnt, uint64_t* ddims, uint64_t* dcand) {
+// Search options with their defaults resolved (all but the refresh step, which
+// plan_scan picks with the kernel).
+ads_search_opts resolve_opts(ads_ivf* x, int32_t K, int32_t nprobe, const ads_search_opts* opts) {
     ads_search_opts o;
     ads_search_opts_default(&o);
     if (opts) o = *opts;
     if (o.first <= 0) o.first = K;
     // auto launch shape: CTAs of 4 warps for D <= 256; wider CTAs amortise the
     // larger per-query shared state (staged query, chunk slots) at high D.
-    // The refresh interval follows the CTA: 64 candidates per warp.
     require(o.scheduler == 0, "search: scheduler must be 0 (query-major; the list-major scheduler was removed)");
     if (o.warps_per_cta <= 0) o.warps_per_cta = x->d <= 256 ? 4 : 10;
-    if (o.step <= 0) o.step = 64 * static_cast<int64_t>(o.warps_per_cta);
     require(o.warps_per_cta >= 1 && o.warps_per_cta <= 32, "search: warps_per_cta in [1, 32]");
     require(o.probe_lo >= 0 && o.probe_lo <= nprobe, "ivf_query: probe_lo must be in [0, n_probe]");
     require(o.queries_per_cta >= 1 && o.queries_per_cta <= 16, "search: queries_per_cta in [1, 16]");
+    return o;
+}
+
+// The scan's launch choices for one search (shared by search_device and
+// ads_ivf_search_plan): the index arrays, the segment plan, the dense prefix phase, the
+// lane walk and the threshold refresh schedule.  o has its defaults resolved except step.
+void plan_scan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0, int32_t dd,
+               const ads_search_opts& o, SearchLaunch& a) {
+    const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
+    const int D = x->d;
+    DevSegPlan& plan = ivf_plan(x, mode, eps0, dd);
+    a.a1 = transformed ? x->a1_t : x->a1_raw;
+    a.a2 = transformed ? x->a2_t : x->a2_raw;
+    a.d1 = x->d1p;
+    a.D = D;
+    a.ids = x->ids;
+    a.list_off = x->list_off;
+    a.nprobe = nprobe;
+    a.probe_lo = o.probe_lo;
+    a.final_fd = mode == ADS_MODE_FD;
+    a.segs = plan.segs;
+    a.tfac = plan.tfac;
+    a.nseg = plan.nseg;
+    a.ntest = plan.ntest;
+    a.vec = plan.vec;
+    a.full = plan.full;
+    // 16-byte line descriptors address A1|A2 (one allocation) in 32 bits of
+    // 16-byte units from a1.
+    const int64_t gap = a.a2 - a.a1;
+    const int64_t units = (gap + static_cast<int64_t>(x->n) * (D - x->d1p)) / 4;
+    a.a2_16 = static_cast<uint32_t>(gap / 4);
+    if (gap < 0 || gap % 4 != 0 || units >= int64_t(0xffffffff)) {
+        a.vec = 1;
+        a.full = 0;
+    }
+    a.warps = o.warps_per_cta;
+    // dense prefix phase (ivf.cu): IVF++ on the transformed split layout with a 32-float
+    // A1 whose end is the first test point (D > d1); opts.tile = -1 turns it off (A/B runs)
+    a.a1i = (mode == ADS_MODE_AD_SPLIT && x->a1i_t && a.vec == 4 && o.tile >= 0 && D > x->d1p) ? x->a1i_t : nullptr;
+    // certified fp32 walk (ivf.cu): requested with walk = 2 (walk 0 keeps the exact walk)
+    require(o.walk >= 0 && o.walk <= 2, "search: walk must be 0, 1 or 2");
+    // walk 0 picks it when a query streams >= 100 000 candidates on average: positives, which
+    // the fp32 walk must re-walk exactly, are then a small fraction of the stream (config 5:
+    // 390 000 candidates, ~0.2 % positives, +5 %; config 2: 15 600 candidates, -1 to -3 %;
+    // profiles/r02/ab_f32_walk.log)
+    // (for a shard: its rows over all k lists, i.e. the candidates this rank streams)
+    const double cand_per_query = static_cast<double>(x->n) / x->k * (nprobe - o.probe_lo);
+    const bool want_f32 = o.walk == 2 || (o.walk == 0 && cand_per_query >= 100000.0);
+    a.f32 = (want_f32 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT) ? 1 : 0;
+    // threshold refresh: first = K; step (candidates per chunk) by kernel shape, from
+    // same-box sweeps (profiles/r02/ab_rewalk_step, r02k): 64 per warp for the exact walk
+    // at D <= 256 (config 2: 384 / 512 measured -1 / -4 %), 96 per warp above (config 3:
+    // 960 +2.5 %, 1280 -12 %), 128 per warp for the dense + fp32 walk, whose compact
+    // chunk state keeps 9 CTAs per SM at 512 (config 5: +10 %; 768 +0.5 % at 8 CTAs)
+    a.first = o.first;
+    const int64_t per_warp = (a.a1i && a.f32) ? 128 : (D > 256 ? 96 : 64);
+    a.step = o.step > 0 ? o.step : per_warp * o.warps_per_cta;
+}
+
+void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq, int32_t K,
+                   int32_t nprobe, int32_t mode, double eps0, int32_t dd, const ads_search_opts* opts,
+                   int32_t* dids, double* ddists, int32_t* dcnt, uint64_t* ddims, uint64_t* dcand) {
+    const ads_search_opts o = resolve_opts(x, K, nprobe, opts);
     cudaStream_t st = x->ctx->stream;
     const bool transformed = mode == ADS_MODE_AD || mode == ADS_MODE_AD_SPLIT;
     const int D = x->d;
@@ -1380,40 +1441,13 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
         launch_select_probes(dist, nq, x->k, nprobe, probes, st);
     }
     if (x->timed) ADS_CUDA(cudaEventRecord(x->ev[3], st));
-    DevSegPlan& plan = ivf_plan(x, mode, eps0, dd);
     SearchLaunch a{};
-    a.a1 = transformed ? x->a1_t : x->a1_raw;
-    a.a2 = transformed ? x->a2_t : x->a2_raw;
-    a.d1 = x->d1p;
-    a.D = D;
-    a.ids = x->ids;
-    a.list_off = x->list_off;
+    plan_scan(x, K, nprobe, mode, eps0, dd, o, a);
     a.Q = Qs;
     a.nq = nq;
     a.probes = probes;
-    a.nprobe = nprobe;
-    a.probe_lo = o.probe_lo;
     a.r0 = o.r0;
     a.K = K;
-    a.final_fd = mode == ADS_MODE_FD;
-    a.segs = plan.segs;
-    a.tfac = plan.tfac;
-    a.nseg = plan.nseg;
-    a.ntest = plan.ntest;
-    a.vec = plan.vec;
-    a.full = plan.full;
-    // 16-byte line descriptors address A1|A2 (one allocation) in 32 bits of
-    // 16-byte units from a1.
-    const int64_t gap = a.a2 - a.a1;
-    const int64_t units = (gap + static_cast<int64_t>(x->n) * (D - x->d1p)) / 4;
-    a.a2_16 = static_cast<uint32_t>(gap / 4);
-    if (gap < 0 || gap % 4 != 0 || units >= int64_t(0xffffffff)) {
-        a.vec = 1;
-        a.full = 0;
-    }
-    a.first = o.first;
-    a.step = o.step;
-    a.warps = o.warps_per_cta;
     a.slots = o.queries_per_cta;
     a.ctas_per_sm = o.ctas_per_sm;
     a.out_ids = dids;
@@ -1423,19 +1457,6 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     a.out_cand = reinterpret_cast<unsigned long long*>(dcand);
     a.counter = x->ctx->counter;
     a.order = nullptr;
-    // dense prefix phase (ivf.cu): IVF++ on the transformed split layout with a 32-float
-    // A1 whose end is the first test point; opts.tile = -1 turns it off (A/B runs)
-    a.a1i = (mode == ADS_MODE_AD_SPLIT && x->a1i_t && a.vec == 4 && o.tile >= 0) ? x->a1i_t : nullptr;
-    // certified fp32 walk (ivf.cu): requested with walk = 2 (walk 0 keeps the exact walk)
-    require(o.walk >= 0 && o.walk <= 2, "search: walk must be 0, 1 or 2");
-    // walk 0 picks it when a query streams >= 100 000 candidates on average: positives, which
-    // the fp32 walk must re-walk exactly, are then a small fraction of the stream (config 5:
-    // 390 000 candidates, ~0.2 % positives, +5 %; config 2: 15 600 candidates, -1 to -3 %;
-    // profiles/r02/ab_f32_walk.log)
-    // (for a shard: its rows over all k lists, i.e. the candidates this rank streams)
-    const double cand_per_query = static_cast<double>(x->n) / x->k * (nprobe - o.probe_lo);
-    const bool want_f32 = o.walk == 2 || (o.walk == 0 && cand_per_query >= 100000.0);
-    a.f32 = (want_f32 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT) ? 1 : 0;
 
     // longest queries first; pointless when the whole batch is resident at once
     if (o.query_order == 2 && nq > 1 && nq > search_resident_ctas(a)) {
@@ -1462,6 +1483,24 @@ int ads_ivf_search_device(ads_ivf* x, const float* dQt, const float* dQraw, int3
         x->ctx->use();
         std::lock_guard<std::mutex> lk(x->ctx->mu);
         search_device(x, dQt, dQraw, nq, K, nprobe, mode, eps0, dd, opts, dids, ddists, dcnt, ddims, dcand);
+    });
+}
+
+int ads_ivf_search_plan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0, int32_t dd,
+                        const ads_search_opts* opts, int64_t* first, int64_t* step, int32_t* warps_per_cta,
+                        int32_t* walk, int32_t* dense) {
+    return guard([&] {
+        validate_search(x, true, true, K, nprobe, mode, eps0, dd);
+        x->ctx->use();
+        std::lock_guard<std::mutex> lk(x->ctx->mu);
+        const ads_search_opts o = resolve_opts(x, K, nprobe, opts);
+        SearchLaunch a{};
+        plan_scan(x, K, nprobe, mode, eps0, dd, o, a);
+        if (first) *first = a.first;
+        if (step) *step = a.step;
+        if (warps_per_cta) *warps_per_cta = a.warps;
+        if (walk) *walk = a.f32 ? 2 : 1;
+        if (dense) *dense = a.a1i ? 1 : 0;
     });
 }
 

@@ -456,10 +456,24 @@ __device__ bool warp_merge_chunk(double* topd, int32_t* topi, SearchShared& sh, 
 // possibly-positive candidates are re-walked exactly in fp64 (one thread each, the
 // reference's order) before the merge.  Decisions, dims and distances are the exact
 // walk's.  Worth it where positives are rare among the candidates (config 5: ~0.1 %).
-template <int VEC, bool FULL, bool DENSE, bool F32>
+// Per-slot chunk state of the search kernel (see the layout there), in 8-byte words.
+__host__ __device__ inline bool pend_in_wbuf(bool dense, bool f32, int cap, int nwarps) {
+    return dense && f32 && 8 * cap + 1024 <= 4096 * nwarps;
+}
+__host__ __device__ inline int slot_bytes_before_surv(bool dense, bool f32, int cap, int nwarps) {
+    const int pre_b = (f32 ? 4 : 8) * cap;
+    const int pend_b = (f32 && !pend_in_wbuf(dense, f32, cap, nwarps)) ? 8 * cap : 0;
+    return ((pre_b + 7) & ~7) + pend_b;
+}
+__host__ __device__ inline int slot_words(bool dense, bool f32, int cap, int nwarps) {
+    if (!dense) return 2 * cap;
+    return (slot_bytes_before_surv(dense, f32, cap, nwarps) + 2 * cap + 7) / 8;
+}
+
 // Register caps (same-box A/B, profiles/r02/ab_regs.log): the certified fp32 walk at 56
 // (9 resident 4-warp CTAs per SM; 64 measured -2.5 % on config 5), the exact walk at 64
 // (8 CTAs; +3 to +4 % on configs 2 and 3, where the fp64 chains need the registers).
+template <int VEC, bool FULL, bool DENSE, bool F32>
 __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int chunk_cap) {
     static_assert(!F32 || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
     using acc_t = typename std::conditional<F32, float, double>::type;
@@ -473,11 +487,24 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
     double* thr = qseg + a.nseg * kQPitch;
     double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
     double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
-    // 2 x chunk_cap: untested-prefix sums, by chunk parity.  A chunk's positives'
-    // distances reuse its own prefix half (pend_d = pre_cur): a slot's prefix is
-    // consumed when the slot is claimed, before it can turn positive.
+    // Per-slot chunk state (slot_words, shared with search_smem).  Lane walk alone: 2 x
+    // chunk_cap untested-prefix sums, by chunk parity; a chunk's positives' distances
+    // reuse its own prefix half (pend_d = pre_cur): a slot's prefix is consumed when the
+    // slot is claimed, before it can turn positive.  DENSE: the survivors' prefixes
+    // (acc_t; the exact walk's double prefix doubles as pend_d) and the survivor list
+    // (16-bit slots); the fp32 walk's pend_d lives in the gather lines past warp 0's
+    // first kilobyte (idle once the lane walk ends: positives come only from the exact
+    // re-walk) when they hold it.
     double* pre_s = topd + a.K;
-    int32_t* lstart = reinterpret_cast<int32_t*>(pre_s + 2 * chunk_cap);
+    acc_t* dpre = reinterpret_cast<acc_t*>(pre_s);
+    const bool pend_wbuf = pend_in_wbuf(DENSE, F32, chunk_cap, nwarps);
+    const int pre_b = static_cast<int>(sizeof(acc_t)) * chunk_cap;
+    double* dpend = !F32 ? pre_s
+                         : (pend_wbuf ? reinterpret_cast<double*>(wbuf_all + 256)
+                                      : reinterpret_cast<double*>(reinterpret_cast<char*>(pre_s) + ((pre_b + 7) & ~7)));
+    uint16_t* surv = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(pre_s) +
+                                                 slot_bytes_before_surv(DENSE, F32, chunk_cap, nwarps));
+    int32_t* lstart = reinterpret_cast<int32_t*>(pre_s + slot_words(DENSE, F32, chunk_cap, nwarps));
     int32_t* cpos = lstart + a.nprobe;
     Seg* segs = reinterpret_cast<Seg*>(cpos + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
@@ -590,10 +617,9 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
             const int64_t span = lo == 0 ? a.first : a.step;
             const int hi = static_cast<int>(lo + span < total ? lo + span : total);
             const int nhi = static_cast<int>(hi + a.step < total ? hi + a.step : total);  // next chunk [hi, nhi)
-            double* pre_cur = DENSE ? pre_s : pre_s + (j & 1) * chunk_cap;
-            double* pend_d = pre_cur;
+            double* pre_cur = pre_s + (j & 1) * chunk_cap;  // lane walk alone (!DENSE)
+            double* pend_d = DENSE ? dpend : pre_cur;
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
-            int32_t* surv = reinterpret_cast<int32_t*>(pre_s + chunk_cap);  // DENSE: the idle half
             // F32 with no finite radius yet (r = +inf before K results): every candidate
             // would reach d == D undecided, so the chunk goes straight to the exact re-walk
             const bool open = F32 && !(sh.r_sq < kInf);
@@ -711,8 +737,8 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                         base = __shfl_sync(kFull, base, 0);
                         if (keep) {
                             const int slot = as - lo + (p - pa);
-                            pre_cur[slot] = static_cast<double>(sa);
-                            surv[base + __popc(kb & ((1u << lane) - 1u))] = slot;
+                            dpre[slot] = sa;
+                            surv[base + __popc(kb & ((1u << lane) - 1u))] = static_cast<uint16_t>(slot);
                         }
                     }
                     off = g - g1 - 1;
@@ -739,7 +765,7 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                                 pos = cpos[slot];
                                 prew = false;
                                 seg = 1;
-                                s = static_cast<acc_t>(pre_cur[slot]);
+                                s = dpre[slot];
                             }
                         } else if (i < hi) {
                             cand = i;
@@ -952,8 +978,9 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
 
 size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
+    const bool dense = a.a1i != nullptr, f32 = a.f32 && a.vec == 4 && a.full;
     size_t b = sizeof(float) * a.warps * 1024;
-    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + 2 * chunk_cap);
+    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + slot_words(dense, f32, chunk_cap, a.warps));
     b += sizeof(int32_t) * (a.nprobe + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + a.nprobe + 1);

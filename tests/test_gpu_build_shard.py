@@ -112,7 +112,7 @@ def test_config5_shape_search_vs_oracle(eng, orc):
     lay = _lay_from_export(idx.export(), idx.n, d, k)
     K, nprobe = cfg.K, cfg.nprobe
     res = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit)
-    step = eng.search_shape(d)[0]
+    step = eng.search_plan(idx, K, nprobe, eng.IvfMode.kAdSplit)["step"]
     for i in range(nq):
         ids, dists, stats = orc.ivf_query(lay, qt[i], qt[i], K, nprobe, "ad-split", 2.1, 32, K, step)
         c = int(res.counts[i])

@@ -34,7 +34,7 @@ def test_full_size_vs_oracle(eng, orc, cfgid, nq):
     K, nprobe = cfg.K, cfg.nprobe
     for mode in ("ad-split", "fd"):
         res = eng.ivf_query_batch(idx, qt, q, K, nprobe, eng.IvfMode(MODE_ID[mode]))
-        step = eng.search_shape(cfg.d)[0]
+        step = eng.search_plan(idx, K, nprobe, eng.IvfMode(MODE_ID[mode]))["step"]
         for i in range(q.shape[0]):
             ids, dists, stats = orc.ivf_query(lay, qt[i], q[i], K, nprobe, mode, 2.1, 32, K, step)
             c = int(res.counts[i])

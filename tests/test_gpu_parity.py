@@ -611,7 +611,9 @@ def test_ivf_long_lists_default_path_bitexact(eng, orc):
            "centroids_raw": ex["centroids_t"], "list_off": ex["list_off"], "ids_flat": ex["ids_flat"],
            "a1_t": ex["a1_t"], "a2_t": ex["a2_t"], "a1_raw": ex["a1_t"], "a2_raw": ex["a2_t"],
            "vec_t": None, "vec_raw": None}
-    step = eng.search_shape(d)[0]
+    plan = eng.search_plan(idx, K, nprobe, eng.IvfMode.kAdSplit)
+    assert plan["walk"] == 2 and plan["dense"]  # the default path at config 5's shape
+    step = plan["step"]
     for i in range(nq):
         ids, dists, stats = orc.ivf_query(lay, qt[i], qt[i], K, nprobe, "ad-split", 2.1, 32, K, step)
         np.testing.assert_array_equal(a.ids[i], ids, err_msg=f"q={i}")
