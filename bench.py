@@ -540,6 +540,7 @@ def run_search(args, D):
         "stages_ms": M["stages_ms"], "dims_per_query": M["dims_per_query"],
         "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
         "threshold_refresh": M["threshold_refresh"], "warps_per_cta": M["warps_per_cta"],
+        "walk": M["walk"], "dense_prefix": M["dense_prefix"],
         "setup": S["info"],
     }
     if D.rank == 0 and args.mode == "search":

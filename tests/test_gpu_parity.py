@@ -593,16 +593,19 @@ def test_ivf_long_lists_default_path_bitexact(eng, orc):
     idx, _, _ = eng.build_ivf_streamed(rows, n, d, m, k, 7, 32, 4, 40_000, chunk=100_000)
     q = eng.synth_rows(1000, d, 256, 7, 2, 0, nq, 1, kind=3, sigma=1.4)
     qt = eng.apply_dataset(m, q)
+    plan = eng.search_plan(idx, K, nprobe, eng.IvfMode.kAdSplit)
+    assert plan["walk"] == 2 and plan["dense"]  # the default path at config 5's shape
+    step = plan["step"]
     a = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit)
     b = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit,
-                            opts=eng.search_opts(walk=1, tile=-1))
+                            opts=eng.search_opts(walk=1, tile=-1, step=step))
     assert float(a.candidates.mean()) >= 100_000
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dims, b.dims)
     np.testing.assert_array_equal(a.dists, b.dists)
     for walk, tile in ((1, 64), (2, -1)):  # the dense phase with the exact walk, the fp32 walk alone
         c = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit,
-                                opts=eng.search_opts(walk=walk, tile=tile))
+                                opts=eng.search_opts(walk=walk, tile=tile, step=step))
         np.testing.assert_array_equal(c.ids, b.ids)
         np.testing.assert_array_equal(c.dims, b.dims)
         np.testing.assert_array_equal(c.dists, b.dists)
@@ -611,9 +614,6 @@ def test_ivf_long_lists_default_path_bitexact(eng, orc):
            "centroids_raw": ex["centroids_t"], "list_off": ex["list_off"], "ids_flat": ex["ids_flat"],
            "a1_t": ex["a1_t"], "a2_t": ex["a2_t"], "a1_raw": ex["a1_t"], "a2_raw": ex["a2_t"],
            "vec_t": None, "vec_raw": None}
-    plan = eng.search_plan(idx, K, nprobe, eng.IvfMode.kAdSplit)
-    assert plan["walk"] == 2 and plan["dense"]  # the default path at config 5's shape
-    step = plan["step"]
     for i in range(nq):
         ids, dists, stats = orc.ivf_query(lay, qt[i], qt[i], K, nprobe, "ad-split", 2.1, 32, K, step)
         np.testing.assert_array_equal(a.ids[i], ids, err_msg=f"q={i}")
