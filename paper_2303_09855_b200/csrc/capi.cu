@@ -488,6 +488,9 @@ void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int6
     a.nseg = dp.nseg;
     a.ntest = dp.ntest;
     a.vec = dp.vec;
+    // 16-byte line descriptors from X (one 32-bit offset per line, shuffled once per copy)
+    a.desc = (dp.vec == 4 && dp.full && (reinterpret_cast<uintptr_t>(b.X) & 15) == 0 &&
+              b.n_rows * static_cast<int64_t>(b.dim) / 4 < int64_t(0xffffffff)) ? 1 : 0;
     a.positive = b.positive;
     a.dims = b.dims;
     a.dist_sq = b.dist_sq;

@@ -11,6 +11,9 @@ namespace ads {
 namespace {
 
 constexpr int kDcoWarps = 4;
+#ifndef DCO_MIN_CTAS
+#define DCO_MIN_CTAS 8  // resident CTAs per SM the descriptor kernel is compiled for (<= 64 registers)
+#endif
 
 struct DcoSmem {
     double r, r_sq;
@@ -19,8 +22,10 @@ struct DcoSmem {
     int stop;
 };
 
-template <int VEC>
-__global__ void __launch_bounds__(kDcoWarps * 32) dco_fixed_kernel(DcoLaunch a) {
+// DESC: lines addressed by 32-bit descriptors (row * D/4 + col/4, 16-byte units from X)
+// and gathered asynchronously like the IVF scan (gather_issue16), every segment 32 floats.
+template <int VEC, bool DESC>
+__global__ void __launch_bounds__(kDcoWarps * 32, DESC ? DCO_MIN_CTAS : 1) dco_fixed_kernel(DcoLaunch a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];  // gather rows: 128-byte aligned (swizzle)
     __shared__ DcoSmem sh;
     // dynamic smem: wbuf [warps*1024 floats] | qseg [nseg*33 doubles] | thr [ntest] | segs [nseg]
@@ -34,6 +39,8 @@ __global__ void __launch_bounds__(kDcoWarps * 32) dco_fixed_kernel(DcoLaunch a) 
     const unsigned lane = lane_id();
     float* wbuf = wbuf_all + warp * 1024;
     for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
+    const char* gbase = lane_base16(a.X);
+    const uint32_t rstr = static_cast<uint32_t>(a.D) >> 2;
 
     for (;;) {
         __syncthreads();
@@ -95,10 +102,18 @@ __global__ void __launch_bounds__(kDcoWarps * 32) dco_fixed_kernel(DcoLaunch a) 
             }
             if (!__any_sync(kFull, j >= 0)) break;
             Seg sg = segs[seg];
-            const float* src = a.X + row * a.D + sg.col;
-            gather_lines<VEC>(wbuf, src, j >= 0 ? sg.len : 0);
+            if constexpr (DESC) {
+                const uint32_t dsc = j >= 0 ? static_cast<uint32_t>(row) * rstr + (static_cast<uint32_t>(sg.col) >> 2)
+                                            : kNoLine;
+                gather_issue16<true>(wbuf, gbase, dsc, 8);
+                cp_async_wait_group<0>();
+                __syncwarp();
+            } else {
+                const float* src = a.X + row * a.D + sg.col;
+                gather_lines<VEC>(wbuf, src, j >= 0 ? sg.len : 0);
+            }
             if (j >= 0) {
-                s = accumulate_line<VEC>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                s = accumulate_line<VEC, DESC>(wbuf, qseg + seg * kQPitch, sg.len, s);
                 const int d = sg.col + sg.len;
                 bool done = false, pos = false;
                 double obs = 0.0;
@@ -165,7 +180,8 @@ void launch_prefix_sums(const float* X, int D, const float* q, const int64_t* ca
 void launch_dco_fixed(const DcoLaunch& a, cudaStream_t st) {
     const size_t smem = sizeof(float) * kDcoWarps * 1024 + sizeof(double) * a.nseg * kQPitch +
                         sizeof(double) * (a.ntest > 0 ? a.ntest : 1) + sizeof(Seg) * a.nseg;
-    auto kern = a.vec == 4 ? dco_fixed_kernel<4> : dco_fixed_kernel<1>;
+    auto kern = a.vec == 4 ? (a.desc ? dco_fixed_kernel<4, true> : dco_fixed_kernel<4, false>)
+                           : dco_fixed_kernel<1, false>;
     ADS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int occ = 0;

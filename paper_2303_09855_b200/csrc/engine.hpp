@@ -60,6 +60,7 @@ struct DcoLaunch {
     const Seg* segs;
     const double* tfac;
     int nseg, ntest, vec;
+    int desc;                  // 1: 32-bit line descriptors (VEC 4, n_rows * D / 4 < 2^32), full 32-float segments
     uint8_t* positive;
     int32_t* dims;
     double* dist_sq;
