@@ -155,6 +155,8 @@ typedef struct {
     uint64_t *dims_per_query; /* nq sums of dims (the roofline byte counter) */
 } ads_dco_batch;
 int ads_dco_fixed(ads_ctx *ctx, const ads_dco_batch *b);
+/* Device pointers; enqueued on the context's stream (window mode returns before the
+ * kernel ends: ads_ctx_sync or a stream-ordered read follows). */
 int ads_dco_fixed_device(ads_ctx *ctx, const ads_dco_batch *b);
 /* The partial squared distances every DCO kind tests, for a batch of rows against one
  * query: dout[c * nb + t] = S_{min((t+1) delta_d, dim)} of row dcand[c] (nb =

@@ -467,10 +467,19 @@ void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int6
     require(b.dim >= 1, "dco: dimension must be >= 1");
     require(b.nq >= 0, "dco: nq must be >= 0");
     require(b.kind >= 0 && b.kind <= 2, "dco: unknown kind");
-    const SegPlan plan = dco_plan(b.kind, b.dim, b.epsilon0, b.delta_d);
     cudaStream_t st = ctx->stream;
-    DevSegPlan dp;
-    dp.upload(plan, st);
+    // segment plans are cached per (kind, D, eps0, delta_d) like ads_dco's: a batch call
+    // then costs its kernel and nothing else on the device
+    const int D = b.dim, dd = b.kind == ADS_DCO_FD ? D : b.delta_d;
+    const auto key = std::make_tuple(b.kind, D, b.kind == ADS_DCO_AD ? b.epsilon0 : 0.0, b.kind == ADS_DCO_FD ? 0 : dd);
+    auto it = ctx->dco_plans.find(key);
+    if (it == ctx->dco_plans.end()) {
+        const SegPlan plan = dco_plan(b.kind, b.dim, b.epsilon0, b.delta_d);
+        auto up = std::make_unique<DevSegPlan>();
+        up->upload(plan, st);
+        it = ctx->dco_plans.emplace(key, std::move(up)).first;
+    }
+    const DevSegPlan& dp = *it->second;
     DcoLaunch a{};
     a.X = b.X;
     a.n_rows = b.n_rows;
@@ -530,8 +539,7 @@ void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int6
     }
     if (b.dims_per_query) ADS_CUDA(cudaMemsetAsync(b.dims_per_query, 0, sizeof(uint64_t) * b.nq, st));
     if (a.ntiles > 0) launch_dco_fixed(a, st);
-    ADS_CUDA(cudaStreamSynchronize(st));  // dp / tile table are freed below
-    dp.release();
+    if (b.cand_rows) ADS_CUDA(cudaStreamSynchronize(st));  // the tile table is freed below
 }
 
 }  // namespace
@@ -539,6 +547,7 @@ void run_dco_device(ads_ctx* ctx, const ads_dco_batch& b, const std::vector<int6
 int ads_dco_fixed_device(ads_ctx* ctx, const ads_dco_batch* b) {
     return guard([&] {
         ctx->use();
+        std::lock_guard<std::mutex> lk(ctx->mu);  // the context's plan cache
         std::vector<int64_t> off;
         if (b->cand_rows) {
             off.resize(static_cast<size_t>(b->nq) + 1);
@@ -553,6 +562,7 @@ int ads_dco_fixed_device(ads_ctx* ctx, const ads_dco_batch* b) {
 int ads_dco_fixed(ads_ctx* ctx, const ads_dco_batch* hb) {
     return guard([&] {
         ctx->use();
+        std::lock_guard<std::mutex> lk(ctx->mu);  // the context's plan cache
         cudaStream_t st = ctx->stream;
         const ads_dco_batch& b = *hb;
         require(b.dim >= 1 && b.nq >= 0 && b.n_rows >= 0, "dco: bad shape");

@@ -609,6 +609,16 @@ def test_ivf_long_lists_default_path_bitexact(eng, orc):
         np.testing.assert_array_equal(c.ids, b.ids)
         np.testing.assert_array_equal(c.dims, b.dims)
         np.testing.assert_array_equal(c.dists, b.dists)
+    # chunk-state edge shapes of the dense + fp32 kernel: odd chunk caps, and chunks too
+    # long for the pending distances to live in the gather lines (8 * cap + 1 KiB > 16 KiB)
+    for first, st in ((99, 333), (K, 2048), (K, 4099)):
+        c = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit,
+                                opts=eng.search_opts(first=first, step=st))
+        e = eng.ivf_query_batch(idx, qt, None, K, nprobe, eng.IvfMode.kAdSplit,
+                                opts=eng.search_opts(first=first, step=st, walk=1, tile=-1))
+        np.testing.assert_array_equal(c.ids, e.ids)
+        np.testing.assert_array_equal(c.dims, e.dims)
+        np.testing.assert_array_equal(c.dists, e.dists)
     ex = idx.export()
     lay = {"n": idx.n, "d": d, "k": k, "d1": 32, "split": True, "centroids_t": ex["centroids_t"],
            "centroids_raw": ex["centroids_t"], "list_off": ex["list_off"], "ids_flat": ex["ids_flat"],
