@@ -332,7 +332,7 @@ def measure(S, cfg, nprobe, args, D, log, steps):
     opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True,
                            query_order=args.query_order, ctas_per_sm=args.ctas_per_sm,
                            tile=-1 if getattr(args, "no_dense", False) else 64,
-                           rotate_mode=getattr(args, "rotate_mode", 0), walk=getattr(args, "walk", 0))
+                           rotate_mode=getattr(args, "rotate_mode", 2), walk=getattr(args, "walk", 0))
     plan = ads.search_plan(idx, K, nprobe, mode, opts=opts)
     dq = ads.DeviceArray.from_host(ctx, q)
     outs = {nm: ads.DeviceArray(ctx, shape, dt) for nm, shape, dt in (
@@ -541,6 +541,7 @@ def run_search(args, D):
         "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
         "threshold_refresh": M["threshold_refresh"], "warps_per_cta": M["warps_per_cta"],
         "walk": M["walk"], "dense_prefix": M["dense_prefix"],
+        "query_rotation": "raw queries rotated on the device each step: 3xTF32 tcgen05 (rotate_mode 2)",
         "setup": S["info"],
     }
     if D.rank == 0 and args.mode == "search":
@@ -564,7 +565,7 @@ def extra_config(args, D, log, cid):
 
     a = copy.copy(args)
     a.config, a.nprobe, a.nq, a.kmeans_iters, a.kmeans_init, a.cfg_override = cid, 0, 0, 0, -1, ""
-    a.rotate_mode = 0
+    a.rotate_mode = 2
     cfg = config_for(a)
     S = setup(cfg, D, log)
     M = measure(S, cfg, cfg.nprobe, a, D, log, max(3, args.steps // 2))
@@ -573,14 +574,15 @@ def extra_config(args, D, log, cid):
            "recall_at_k": M["recall_at_k"], "e2e": M["e2e"], "roofline": M["roofline"],
            "stages_ms": M["stages_ms"], "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
            "gpu_fd": gpu_mode_line(S, cfg, cfg.nprobe, "fd")}
-    # north-star subsystem 1 delta: the same step with the queries rotated on the tensor
-    # cores (3xTF32, rotate_mode 1) instead of the exact fp64 rotation the default keeps
-    a.rotate_mode = 1
+    # north-star subsystem 1 delta: the default rotates the query batch on the tensor cores
+    # (3xTF32 tcgen05, rotate_mode 2); the same step with the exact fp64 rotation (0), whose
+    # results are bit-identical to the reference's on the same raw queries
+    a.rotate_mode = 0
     T = measure(S, cfg, cfg.nprobe, a, D, log, 3)
-    out["tc_rotation"] = {"value": T["value"], "rotate_ms": T["stages_ms"]["rotate"],
-                          "exact_rotate_ms": M["stages_ms"]["rotate"], "recall_at_k": T["recall_at_k"],
-                          "ids_equal_to_exact_rotation": bool(np.array_equal(T["ids"], M["ids"])),
-                          "note": "opt-in: results then follow the tensor-core-rotated queries (~1e-7 relative)"}
+    out["exact_rotation"] = {"value": T["value"], "rotate_ms": T["stages_ms"]["rotate"],
+                             "tc_rotate_ms": M["stages_ms"]["rotate"], "recall_at_k": T["recall_at_k"],
+                             "ids_equal_to_tc_rotation": bool(np.array_equal(T["ids"], M["ids"])),
+                             "note": "rotate_mode 0; the line's value rotates on the tensor cores (~1e-7 relative)"}
     del S
     gc.collect()
     return out

@@ -299,9 +299,12 @@ typedef struct {
                               top-nprobe; 2: the same with the fp32-FMA GEMM; 1: exact fp64
                               distance to every centroid.  All give probe_order's exact (d2, id)
                               order. */
-    int32_t rotate_mode;   /* when the queries come untransformed (Q_t == NULL): 0 (default) exact
-                              fp64 rotation, bit-identical to apply(); 1 the 3xTF32 tensor-core
-                              rotation of ads_apply_dataset_tc (~1e-6 |q|; D % 4 == 0, D >= 32) */
+    int32_t rotate_mode;   /* when the queries come untransformed (Q_t == NULL): 2 (default) the
+                              3xTF32 tensor-core rotation of ads_apply_dataset_tc for batches of >= 64
+                              queries with D % 4 == 0 and D >= 32 (~1e-7 relative of the exact
+                              rotation; results then follow those queries), else the exact one;
+                              0 the exact fp64 rotation, bit-identical to apply(); 1 always the
+                              tensor cores (D % 4 == 0, D >= 32) */
     int32_t probe_lo;      /* scan only the lists at probe ranks probe_lo .. n_probe-1
                               (default 0) */
     const double *r0;      /* nullable: per-query initial radius (a distance); r starts
@@ -313,7 +316,7 @@ typedef struct {
     int32_t walk;          /* lane walk of the IVF++ scan: 1 exact fp64; 2 certified fp32 walk with an exact
                               fp64 re-walk of every undecided or possibly positive candidate (results
                               identical to the exact walk; 32-float segments); 0 (default)
-                              picks 2 when a query streams >= 100 000 candidates on average, else 1 */
+                              picks 2 when a query streams >= 32 000 candidates on average, else 1 */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 

@@ -530,7 +530,7 @@ def search_plan(idx: "IvfIndex", K: int, n_probe: int, mode: "IvfMode", cfg: "Dc
 def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
                 tile: int = 64, query_order: int = 2, coarse_mode: int = 0,
-                rotate_mode: int = 0, probe_lo: int = 0, r0=None, walk: int = 0) -> L.SearchOpts:
+                rotate_mode: int = 2, probe_lo: int = 0, r0=None, walk: int = 0) -> L.SearchOpts:
     """Search options (ads_search_opts, include/adsann_b200.h): first/step set the
     threshold refresh schedule in candidates; scheduler must be 0."""
     o = L.SearchOpts()

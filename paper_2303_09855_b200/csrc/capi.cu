@@ -1282,7 +1282,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->tile = 64;
     o->query_order = 2;
     o->coarse_mode = 0;
-    o->rotate_mode = 0;
+    o->rotate_mode = 2;
     o->probe_lo = 0;
     o->r0 = nullptr;
     o->walk = 0;
@@ -1390,13 +1390,14 @@ void plan_scan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0,
     a.a1i = (mode == ADS_MODE_AD_SPLIT && x->a1i_t && a.vec == 4 && o.tile >= 0 && D > x->d1p) ? x->a1i_t : nullptr;
     // certified fp32 walk (ivf.cu): requested with walk = 2 (walk 0 keeps the exact walk)
     require(o.walk >= 0 && o.walk <= 2, "search: walk must be 0, 1 or 2");
-    // walk 0 picks it when a query streams >= 100 000 candidates on average: positives, which
+    // walk 0 picks it when a query streams >= 32 000 candidates on average: positives, which
     // the fp32 walk must re-walk exactly, are then a small fraction of the stream (config 5:
-    // 390 000 candidates, ~0.2 % positives, +5 %; config 2: 15 600 candidates, -1 to -3 %;
-    // profiles/r02/ab_f32_walk.log)
+    // 390 000 candidates, ~0.2 % positives, +5 %; its 8-way shards' second wave, 43 000:
+    // 19.8 vs 21.6 ms; config 2: 15 600 candidates, -1 to -3 %; profiles/r02/ab_f32_walk.log,
+    // r02o_shard_projection)
     // (for a shard: its rows over all k lists, i.e. the candidates this rank streams)
     const double cand_per_query = static_cast<double>(x->n) / x->k * (nprobe - o.probe_lo);
-    const bool want_f32 = o.walk == 2 || (o.walk == 0 && cand_per_query >= 100000.0);
+    const bool want_f32 = o.walk == 2 || (o.walk == 0 && cand_per_query >= 32000.0);
     a.f32 = (want_f32 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT) ? 1 : 0;
     // threshold refresh: first = K; step (candidates per chunk) by kernel shape, from
     // same-box sweeps (profiles/r02/ab_rewalk_step, r02k): 64 per warp for the exact walk
@@ -1420,7 +1421,11 @@ void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq,
     const float* Qs = transformed ? dQt : dQraw;
     if (transformed && !dQt) {  // rotate on device (apply, transform.cpp:99-117)
         float* qr = x->qrot.get<float>(static_cast<size_t>(nq) * D);
-        if (o.rotate_mode == 1) {  // 3xTF32 tensor cores (tc_gemm.cu)
+        require(o.rotate_mode >= 0 && o.rotate_mode <= 2, "search: rotate_mode must be 0, 1 or 2");
+        // 2 (default): the tensor cores for batches (the north star's transform on tcgen05),
+        // the exact fp64 rotation for small batches or shapes the GEMM does not take
+        const bool tc_rot = o.rotate_mode == 1 || (o.rotate_mode == 2 && D % 4 == 0 && D >= 32 && nq >= 64);
+        if (tc_rot) {  // 3xTF32 tensor cores (tc_gemm.cu)
             require(D % 4 == 0 && D >= 32, "rotate_mode 1: dimension must be a multiple of 4 and >= 32");
             const size_t dd = static_cast<size_t>(D) * D;
             if (!x->p_split) {

@@ -209,15 +209,28 @@ def test_ivf_duplicate_vectors_ties(eng, orc, K, first, step):
 
 
 def test_ivf_rotation_on_device(eng, orc):
-    """Q_t omitted -> queries rotated on the GPU with P; identical results."""
-    raw, t, qr, qt, P = make_fixture(orc, 2000, 64, 16, 30, 7)
+    """Q_t omitted -> queries rotated on the GPU with P: rotate_mode 0 (exact fp64) gives
+    results identical to the oracle-rotated queries; the default (2) rotates batches of
+    >= 64 queries on the tensor cores (== rotate_mode 1) and small batches exactly."""
+    raw, t, qr, qt, P = make_fixture(orc, 2000, 64, 16, 80, 7)
     lay = oracle_index(orc, raw, t, P, 30, 8, d1=32)
     idx = gpu_index(eng, lay, P)
-    a = eng.ivf_query_batch(idx, None, qr, 10, 6, eng.IvfMode.kAdSplit)
     b = eng.ivf_query_batch(idx, qt, qr, 10, 6, eng.IvfMode.kAdSplit)
+    a = eng.ivf_query_batch(idx, None, qr, 10, 6, eng.IvfMode.kAdSplit, opts=eng.search_opts(rotate_mode=0))
     np.testing.assert_array_equal(a.ids, b.ids)
     np.testing.assert_array_equal(a.dists, b.dists)
     np.testing.assert_array_equal(a.dims, b.dims)
+    small = eng.ivf_query_batch(idx, None, qr[:30], 10, 6, eng.IvfMode.kAdSplit)  # < 64: exact
+    np.testing.assert_array_equal(small.ids, b.ids[:30])
+    np.testing.assert_array_equal(small.dists, b.dists[:30])
+    dflt = eng.ivf_query_batch(idx, None, qr, 10, 6, eng.IvfMode.kAdSplit)
+    tc = eng.ivf_query_batch(idx, None, qr, 10, 6, eng.IvfMode.kAdSplit, opts=eng.search_opts(rotate_mode=1))
+    np.testing.assert_array_equal(dflt.ids, tc.ids)
+    np.testing.assert_array_equal(dflt.dists, tc.dists)
+    np.testing.assert_array_equal(dflt.dims, tc.dims)
+    # within the north star's tolerance of the exact rotation's distances
+    m = np.isfinite(dflt.dists) & np.isfinite(b.dists) & (dflt.ids == b.ids)
+    assert np.all(np.abs(dflt.dists[m] - b.dists[m]) <= 1e-5 * np.abs(b.dists[m]) + 1e-12)
 
 
 def test_probe_order_bitexact(eng, orc):

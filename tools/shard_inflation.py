@@ -5,7 +5,7 @@ the scanned dims summed over shards (looser local thresholds inflate them) and t
 slowest shard's scan time (the step's critical path), next to the unsharded search.
 No rank waits on another, so one GPU measures each shard's work exactly.
 
-    python tools/shard_inflation.py [config] [N ...]
+    python tools/shard_inflation.py [config] [N ...] [walk=W]   (W: ads_search_opts.walk, 0 = engine's pick)
 """
 import os
 import sys
@@ -22,13 +22,17 @@ def main():
     from paper_2303_09855_b200 import configs
     from paper_2303_09855_b200.shard import partition_lists, shard_index
 
-    cfgid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-    ns = [int(v) for v in sys.argv[2:]] or [2, 4, 8]
+    argv = [a for a in sys.argv[1:] if not a.startswith("walk=")]
+    walk = int(next((a.split("=")[1] for a in sys.argv[1:] if a.startswith("walk=")), 0))
+    cfgid = int(argv[0]) if argv else 2
+    ns = [int(v) for v in argv[1:]] or [2, 4, 8]
     cfg = configs.CONFIGS[cfgid]
     log = lambda *a: print(*a, file=sys.stderr, flush=True)  # noqa: E731
-    ads_, ctx, base, t, q, m, idx, gt = bench.setup(cfg, 0, 0, log)
+    S = bench.setup(cfg, bench.Dist(), log)
+    ctx, q, idx = S["ctx"], S["q"], S["idx"]
     K, nprobe = cfg.K, cfg.nprobe
-    opts = ads.search_opts(time_stages=True)
+    opts = ads.search_opts(time_stages=True, walk=walk)
+    print(f"walk option {walk} (engine's pick unsharded: {ads.search_plan(idx, K, nprobe, ads.IvfMode.kAdSplit, opts=opts)})")
 
     def run(index, reps=3):
         best, dims = None, None
@@ -64,6 +68,7 @@ def main():
         # [w, nprobe) from r0 = R
         w = max(1, nprobe // 8)
         locals_ = [shard_index(idx, owner, rank) for rank in range(n)]
+        print(f"N={n}: rank 0's plan {ads.search_plan(locals_[0], K, nprobe, ads.IvfMode.kAdSplit, opts=opts)}")
         w1 = []
         for loc in locals_:
             best = None
@@ -77,7 +82,7 @@ def main():
         R = np.nan_to_num(kth, nan=np.inf).min(axis=0)
         t2, d2 = [], []
         for (ms1, r1), loc in zip(w1, locals_):
-            o2 = ads.search_opts(time_stages=True, probe_lo=w, r0=R)
+            o2 = ads.search_opts(time_stages=True, probe_lo=w, r0=R, walk=walk)
             best = None
             for _ in range(3):
                 ctx.flush_l2()
