@@ -78,6 +78,22 @@ def run_transform(args, D):
         e2e_s.append(_time.perf_counter() - t0)
     e2e_sec = float(np.mean(e2e_s))
     log(f"exact fp64: {exact_ms:.2f} ms, 3xTF32 tensor cores: {tc_ms:.2f} ms, max |err|/|x| {err:.2e}")
+    # the binding roof: tensor pipe at high D (1 M x 960), HBM at low D (config 5's 96:
+    # 72 issued TF32 flops per byte, below the ridge): X read + Y written once
+    from bench import measured_peaks
+
+    hbm = measured_peaks()
+    gbs = 8.0 * n * d / (tc_ms / 1e3) / 1e9
+    tensor = {"bound": "tensor", "achieved": achieved, "peak": peak["tflops"], "unit": "TFLOP/s",
+              "frac": achieved / peak["tflops"], "peak_source": peak["source"]}
+    mem = {"bound": "hbm", "achieved": gbs, "peak": hbm["hbm_gbs"], "unit": "GB/s",
+           "frac": gbs / hbm["hbm_gbs"], "peak_source": hbm["source"] + ", copy"}
+    roofline = dict(mem if mem["frac"] > tensor["frac"] else tensor)
+    roofline.update({"other": tensor if roofline["bound"] == "hbm" else mem,
+                     "traffic": 7.66 if (n, d) == (1_000_000, 960) else None,
+                     "traffic_unit": "GB per launch (ncu dram read+write, profiles/r01_ncu_tensorcore.md, prof_pair2)",
+                     "useful_tflops": useful / (tc_ms / 1e3) / 1e12,
+                     "kernel": "tc_rotate_pair_kernel (TF32 flops issued = 3 x 2 n D^2; useful = 2 n D^2)"})
     return {
         "metric": "dataset rotation vectors/s (3xTF32 tensor cores)", "value": n / (tc_ms / 1e3),
         "unit": "vectors/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tc_ms,
@@ -91,12 +107,6 @@ def run_transform(args, D):
                 "d2h_bytes_per_step": int(X.nbytes),
                 "timing": "Transform.apply_dataset_tc on host arrays (ads_apply_dataset_tc), wall clock"},
         "gpu_launches": args.steps,  # one persistent tc_rotate_kernel per step (split fused)
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak["tflops"], "unit": "TFLOP/s",
-                     "frac": achieved / peak["tflops"],
-                     "traffic": 7.66 if (n, d) == (1_000_000, 960) else None, "traffic_unit": "GB per launch (ncu dram read+write, "
-                                                      "profiles/r01_ncu_tensorcore.md, prof_pair2)",
-                     "useful_tflops": useful / (tc_ms / 1e3) / 1e12,
-                     "kernel": "tc_rotate_pair_kernel (TF32 flops issued = 3 x 2 n D^2; useful = 2 n D^2)",
-                     "peak_source": peak["source"]},
+        "roofline": roofline,
         "clocks": clocks,
     }
