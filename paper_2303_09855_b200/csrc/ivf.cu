@@ -22,6 +22,15 @@
 #include "engine.hpp"
 #include "scan_engine.cuh"
 
+// Scan experiments (off in the product build): ADS_PF = 1 / 4 L2 prefetches of a lane's
+// next segment (1 = the line's first sector, 4 = all four), 2 = one 128-byte bulk prefetch.
+#ifndef ADS_PF
+#define ADS_PF 0
+#endif
+#ifndef ADS_PF_MIN
+#define ADS_PF_MIN 1
+#endif
+
 namespace ads {
 
 namespace {
@@ -808,6 +817,23 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                                           : static_cast<uint32_t>(pos) * str2 + a2c + (sg.col >> 2);
                     if constexpr (F32) gather_issue16<FULL>(gdst, gbase, dsc, sg.len >> 2);
                     else gather_issue16<FULL>(wbuf, gbase, dsc, sg.len >> 2);
+#if ADS_PF
+                    // L2 prefetch of the lane's next segment once its candidate has passed
+                    // ADS_PF_MIN tests: the next gather then waits on L2, not DRAM
+                    if (!F32 && cand >= 0 && !prew && seg >= ADS_PF_MIN && seg + 1 < a.nseg) {
+                        const Seg sn = segs[seg + 1];
+                        const uint32_t nd = sn.arr == 0 ? static_cast<uint32_t>(pos) * str1 + (sn.col >> 2)
+                                                        : static_cast<uint32_t>(pos) * str2 + a2c + (sn.col >> 2);
+                        const char* pa = reinterpret_cast<const char*>(a.a1) + static_cast<uint64_t>(nd) * 16u;
+#if ADS_PF == 2
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;" ::"l"(pa) : "memory");
+#else
+#pragma unroll
+                        for (int k = 0; k < ADS_PF; ++k)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 32 * k));
+#endif
+                    }
+#endif
                 } else {
                     const float* src = sg.arr == 0 ? a.a1 + static_cast<int64_t>(pos) * a.d1 + sg.col
                                                    : a.a2 + static_cast<int64_t>(pos) * (a.D - a.d1) + (sg.col - a.d1);
