@@ -853,7 +853,7 @@ def main():
     ap.add_argument("--nprobe", type=int, default=0)
     ap.add_argument("--nq", type=int, default=0)
     ap.add_argument("--step", type=int, default=0, help="threshold refresh interval (0: 64 x warps)")
-    ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0: 4 for D <= 256, else 10)")
+    ap.add_argument("--warps", type=int, default=0, help="warps per CTA (0: 4 for D <= 256, else 8)")
     ap.add_argument("--ctas-per-sm", type=int, default=0, help="cap on resident search CTAs per SM (0: occupancy)")
     ap.add_argument("--query-order", type=int, default=2,
                     help="2: longest queries first (default), 1: L2-locality order, 0: input order")

@@ -278,8 +278,8 @@ int ads_ivf_export(ads_ivf *idx, float *centroids_t, float *centroids_raw, int64
  * refresh (ivf.cpp:331, 391), larger values batch it. */
 typedef struct {
     int64_t first;         /* default K */
-    int64_t step;          /* 0 (default): 64 * warps_per_cta candidates */
-    int32_t warps_per_cta; /* 0 (default): 4 for D <= 256, else 10 */
+    int64_t step;          /* 0 (default): 64 (D <= 256) or 128 candidates per warp; see ads_ivf_search_plan */
+    int32_t warps_per_cta; /* 0 (default): 4 for D <= 256, else 8 */
     int32_t queries_per_cta; /* reserved: the query-major kernel serves one query per CTA */
     int32_t ctas_per_sm;   /* 0 = occupancy maximum */
     int32_t time_stages;   /* 1: record per-stage CUDA-event times (ads_ivf_last_timings) */

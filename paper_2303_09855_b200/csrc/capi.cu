@@ -1274,7 +1274,7 @@ int ads_ivf_export(ads_ivf* x, float* centroids_t, float* centroids_raw, int64_t
 void ads_search_opts_default(ads_search_opts* o) {
     o->first = 0;          // 0 -> K
     o->step = 0;           // 0 -> 64 * warps_per_cta
-    o->warps_per_cta = 0;  // 0 -> 4 for D <= 256, else 10
+    o->warps_per_cta = 0;  // 0 -> 4 for D <= 256, else 8
     o->queries_per_cta = 4;
     o->ctas_per_sm = 0;
     o->time_stages = 0;
@@ -1345,7 +1345,9 @@ ads_search_opts resolve_opts(ads_ivf* x, int32_t K, int32_t nprobe, const ads_se
     // auto launch shape: CTAs of 4 warps for D <= 256; wider CTAs amortise the
     // larger per-query shared state (staged query, chunk slots) at high D.
     require(o.scheduler == 0, "search: scheduler must be 0 (query-major; the list-major scheduler was removed)");
-    if (o.warps_per_cta <= 0) o.warps_per_cta = x->d <= 256 ? 4 : 10;
+    // 8-warp CTAs above D = 256: with one prefix buffer (no untested prefix to pre-walk)
+    // four fit per SM, 32 warps (config 3: +2.5 % over 3 x 10 warps, profiles/r02/ab_w)
+    if (o.warps_per_cta <= 0) o.warps_per_cta = x->d <= 256 ? 4 : 8;
     require(o.warps_per_cta >= 1 && o.warps_per_cta <= 32, "search: warps_per_cta in [1, 32]");
     require(o.probe_lo >= 0 && o.probe_lo <= nprobe, "ivf_query: probe_lo must be in [0, n_probe]");
     require(o.queries_per_cta >= 1 && o.queries_per_cta <= 16, "search: queries_per_cta in [1, 16]");
@@ -1375,6 +1377,7 @@ void plan_scan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0,
     a.ntest = plan.ntest;
     a.vec = plan.vec;
     a.full = plan.full;
+    a.nseg0 = plan.nseg0;
     // 16-byte line descriptors address A1|A2 (one allocation) in 32 bits of
     // 16-byte units from a1.
     const int64_t gap = a.a2 - a.a1;
@@ -1401,11 +1404,12 @@ void plan_scan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0,
     a.f32 = (want_f32 && a.vec == 4 && a.full && mode == ADS_MODE_AD_SPLIT) ? 1 : 0;
     // threshold refresh: first = K; step (candidates per chunk) by kernel shape, from
     // same-box sweeps (profiles/r02/ab_rewalk_step, r02k): 64 per warp for the exact walk
-    // at D <= 256 (config 2: 384 / 512 measured -1 / -4 %), 96 per warp above (config 3:
-    // 960 +2.5 %, 1280 -12 %), 128 per warp for the dense + fp32 walk, whose compact
+    // at D <= 256 (config 2: 384 / 512 measured -1 / -4 %), 128 per warp above (config 3
+    // at 8 warps: 768 -1.2 %, 1024 best; refreshing less often costs dims: +2 % at 1280
+    // with 10 warps, profiles/r02/ab_step1), 128 per warp for the dense + fp32 walk, whose compact
     // chunk state keeps 9 CTAs per SM at 512 (config 5: +10 %; 768 +0.5 % at 8 CTAs)
     a.first = o.first;
-    const int64_t per_warp = (a.a1i && a.f32) ? 128 : (D > 256 ? 96 : 64);
+    const int64_t per_warp = (a.a1i && a.f32) ? 128 : (D > 256 ? 128 : 64);
     a.step = o.step > 0 ? o.step : per_warp * o.warps_per_cta;
 }
 

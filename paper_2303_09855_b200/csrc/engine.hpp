@@ -35,6 +35,7 @@ struct DevSegPlan {
     Seg* segs = nullptr;
     double* tfac = nullptr;
     int nseg = 0, ntest = 0, vec = 4, full = 0;
+    int nseg0 = 0;  // leading segments no test depends on (the search's pre-walk depth)
     void upload(const SegPlan& p, cudaStream_t st);
     void release();
 };
@@ -93,6 +94,8 @@ struct SearchLaunch {
     const double* tfac;
     int nseg, ntest, vec;
     int full;          // every segment is 32 floats (no per-line length shuffle)
+    int nseg0;         // leading untested segments: lanes idle at a chunk's tail pre-walk
+                       // them for the next chunk (0: no pre-walk, one prefix buffer)
     int64_t first, step;
     int warps;         // per CTA
     int slots;         // queries served concurrently per CTA

@@ -22,15 +22,6 @@
 #include "engine.hpp"
 #include "scan_engine.cuh"
 
-// Scan experiments (off in the product build): ADS_PF = 1 / 4 L2 prefetches of a lane's
-// next segment (1 = the line's first sector, 4 = all four), 2 = one 128-byte bulk prefetch.
-#ifndef ADS_PF
-#define ADS_PF 0
-#endif
-#ifndef ADS_PF_MIN
-#define ADS_PF_MIN 1
-#endif
-
 namespace ads {
 
 namespace {
@@ -474,8 +465,8 @@ __host__ __device__ inline int slot_bytes_before_surv(bool dense, bool f32, int 
     const int pend_b = (f32 && !pend_in_wbuf(dense, f32, cap, nwarps)) ? 8 * cap : 0;
     return ((pre_b + 7) & ~7) + pend_b;
 }
-__host__ __device__ inline int slot_words(bool dense, bool f32, int cap, int nwarps) {
-    if (!dense) return 2 * cap;
+__host__ __device__ inline int slot_words(bool dense, bool f32, int cap, int nwarps, bool prewalk) {
+    if (!dense) return prewalk ? 2 * cap : cap;
     return (slot_bytes_before_surv(dense, f32, cap, nwarps) + 2 * cap + 7) / 8;
 }
 
@@ -497,7 +488,8 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
     double* tfac = thr + (a.ntest > 0 ? a.ntest : 1);
     double* topd = tfac + (a.ntest > 0 ? a.ntest : 1);
     // Per-slot chunk state (slot_words, shared with search_smem).  Lane walk alone: 2 x
-    // chunk_cap untested-prefix sums, by chunk parity; a chunk's positives' distances
+    // chunk_cap untested-prefix sums, by chunk parity, when the plan has an untested prefix
+    // to pre-walk (a.nseg0 > 0), else one chunk_cap buffer; a chunk's positives' distances
     // reuse its own prefix half (pend_d = pre_cur): a slot's prefix is consumed when the
     // slot is claimed, before it can turn positive.  DENSE: the survivors' prefixes
     // (acc_t; the exact walk's double prefix doubles as pend_d) and the survivor list
@@ -513,7 +505,8 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                                       : reinterpret_cast<double*>(reinterpret_cast<char*>(pre_s) + ((pre_b + 7) & ~7)));
     uint16_t* surv = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(pre_s) +
                                                  slot_bytes_before_surv(DENSE, F32, chunk_cap, nwarps));
-    int32_t* lstart = reinterpret_cast<int32_t*>(pre_s + slot_words(DENSE, F32, chunk_cap, nwarps));
+    const bool prewalk = a.nseg0 > 0;
+    int32_t* lstart = reinterpret_cast<int32_t*>(pre_s + slot_words(DENSE, F32, chunk_cap, nwarps, prewalk));
     int32_t* cpos = lstart + a.nprobe;
     Seg* segs = reinterpret_cast<Seg*>(cpos + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
@@ -560,17 +553,13 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
         }
         return lstart[l] + (i - pre[l]);
     };
-    int nseg0 = -1;  // leading segments no threshold test depends on (set after the first barrier)
+    // leading segments no threshold test depends on (the split layouts' A1 prefix and FD's
+    // whole walk but the last segment are tested against nothing, ivf.cpp:366-386): lanes
+    // left idle at a chunk's tail precompute them for the next chunk
+    const int nseg0 = a.nseg0;
 
     for (;;) {
         __syncthreads();
-        if (nseg0 < 0) {
-            // The split layouts' A1 prefix (and FD's whole walk but the last
-            // segment) is tested against nothing (ivf.cpp:366-386): lanes left
-            // idle at a chunk's tail precompute it for the next chunk.
-            nseg0 = 0;
-            while (nseg0 < a.nseg - 1 && segs[nseg0].test < 0) ++nseg0;
-        }
         if (threadIdx.x == 0) {
             const int w = static_cast<int>(atomicAdd(a.counter, 1ull));
             sh.stop = w >= a.nq;
@@ -626,7 +615,7 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
             const int64_t span = lo == 0 ? a.first : a.step;
             const int hi = static_cast<int>(lo + span < total ? lo + span : total);
             const int nhi = static_cast<int>(hi + a.step < total ? hi + a.step : total);  // next chunk [hi, nhi)
-            double* pre_cur = pre_s + (j & 1) * chunk_cap;  // lane walk alone (!DENSE)
+            double* pre_cur = pre_s + (prewalk ? (j & 1) * chunk_cap : 0);  // lane walk alone (!DENSE)
             double* pend_d = DENSE ? dpend : pre_cur;
             double* pre_nxt = pre_s + ((j & 1) ^ 1) * chunk_cap;
             // F32 with no finite radius yet (r = +inf before K results): every candidate
@@ -817,23 +806,6 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                                           : static_cast<uint32_t>(pos) * str2 + a2c + (sg.col >> 2);
                     if constexpr (F32) gather_issue16<FULL>(gdst, gbase, dsc, sg.len >> 2);
                     else gather_issue16<FULL>(wbuf, gbase, dsc, sg.len >> 2);
-#if ADS_PF
-                    // L2 prefetch of the lane's next segment once its candidate has passed
-                    // ADS_PF_MIN tests: the next gather then waits on L2, not DRAM
-                    if (!F32 && cand >= 0 && !prew && seg >= ADS_PF_MIN && seg + 1 < a.nseg) {
-                        const Seg sn = segs[seg + 1];
-                        const uint32_t nd = sn.arr == 0 ? static_cast<uint32_t>(pos) * str1 + (sn.col >> 2)
-                                                        : static_cast<uint32_t>(pos) * str2 + a2c + (sn.col >> 2);
-                        const char* pa = reinterpret_cast<const char*>(a.a1) + static_cast<uint64_t>(nd) * 16u;
-#if ADS_PF == 2
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;" ::"l"(pa) : "memory");
-#else
-#pragma unroll
-                        for (int k = 0; k < ADS_PF; ++k)
-                            asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 32 * k));
-#endif
-                    }
-#endif
                 } else {
                     const float* src = sg.arr == 0 ? a.a1 + static_cast<int64_t>(pos) * a.d1 + sg.col
                                                    : a.a2 + static_cast<int64_t>(pos) * (a.D - a.d1) + (sg.col - a.d1);
@@ -1006,7 +978,7 @@ size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
     const bool dense = a.a1i != nullptr, f32 = a.f32 && a.vec == 4 && a.full;
     size_t b = sizeof(float) * a.warps * 1024;
-    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + slot_words(dense, f32, chunk_cap, a.warps));
+    b += sizeof(double) * (a.nseg * kQPitch + 2 * nt + a.K + slot_words(dense, f32, chunk_cap, a.warps, a.nseg0 > 0));
     b += sizeof(int32_t) * (a.nprobe + chunk_cap + ((chunk_cap + a.nprobe) & 1));
     b += sizeof(Seg) * a.nseg;
     b += sizeof(int32_t) * (a.K + a.nprobe + 1);

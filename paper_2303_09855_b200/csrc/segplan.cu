@@ -76,6 +76,8 @@ void DevSegPlan::upload(const SegPlan& p, cudaStream_t st) {
     ntest = static_cast<int>(p.test_factor.size());
     vec = p.vec;
     full = p.full;
+    nseg0 = 0;
+    while (nseg0 < nseg - 1 && p.segs[nseg0].test < 0) ++nseg0;
     ADS_CUDA(cudaMallocAsync(&segs, sizeof(Seg) * nseg, st));
     ADS_CUDA(cudaMemcpyAsync(segs, p.segs.data(), sizeof(Seg) * nseg, cudaMemcpyHostToDevice, st));
     ADS_CUDA(cudaMallocAsync(&tfac, sizeof(double) * std::max(ntest, 1), st));

@@ -1,5 +1,5 @@
 """Parity at BASELINE.json's full sizes: config 2's 1 M x 128 index (4096 lists,
-k-means++ + 25 Lloyd iterations) and config 3's 1 M x 960 index (10-warp CTAs,
+k-means++ + 25 Lloyd iterations) and config 3's 1 M x 960 index (8-warp CTAs,
 30 segments per walk), built on the GPU, exported and searched by the C oracle
 for a subset of queries, bit for bit: ids, distances and dims under the
 engine's default batched refresh schedule, and under the reference's
