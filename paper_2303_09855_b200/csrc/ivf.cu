@@ -231,6 +231,21 @@ __device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double 
     __syncwarp();
 }
 
+// Live candidates per warp at or below which a step goes deep (0: off).
+#ifndef ADS_DEEP_TAIL
+#define ADS_DEEP_TAIL 16
+#endif
+constexpr int kDeepTail = ADS_DEEP_TAIL;
+#ifndef ADS_DEEP_SHIFT
+#define ADS_DEEP_SHIFT 2
+#endif
+constexpr int kDeepShift = ADS_DEEP_SHIFT;  // a candidate takes at most 1 << kDeepShift rows in a deep step
+
+#ifndef ADS_DEEP_MIN_NSEG
+#define ADS_DEEP_MIN_NSEG 8
+#endif
+constexpr int kDeepMinSeg = ADS_DEEP_MIN_NSEG;  // walks shorter than this have no tail to speak of
+
 struct SearchShared {
     double r, r_sq;
     int q, stop, total, next, cnt, pnext;
@@ -473,8 +488,9 @@ __host__ __device__ inline int slot_words(bool dense, bool f32, int cap, int nwa
 // Register caps (same-box A/B, profiles/r02/ab_regs.log): the certified fp32 walk at 56
 // (9 resident 4-warp CTAs per SM; 64 measured -2.5 % on config 5), the exact walk at 64
 // (8 CTAs; +3 to +4 % on configs 2 and 3, where the fp64 chains need the registers).
-template <int VEC, bool FULL, bool DENSE, bool F32>
+template <int VEC, bool FULL, bool DENSE, bool F32, bool DEEP = false>
 __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int chunk_cap) {
+    static_assert(!DEEP || (VEC == 4 && !F32), "deep tail steps: 16-byte lines, exact walk");
     static_assert(!F32 || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
     using acc_t = typename std::conditional<F32, float, double>::type;
     extern __shared__ __align__(128) unsigned char smem_raw[];  // gather rows: 128-byte aligned (swizzle)
@@ -797,7 +813,69 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                         }
                     }
                 }
-                if (!__any_sync(kFull, cand >= 0)) break;
+                if constexpr (!DEEP) {
+                    if (!__any_sync(kFull, cand >= 0)) break;
+                } else {
+                    // (a ballot every step measured 1 % ahead of gating this on the stream's end)
+                    const unsigned livem = __ballot_sync(kFull, cand >= 0);
+                    if (!livem) break;
+                    // Deep tail step.  With <= 16 live candidates in the warp (a chunk's tail,
+                    // or its first K candidates) the free rows of the gather buffer carry the
+                    // live candidates' NEXT segments: candidate of rank r owns rows r*k .. r*k+k-1
+                    // (k = 2, or 4 at <= 8 live) and its lane walks them in order, testing after each as
+                    // always, so sums, decisions and dims are unchanged; a row fetched past a
+                    // rejection is the only cost.  The tail is latency-bound (a step is one DRAM
+                    // round trip whatever the lane count), so it ends k times sooner.
+                    const int nlive = __popc(livem);
+                    if (nlive <= kDeepTail) {
+                        // rows per candidate: 2, 4 ... (1 << kDeepShift) as the live count halves
+                        int ks = 1;
+#pragma unroll
+                        for (int t = 2; t <= kDeepShift; ++t) ks += nlive <= (32 >> t) ? 1 : 0;
+                        const int rnk = static_cast<int>(lane) >> ks, off = static_cast<int>(lane) & ((1 << ks) - 1);
+                        const unsigned srcl = __fns(livem, 0, rnk + 1) & 31u;
+                        const int ppos = __shfl_sync(kFull, pos, srcl), pseg = __shfl_sync(kFull, seg, srcl);
+                        const int rseg = pseg + off;
+                        uint32_t dsc = kNoLine;
+                        int nch = 0;
+                        if (rnk < nlive && rseg < a.nseg) {
+                            const Seg g = segs[rseg];
+                            dsc = g.arr == 0 ? static_cast<uint32_t>(ppos) * str1 + (g.col >> 2)
+                                             : static_cast<uint32_t>(ppos) * str2 + a2c + (g.col >> 2);
+                            nch = g.len >> 2;
+                        }
+                        gather_issue16<FULL>(wbuf, gbase, dsc, nch);
+                        cp_async_wait_group<0>();
+                        __syncwarp();
+                        if (cand >= 0) {
+                            const unsigned row0 = static_cast<unsigned>(__popc(livem & ((1u << lane) - 1u))) << ks;
+                            for (int m = 0; m < (1 << ks); ++m) {
+                                const Seg sg = segs[seg];
+                                s = accumulate_row<FULL>(wbuf, row0 + m, qseg + seg * kQPitch, sg.len, s);
+                                if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
+                                    my_dims += static_cast<unsigned long long>(sg.col + sg.len);
+                                    cand = -1;
+                                    break;
+                                }
+                                if (seg == a.nseg - 1) {  // d == D (dco.hpp:145; ivf.cpp:335-338)
+                                    my_dims += static_cast<unsigned long long>(a.D);
+                                    const bool positive = a.final_fd ? __dsqrt_rn(s) <= r : s <= r_sq;
+                                    if (positive) {
+                                        const int slot = cand - lo;
+                                        pend_d[slot] = __dsqrt_rn(s);
+                                        pend_i[slot] = a.ids[pos];
+                                        atomicOr(&pflag[slot >> 5], 1u << (slot & 31));
+                                    }
+                                    cand = -1;
+                                    break;
+                                }
+                                ++seg;
+                            }
+                        }
+                        __syncwarp();
+                        continue;
+                    }
+                }
                 const Seg sg = segs[seg];
                 if constexpr (VEC == 4) {
                     uint32_t dsc = kNoLine;
@@ -1106,6 +1184,13 @@ struct SearchShape {
     int occ;  // resident CTAs per SM
 };
 
+// Deep tail steps pay where walks are long (config 3: 30 segments, +5 %); below
+// kDeepMinSeg segments a chunk's tail is a few steps and the plain kernel is level or
+// ahead (config 2, 4 segments: -0.7 %).  Not with the pre-walk (no lane is idle there).
+bool search_deep(const SearchLaunch& a) {
+    return kDeepTail > 0 && a.vec == 4 && !a.f32 && a.nseg0 == 0 && a.nseg >= kDeepMinSeg;
+}
+
 SearchShape search_shape_of(const SearchLaunch& a) {
     const int64_t cap64 = a.first > a.step ? a.first : a.step;
     if (a.first < 1 || a.step < 1) throw std::invalid_argument("search: threshold schedule must be >= 1");
@@ -1115,6 +1200,9 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     sh.smem = search_smem(a, sh.cap);
     if (a.f32 && a.vec == 4 && a.full)
         sh.kern = a.a1i ? ivf_search_kernel<4, true, true, true> : ivf_search_kernel<4, true, false, true>;
+    else if (search_deep(a))
+        sh.kern = a.a1i ? (a.full ? ivf_search_kernel<4, true, true, false, true> : ivf_search_kernel<4, false, true, false, true>)
+                        : (a.full ? ivf_search_kernel<4, true, false, false, true> : ivf_search_kernel<4, false, false, false, true>);
     else if (a.a1i)
         sh.kern = a.full ? ivf_search_kernel<4, true, true, false> : ivf_search_kernel<4, false, true, false>;
     else

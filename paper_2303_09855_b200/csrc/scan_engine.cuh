@@ -156,6 +156,33 @@ __device__ __forceinline__ void gather_lines(float* wbuf, const float* src, int 
 
 // Adds the lane's gathered segment (len floats) to s, index order, fp64.
 // FULL: len == 32 for every segment (no per-chunk guard).
+// row_key for an explicit row of the gather buffer (deep tail steps: a lane walks
+// several rows in one step)
+__device__ __forceinline__ unsigned row_key_at(const float* wbuf, unsigned row) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(wbuf)) + row * 128u + ((row & 7u) << 4);
+}
+
+// VEC=4 only: the segment gathered into buffer row `row`.
+template <bool FULL>
+__device__ __forceinline__ double accumulate_row(const float* wbuf, unsigned row, const double* qq, int len,
+                                                 double s) {
+    const int nc = FULL ? 8 : len >> 2;
+    const unsigned rk = row_key_at(wbuf, row);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        if (FULL || c < nc) {
+            const float4 v = lds128(rk ^ (static_cast<unsigned>(c) << 4));
+            const double2 q0 = *reinterpret_cast<const double2*>(qq + c * 4);
+            const double2 q1 = *reinterpret_cast<const double2*>(qq + c * 4 + 2);
+            s = sq_diff_acc(s, v.x, q0.x);
+            s = sq_diff_acc(s, v.y, q0.y);
+            s = sq_diff_acc(s, v.z, q1.x);
+            s = sq_diff_acc(s, v.w, q1.y);
+        }
+    }
+    return s;
+}
+
 template <int VEC, bool FULL = false>
 __device__ __forceinline__ double accumulate_line(const float* wbuf, const double* qq, int len,
                                                   double s) {

@@ -592,6 +592,34 @@ def test_ivf_certified_f32_walk_bitexact(eng, orc, case, K, monkeypatch):
     np.testing.assert_array_equal(a.dims, b.dims)
 
 
+@pytest.mark.parametrize("case", [(2500, 960, 12, 16, 32, 32),   # config 3's plan: 30 full segments
+                                  (2500, 300, 12, 16, 32, 32),   # ragged last segment (12 floats)
+                                  (3000, 256, 16, 20, 32, 16),   # 16-float segments (half lines)
+                                  (2000, 512, 8, 12, 64, 48)])   # d1 != delta_d, ragged
+@pytest.mark.parametrize("warps", [0, 4, 8])
+def test_ivf_deep_tail_steps_bitexact(eng, orc, case, warps, monkeypatch):
+    """Long walks (>= 8 segments) run the kernel with deep tail steps: a warp left with
+    <= 16 live candidates fetches 2 or 4 consecutive segments of each per step and tests
+    after every one.  Ids, distances, dims and candidate counts == the oracle at the
+    reference schedule and at batched schedules whose chunks are mostly tail (7, 64) or
+    mostly body (1000); all AD/PD modes; with and without the dense prefix phase."""
+    monkeypatch.setenv("ADS_DENSE_MIN_LIST", "0")
+    n, d, blobs, k, d1, dd = case
+    raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 12, 700 + d)
+    lay = oracle_index(orc, raw, t, P, k, 701, d1=d1)
+    idx = gpu_index(eng, lay, P)
+    cfg = eng.DcoConfig(2.1, dd)
+    K = 10
+    for mode in ("ad-split", "ad", "pd-split"):
+        for first, step in ((1, 1), (K, 64), (K, 7), (K, 1000)):
+            for nprobe in (2, k):
+                for tile in ((-1, 64) if (mode == "ad-split" and d1 == 32) else (-1,)):
+                    res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg,
+                                              opts=eng.search_opts(first=first, step=step, tile=tile,
+                                                                   warps_per_cta=warps, walk=1))
+                    assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, dd, first, step)
+
+
 def test_ivf_long_lists_default_path_bitexact(eng, orc):
     """The default path at config 5's shape of work: 6 250-row lists (the interleaved A1
     copy and its dense prefix phase) and 100 000 candidates per query (the certified fp32
