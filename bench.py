@@ -332,7 +332,8 @@ def measure(S, cfg, nprobe, args, D, log, steps):
     opts = ads.search_opts(first=0, step=args.step, warps_per_cta=args.warps, time_stages=True,
                            query_order=args.query_order, ctas_per_sm=args.ctas_per_sm,
                            tile=-1 if getattr(args, "no_dense", False) else 64,
-                           rotate_mode=getattr(args, "rotate_mode", 2), walk=getattr(args, "walk", 0))
+                           rotate_mode=getattr(args, "rotate_mode", 2), walk=getattr(args, "walk", 0),
+                           lag=getattr(args, "lag", 0))
     plan = ads.search_plan(idx, K, nprobe, mode, opts=opts)
     dq = ads.DeviceArray.from_host(ctx, q)
     outs = {nm: ads.DeviceArray(ctx, shape, dt) for nm, shape, dt in (
@@ -860,6 +861,8 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--walk", type=int, default=0,
                     help="lane walk: 0 engine default, 1 exact fp64, 2 certified fp32 + exact re-walk")
+    ap.add_argument("--lag", type=int, default=0,
+                    help="1: overlapped chunks (opts.lag; exact walk without the dense phase)")
     ap.add_argument("--no-dense", action="store_true",
                     help="A/B: the lane walk gathers A1 too (no dense prefix phase)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

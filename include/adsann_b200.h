@@ -317,6 +317,11 @@ typedef struct {
                               fp64 re-walk of every undecided or possibly positive candidate (results
                               identical to the exact walk; 32-float segments); 0 (default)
                               picks 2 when a query streams >= 32 000 candidates on average, else 1 */
+    int32_t lag;           /* 1: overlapped chunks (exact walk on 16-byte lines without the dense phase):
+                              lanes that find a chunk's stream exhausted start on the next chunk, and
+                              every chunk c >= 2 is tested against the thresholds after chunk c - 2
+                              (chunk 1 against chunk 0's), a deterministic schedule the oracle replays;
+                              0 (default): every chunk sees the thresholds after the one before it */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 
@@ -338,10 +343,11 @@ int ads_ivf_search_device(ads_ivf *idx, const float *dQ_t, const float *dQ_raw, 
 /* The scan schedule ads_ivf_search would use for these arguments (no search runs):
  * the threshold refresh schedule (first, step: the oracle replays it), the CTA width,
  * the lane walk (1 exact fp64, 2 certified fp32 + exact re-walk) and whether the dense
- * A1 prefix phase runs.  Results depend on (first, step) only. */
+ * A1 prefix phase runs, and lag: 1 when the chunks overlap (opts.lag = 1 on a plan that
+ * takes it).  Results depend on (first, step, lag) only.  Outputs may be NULL. */
 int ads_ivf_search_plan(ads_ivf *idx, int32_t K, int32_t nprobe, int32_t mode, double epsilon0,
                         int32_t delta_d, const ads_search_opts *opts, int64_t *first, int64_t *step,
-                        int32_t *warps_per_cta, int32_t *walk, int32_t *dense);
+                        int32_t *warps_per_cta, int32_t *walk, int32_t *dense, int32_t *lag);
 /* probe_order, ivf.cpp:283-292, batched: nprobe list ids per query. */
 int ads_ivf_probe_order(ads_ivf *idx, const float *Q, int32_t nq, int32_t nprobe,
                         int32_t transformed, int32_t *probes);

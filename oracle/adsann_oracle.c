@@ -661,12 +661,15 @@ int orc_ivf_query_ext(const orc_ivf *idx, const float *q_t, const float *q_raw, 
 
 /* lag = 1: the positives of a chunk are offered one refresh later, so the
  * candidates of chunk j see the heap after chunks 0 .. j-2 (the GPU's mixed
- * scan re-walks a chunk's undecided candidates during the next chunk). */
+ * scan re-walks a chunk's undecided candidates during the next chunk).
+ * lag = 2: the same from chunk 2 on; chunk 1 still sees chunk 0's positives
+ * (the GPU's overlapped chunks, opts.lag = 1: chunk c >= 2 is tested against
+ * the thresholds after chunk c - 2, chunk 1 against chunk 0's). */
 int orc_ivf_query_lag(const orc_ivf *idx, const float *q_t, const float *q_raw, int32_t K,
                       int32_t nprobe, int mode, double eps0, int32_t delta_d, int64_t first,
                       int64_t step, int32_t lag, int32_t *ids, double *dists, int32_t *count,
                       uint64_t *stats) {
-    if (lag < 0 || lag > 1) return fail(1, "ivf_query: lag must be 0 or 1");
+    if (lag < 0 || lag > 2) return fail(1, "ivf_query: lag must be 0, 1 or 2");
     return ivf_query_impl(idx, q_t, q_raw, K, nprobe, mode, eps0, delta_d, first, step, 0, INFINITY,
                           NULL, 0, lag, ids, dists, count, stats);
 }
@@ -749,12 +752,13 @@ static int ivf_query_impl(const orc_ivf *idx, const float *q_t, const float *q_r
             pos += idx->list_off[probes[pi] + 1] - idx->list_off[probes[pi]];
         }
     }
-    int64_t i = 0;
+    int64_t i = 0, nref = 0;
     for (int32_t pi = probe_lo; pi < nprobe; ++pi) {
         const int32_t c = probes[pi];
         for (int64_t p = idx->list_off[c]; p < idx->list_off[c + 1]; ++p, ++i) {
             if (i == 0 || (waves ? mark[i] : (i >= first && (i - first) % step == 0))) {
-                if (lag) {
+                const int64_t ref = nref++; /* 0 at the stream start, c at the start of chunk c */
+                if (lag == 1 || (lag == 2 && ref >= 2)) {
                     for (int64_t j = 0; j < nheld; ++j) heap_offer(&heap, held[j].dist, held[j].id);
                     pair_t *t = held;
                     held = pending;

@@ -52,7 +52,7 @@ class SearchOpts(C.Structure):
     _fields_ = [("first", i64), ("step", i64), ("warps_per_cta", i32), ("queries_per_cta", i32),
                 ("ctas_per_sm", i32), ("time_stages", i32), ("scheduler", i32), ("tile", i32),
                 ("query_order", i32), ("coarse_mode", i32), ("rotate_mode", i32),
-                ("probe_lo", i32), ("r0", vp), ("walk", i32)]
+                ("probe_lo", i32), ("r0", vp), ("walk", i32), ("lag", i32)]
 
 
 def _sig(name, args, res=C.c_int):
@@ -114,7 +114,7 @@ ads_ivf_search = _sig("ads_ivf_search", [vp, vp, vp, i32, i32, i32, i32, f64, i3
 ads_ivf_search_device = _sig("ads_ivf_search_device", [vp, vp, vp, i32, i32, i32, i32, f64, i32,
                                                        C.POINTER(SearchOpts), vp, vp, vp, vp, vp])
 ads_ivf_search_plan = _sig("ads_ivf_search_plan", [vp, i32, i32, i32, f64, i32, C.POINTER(SearchOpts),
-                                                   vp, vp, vp, vp, vp])
+                                                   vp, vp, vp, vp, vp, vp])
 ads_ivf_probe_order = _sig("ads_ivf_probe_order", [vp, vp, i32, i32, i32, vp])
 ads_ivf_last_timings = _sig("ads_ivf_last_timings", [vp, vp])
 ads_ivf_coarse_stats = _sig("ads_ivf_coarse_stats", [vp, vp])

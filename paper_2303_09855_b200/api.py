@@ -516,21 +516,23 @@ def search_plan(idx: "IvfIndex", K: int, n_probe: int, mode: "IvfMode", cfg: "Dc
                 opts: Optional[L.SearchOpts] = None) -> dict:
     """The scan schedule a search with these arguments uses (ads_ivf_search_plan): the
     threshold refresh schedule (first, step), warps_per_cta, walk (1 exact, 2 certified
-    fp32) and dense (the A1 prefix phase).  Results depend on (first, step) only."""
+    fp32), dense (the A1 prefix phase) and lag (1: overlapped chunks; the oracle replays it
+    as lag = 2).  Results depend on (first, step, lag) only."""
     cfg = cfg or DcoConfig()
     o = opts or search_opts()
     first, step = C.c_int64(), C.c_int64()
-    warps, walk, dense = C.c_int32(), C.c_int32(), C.c_int32()
+    warps, walk, dense, lag = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
     check(L.ads_ivf_search_plan(idx.h, K, n_probe, int(mode), cfg.epsilon0, cfg.delta_d, C.byref(o),
-                                C.byref(first), C.byref(step), C.byref(warps), C.byref(walk), C.byref(dense)))
+                                C.byref(first), C.byref(step), C.byref(warps), C.byref(walk), C.byref(dense),
+                                C.byref(lag)))
     return {"first": first.value, "step": step.value, "warps_per_cta": warps.value, "walk": walk.value,
-            "dense": bool(dense.value)}
+            "dense": bool(dense.value), "lag": lag.value}
 
 
 def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_per_cta: int = 1,
                 ctas_per_sm: int = 0, time_stages: bool = False, scheduler: int = 0,
                 tile: int = 64, query_order: int = 2, coarse_mode: int = 0,
-                rotate_mode: int = 2, probe_lo: int = 0, r0=None, walk: int = 0) -> L.SearchOpts:
+                rotate_mode: int = 2, probe_lo: int = 0, r0=None, walk: int = 0, lag: int = 0) -> L.SearchOpts:
     """Search options (ads_search_opts, include/adsann_b200.h): first/step set the
     threshold refresh schedule in candidates; scheduler must be 0."""
     o = L.SearchOpts()
@@ -541,6 +543,7 @@ def search_opts(first: int = 0, step: int = 0, warps_per_cta: int = 0, queries_p
     o.rotate_mode = rotate_mode
     o.probe_lo = probe_lo
     o.walk = walk
+    o.lag = lag
     if r0 is not None:  # per-query initial radii (host array for the host API)
         if isinstance(r0, DeviceArray):
             o.r0 = r0.ptr

@@ -1286,6 +1286,7 @@ void ads_search_opts_default(ads_search_opts* o) {
     o->probe_lo = 0;
     o->r0 = nullptr;
     o->walk = 0;
+    o->lag = 0;
 }
 
 namespace {
@@ -1408,9 +1409,13 @@ void plan_scan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0,
     // at 8 warps: 768 -1.2 %, 1024 best; refreshing less often costs dims: +2 % at 1280
     // with 10 warps, profiles/r02/ab_step1), 128 per warp for the dense + fp32 walk, whose compact
     // chunk state keeps 9 CTAs per SM at 512 (config 5: +10 %; 768 +0.5 % at 8 CTAs)
+    require(o.lag == 0 || o.lag == 1, "search: lag must be 0 or 1");
+    // overlapped chunks: where the plain exact lane walk runs; two chunk states in shared
+    // memory, so half the refresh step
+    a.lag = (o.lag == 1 && a.vec == 4 && !a.f32 && !a.a1i && a.nseg0 == 0) ? 1 : 0;
     a.first = o.first;
     const int64_t per_warp = (a.a1i && a.f32) ? 128 : (D > 256 ? 128 : 64);
-    a.step = o.step > 0 ? o.step : per_warp * o.warps_per_cta;
+    a.step = o.step > 0 ? o.step : per_warp * o.warps_per_cta / (a.lag ? 2 : 1);
 }
 
 void search_device(ads_ivf* x, const float* dQt, const float* dQraw, int32_t nq, int32_t K,
@@ -1510,7 +1515,7 @@ int ads_ivf_search_device(ads_ivf* x, const float* dQt, const float* dQraw, int3
 
 int ads_ivf_search_plan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0, int32_t dd,
                         const ads_search_opts* opts, int64_t* first, int64_t* step, int32_t* warps_per_cta,
-                        int32_t* walk, int32_t* dense) {
+                        int32_t* walk, int32_t* dense, int32_t* lag) {
     return guard([&] {
         validate_search(x, true, true, K, nprobe, mode, eps0, dd);
         x->ctx->use();
@@ -1523,6 +1528,7 @@ int ads_ivf_search_plan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, dou
         if (warps_per_cta) *warps_per_cta = a.warps;
         if (walk) *walk = a.f32 ? 2 : 1;
         if (dense) *dense = a.a1i ? 1 : 0;
+        if (lag) *lag = a.lag;
     });
 }
 

@@ -109,6 +109,7 @@ struct SearchLaunch {
     const int32_t* order;  // nullable: work item w searches query order[w]
     const float* a1i;      // nullable: the interleaved A1 copy (d1 == 32, split, AD): dense prefix phase
     int f32;               // 1: certified fp32 walk + exact re-walk (full 32-float lines only)
+    int lag;               // 1: overlapped chunks, lag-1 refresh schedule (ivf_search_lag_kernel)
 };
 void launch_ivf_search(const SearchLaunch& a, cudaStream_t st);
 // CTAs of the search grid resident at once (num_sms x occupancy for this launch shape).

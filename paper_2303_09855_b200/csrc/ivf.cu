@@ -1052,6 +1052,359 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Overlapped chunks (opts.lag = 1; exact walk on 16-byte lines, no dense phase, no pre-walk).
+//
+// In ivf_search_kernel a chunk ends with a barrier (merge + threshold refresh), so its lanes
+// run dry one by one while the last long walks finish: with 30-segment walks about a quarter
+// of all lane steps are idle (config 3: 25 of 32 lanes live per instruction, against 32 for
+// FDScanning on the same engine, which is the whole gap between the two).  Here lanes that
+// find chunk w's stream exhausted claim candidates of chunk w + 1 at once.  For the result
+// to be a function of the schedule alone, ALL of chunk c (>= 2) is tested against the
+// thresholds after the merge of chunk c - 2 (the lag-1 schedule; chunk 1 waits for chunk 0,
+// whose r = +inf would otherwise send a whole extra chunk to d = D).  The merge stays
+// synchronous and in chunk order: window w ends when every candidate of chunk w has retired
+// (each warp reports once that the stream is exhausted and it holds none); candidates of
+// chunk w + 1 in flight stay in their lanes' registers across the barrier and carry on in
+// window w + 1.  Chunk state (slot -> position / id, positives' distances, flags), the
+// thresholds and r exist twice, by chunk parity.  The oracle replays the schedule
+// (orc_ivf_query_lag, lag = 2), so results are bit-exact against it.
+struct LagShared {
+    int nextp[2];    // claim pointers of the two chunks in flight, by parity
+    unsigned quiet;  // warps that hold no candidate of the window's chunk any more
+    double r[2], r_sq[2];
+};
+
+template <bool FULL>
+__global__ void __maxnreg__(64) ivf_search_lag_kernel(SearchLaunch a, int chunk_cap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ SearchShared sh;
+    __shared__ LagShared lg;
+    const int nwarps = blockDim.x >> 5;
+    const int nt = a.ntest > 0 ? a.ntest : 1;
+    const int pw32 = (chunk_cap + 31) >> 5;
+    float* wbuf_all = reinterpret_cast<float*>(smem_raw);
+    double* qseg = reinterpret_cast<double*>(wbuf_all + nwarps * 1024);
+    double* thr2 = qseg + a.nseg * kQPitch;  // [2][nt]
+    double* tfac = thr2 + 2 * nt;
+    double* topd = tfac + nt;
+    double* pend2 = topd + a.K;  // [2][chunk_cap] positives' distances
+    int32_t* lstart = reinterpret_cast<int32_t*>(pend2 + 2 * chunk_cap);
+    int32_t* cpos2 = lstart + a.nprobe;  // [2][chunk_cap] slot -> position, then the positive's id
+    Seg* segs = reinterpret_cast<Seg*>(cpos2 + 2 * chunk_cap + (a.nprobe & 1));
+    int32_t* topi = reinterpret_cast<int32_t*>(segs + a.nseg);
+    int32_t* pre = topi + a.K;
+    unsigned* pflag2 = reinterpret_cast<unsigned*>(pre + a.nprobe + 1);  // [2][pw32]
+    int* wc = reinterpret_cast<int*>(wbuf_all);
+    if (threadIdx.x == 0 && (__cvta_generic_to_shared(smem_raw) & 127u)) __trap();
+
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const unsigned allw = nwarps >= 32 ? ~0u : (1u << nwarps) - 1u;
+    float* wbuf = wbuf_all + warp * 1024;
+    for (int i = threadIdx.x; i < a.nseg; i += blockDim.x) segs[i] = a.segs[i];
+    for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) tfac[i] = a.tfac[i];
+    const uint32_t str1 = static_cast<uint32_t>(a.d1) >> 2, str2 = static_cast<uint32_t>(a.D - a.d1) >> 2;
+    const uint32_t a2c = a.a2_16 - (static_cast<uint32_t>(a.d1) >> 2);
+    const char* gbase = lane_base16(a.a1);
+    const int nl = a.nprobe - a.probe_lo;
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int w = static_cast<int>(atomicAdd(a.counter, 1ull));
+            sh.stop = w >= a.nq;
+            sh.q = sh.stop ? w : (a.order ? a.order[w] : w);
+            sh.cnt = 0;
+            const double r0 = (!sh.stop && a.r0) ? a.r0[sh.q] : kInf;
+            sh.r = r0;
+            sh.r_sq = __dmul_rn(r0, r0);
+            lg.r[0] = lg.r[1] = r0;
+            lg.r_sq[0] = lg.r_sq[1] = sh.r_sq;
+            sh.dims = 0;
+        }
+        __syncthreads();
+        if (sh.stop) break;
+        const int qi = sh.q;
+        stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) {
+            const double t = __dmul_rn(tfac[i], sh.r_sq);
+            thr2[i] = t;
+            thr2[nt + i] = t;
+        }
+        if (warp == 0) {  // probed lists -> stream prefix offsets
+            int carry = 0;
+            for (int base = 0; base < nl; base += 32) {
+                const int i = base + static_cast<int>(lane);
+                int len = 0;
+                if (i < nl) {
+                    const int p = a.probes[static_cast<int64_t>(qi) * a.nprobe + a.probe_lo + i];
+                    const int64_t s0 = a.list_off[p];
+                    lstart[i] = static_cast<int32_t>(s0);
+                    len = static_cast<int>(a.list_off[p + 1] - s0);
+                }
+                int incl = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(kFull, incl, o);
+                    if (static_cast<int>(lane) >= o) incl += v;
+                }
+                if (i < nl) pre[i + 1] = carry + incl;
+                carry += __shfl_sync(kFull, incl, 31);
+            }
+            if (lane == 0) {
+                pre[0] = 0;
+                sh.total = carry;
+            }
+        }
+        __syncthreads();
+        const int total = sh.total;
+        unsigned long long my_dims = 0;
+        // chunk c = [clo(c), clo(c + 1)): first, then step candidates each
+        auto clo = [&](int c) -> int {
+            if (c <= 0) return 0;
+            const int64_t v = a.first + static_cast<int64_t>(c - 1) * a.step;
+            return static_cast<int>(v < total ? v : total);
+        };
+        const int nchunks = total <= 0 ? 0
+                                       : 1 + (total > a.first ? static_cast<int>((total - a.first + a.step - 1) / a.step) : 0);
+        // slot -> flat position of chunk c into its parity's map; flags cleared
+        auto map_chunk = [&](int c) {
+            const int lo = clo(c), n = clo(c + 1) - lo;
+            int32_t* cp = cpos2 + (c & 1) * chunk_cap;
+            const int per = (n + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
+            const int s0 = static_cast<int>(threadIdx.x) * per, s1 = min(n, s0 + per);
+            if (s0 < s1) {
+                int l = 0, h = nl - 1;
+                while (l < h) {
+                    const int mid = (l + h + 1) >> 1;
+                    if (pre[mid] <= lo + s0) l = mid;
+                    else h = mid - 1;
+                }
+                for (int sl = s0; sl < s1; ++sl) {
+                    while (pre[l + 1] <= lo + sl) ++l;
+                    cp[sl] = lstart[l] + (lo + sl - pre[l]);
+                }
+            }
+            for (int w = threadIdx.x; w < (n + 31) / 32; w += blockDim.x) pflag2[(c & 1) * pw32 + w] = 0;
+        };
+        if (nchunks > 0) map_chunk(0);
+        if (threadIdx.x == 0) lg.nextp[0] = 0;
+
+        // lane state: cand = slot | parity << 30 (or -1); lives across windows
+        int cand = -1, seg = 0, pos = 0;
+        double s = 0.0;
+        for (int w = 0; w < nchunks; ++w) {
+            const int pw = w & 1, pn = pw ^ 1;
+            const int lo = clo(w), hi = clo(w + 1), nhi = clo(w + 2);
+            const bool spill = w >= 1 && w + 1 < nchunks;  // chunk 1 waits for chunk 0's merge
+            if (w + 1 < nchunks) map_chunk(w + 1);
+            if (threadIdx.x == 0) {
+                lg.nextp[pn] = hi;
+                lg.quiet = 0;
+            }
+            __syncthreads();
+            bool dry_cur = false, dry_nxt = !spill, quiet_me = false;  // warp-uniform
+            for (;;) {
+                if (*reinterpret_cast<volatile unsigned*>(&lg.quiet) == allw) break;
+                unsigned need = __ballot_sync(kFull, cand < 0);
+                if (need && !dry_cur) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&lg.nextp[pw], __popc(need));
+                    base = __shfl_sync(kFull, base, 0);
+                    dry_cur = base + __popc(need) > hi;
+                    const int i = base + __popc(need & ((1u << lane) - 1u));
+                    if (cand < 0 && i < hi) {
+                        cand = (i - lo) | (pw << 30);
+                        pos = cpos2[pw * chunk_cap + (i - lo)];
+                        seg = 0;
+                        s = 0.0;
+                    }
+                    need = __ballot_sync(kFull, cand < 0);
+                }
+                if (need && !dry_nxt) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&lg.nextp[pn], __popc(need));
+                    base = __shfl_sync(kFull, base, 0);
+                    dry_nxt = base + __popc(need) > nhi;
+                    const int i = base + __popc(need & ((1u << lane) - 1u));
+                    if (cand < 0 && i < nhi) {
+                        cand = (i - hi) | (pn << 30);
+                        pos = cpos2[pn * chunk_cap + (i - hi)];
+                        seg = 0;
+                        s = 0.0;
+                    }
+                }
+                if (dry_cur && !quiet_me) {
+                    if (!__any_sync(kFull, cand >= 0 && (cand >> 30) == pw)) {
+                        quiet_me = true;
+                        __threadfence_block();  // this warp's positives of chunk w are written
+                        if (lane == 0) atomicOr(&lg.quiet, 1u << warp);
+                    }
+                }
+                const unsigned livem = __ballot_sync(kFull, cand >= 0);
+                if (!livem) {
+                    if (quiet_me && dry_nxt) break;  // nothing to carry, nothing left to claim
+                    continue;
+                }
+                const int nlive = __popc(livem);
+                const int par = cand >= 0 ? cand >> 30 : 0;
+                if (nlive <= kDeepTail && a.nseg >= kDeepMinSeg) {  // deep tail step (ivf_search_kernel, DEEP)
+                    int ks = 1;
+#pragma unroll
+                    for (int t = 2; t <= kDeepShift; ++t) ks += nlive <= (32 >> t) ? 1 : 0;
+                    const int rnk = static_cast<int>(lane) >> ks, off = static_cast<int>(lane) & ((1 << ks) - 1);
+                    const unsigned srcl = __fns(livem, 0, rnk + 1) & 31u;
+                    const int ppos = __shfl_sync(kFull, pos, srcl), pseg = __shfl_sync(kFull, seg, srcl);
+                    const int rseg = pseg + off;
+                    uint32_t dsc = kNoLine;
+                    int nch = 0;
+                    if (rnk < nlive && rseg < a.nseg) {
+                        const Seg g = segs[rseg];
+                        dsc = g.arr == 0 ? static_cast<uint32_t>(ppos) * str1 + (g.col >> 2)
+                                         : static_cast<uint32_t>(ppos) * str2 + a2c + (g.col >> 2);
+                        nch = g.len >> 2;
+                    }
+                    gather_issue16<FULL>(wbuf, gbase, dsc, nch);
+                    cp_async_wait_group<0>();
+                    __syncwarp();
+                    if (cand >= 0) {
+                        const unsigned row0 = static_cast<unsigned>(__popc(livem & ((1u << lane) - 1u))) << ks;
+                        const double* thr = thr2 + par * nt;
+                        for (int m = 0; m < (1 << ks); ++m) {
+                            const Seg sg = segs[seg];
+                            s = accumulate_row<FULL>(wbuf, row0 + m, qseg + seg * kQPitch, sg.len, s);
+                            if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
+                                my_dims += static_cast<unsigned long long>(sg.col + sg.len);
+                                cand = -1;
+                                break;
+                            }
+                            if (seg == a.nseg - 1) {  // d == D (dco.hpp:145; ivf.cpp:335-338)
+                                my_dims += static_cast<unsigned long long>(a.D);
+                                const bool positive = a.final_fd ? __dsqrt_rn(s) <= lg.r[par] : s <= lg.r_sq[par];
+                                if (positive) {
+                                    const int slot = cand & 0x3fffffff;
+                                    pend2[par * chunk_cap + slot] = __dsqrt_rn(s);
+                                    cpos2[par * chunk_cap + slot] = a.ids[pos];
+                                    atomicOr(&pflag2[par * pw32 + (slot >> 5)], 1u << (slot & 31));
+                                }
+                                cand = -1;
+                                break;
+                            }
+                            ++seg;
+                        }
+                    }
+                    __syncwarp();
+                    continue;
+                }
+                const Seg sg = segs[seg];
+                uint32_t dsc = kNoLine;
+                if (cand >= 0)
+                    dsc = sg.arr == 0 ? static_cast<uint32_t>(pos) * str1 + (sg.col >> 2)
+                                      : static_cast<uint32_t>(pos) * str2 + a2c + (sg.col >> 2);
+                gather_issue16<FULL>(wbuf, gbase, dsc, sg.len >> 2);
+                cp_async_wait_group<0>();
+                __syncwarp();
+                if (cand >= 0) {
+                    s = accumulate_line<4, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                    if (sg.test >= 0 && s > thr2[par * nt + sg.test]) {  // reject (dco.hpp:141)
+                        my_dims += static_cast<unsigned long long>(sg.col + sg.len);
+                        cand = -1;
+                    } else if (seg == a.nseg - 1) {  // d == D (dco.hpp:145; ivf.cpp:335-338)
+                        my_dims += static_cast<unsigned long long>(a.D);
+                        const bool positive = a.final_fd ? __dsqrt_rn(s) <= lg.r[par] : s <= lg.r_sq[par];
+                        if (positive) {
+                            const int slot = cand & 0x3fffffff;
+                            pend2[par * chunk_cap + slot] = __dsqrt_rn(s);
+                            cpos2[par * chunk_cap + slot] = a.ids[pos];
+                            atomicOr(&pflag2[par * pw32 + (slot >> 5)], 1u << (slot & 31));
+                        }
+                        cand = -1;
+                    } else {
+                        ++seg;
+                    }
+                }
+            }
+            __syncthreads();
+            // merge chunk w in candidate order (as ivf_search_kernel), then the thresholds of
+            // chunk w + 2 (and of chunk 1 after chunk 0) into chunk w's parity
+            double* pend_d = pend2 + pw * chunk_cap;
+            int32_t* pend_i = cpos2 + pw * chunk_cap;
+            const unsigned* pflag = pflag2 + pw * pw32;
+            const int n = hi - lo;
+            int npos = 0;
+            for (int k = 0; k < (n + 31) >> 5; ++k) npos += __popc(pflag[k]);
+            int seq = -1;
+            if (npos > 32 && n <= 2 * static_cast<int>(blockDim.x) && sh.cnt <= 2 * static_cast<int>(blockDim.x)) {
+                const int rc = cta_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n, wc);
+                if (rc < 0) seq = -rc - 1;
+                npos = 0;
+            }
+            if (warp == 0) {
+                bool merged = npos == 0;
+                if (!merged && npos <= 32) merged = warp_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n);
+                for (int k = 0; k < seq; ++k) warp_offer(topd, topi, &sh.cnt, a.K, pend_d[k], pend_i[k]);
+                const int nw = merged ? 0 : (n + 31) / 32;
+                for (int k = 0; k < nw; ++k) {
+                    unsigned bits = pflag[k];
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const int slot = k * 32 + b;
+                        warp_offer(topd, topi, &sh.cnt, a.K, pend_d[slot], pend_i[slot]);
+                    }
+                }
+                if (sh.cnt == a.K) {  // ivf.cpp:268-270; dco.hpp:125
+                    const double rn = topd[a.K - 1];
+                    const double rsq = __dmul_rn(rn, rn);
+                    for (int i = static_cast<int>(lane); i < a.ntest; i += 32) {
+                        const double t = __dmul_rn(tfac[i], rsq);
+                        thr2[pw * nt + i] = t;
+                        if (w == 0) thr2[pn * nt + i] = t;
+                    }
+                    if (lane == 0) {
+                        sh.r = rn;
+                        sh.r_sq = rsq;
+                        lg.r[pw] = rn;
+                        lg.r_sq[pw] = rsq;
+                        if (w == 0) {
+                            lg.r[pn] = rn;
+                            lg.r_sq[pn] = rsq;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) my_dims += __shfl_xor_sync(kFull, my_dims, o);
+        if (lane == 0) atomicAdd(&sh.dims, my_dims);
+        __syncthreads();
+        const int cnt = sh.cnt;
+        for (int i = threadIdx.x; i < a.K; i += blockDim.x) {
+            const int64_t o = static_cast<int64_t>(qi) * a.K + i;
+            a.out_ids[o] = i < cnt ? topi[i] : -1;
+            a.out_dists[o] = i < cnt ? topd[i] : __longlong_as_double(0x7ff8000000000000ll);
+        }
+        if (threadIdx.x == 0) {
+            a.out_cnt[qi] = cnt;
+            a.out_dims[qi] = sh.dims;
+            if (a.out_cand) a.out_cand[qi] = static_cast<unsigned long long>(total);
+        }
+    }
+}
+
+size_t search_smem_lag(const SearchLaunch& a, int chunk_cap) {
+    const int nt = a.ntest > 0 ? a.ntest : 1;
+    size_t b = sizeof(float) * a.warps * 1024;
+    b += sizeof(double) * (a.nseg * kQPitch + 3 * nt + a.K + 2 * chunk_cap);
+    b += sizeof(int32_t) * (a.nprobe + 2 * chunk_cap + (a.nprobe & 1));
+    b += sizeof(Seg) * a.nseg;
+    b += sizeof(int32_t) * (a.K + a.nprobe + 1);
+    b += sizeof(unsigned) * 2 * ((chunk_cap + 31) / 32);
+    return b;
+}
+
 size_t search_smem(const SearchLaunch& a, int chunk_cap) {
     const int nt = a.ntest > 0 ? a.ntest : 1;
     const bool dense = a.a1i != nullptr, f32 = a.f32 && a.vec == 4 && a.full;
@@ -1191,6 +1544,11 @@ bool search_deep(const SearchLaunch& a) {
     return kDeepTail > 0 && a.vec == 4 && !a.f32 && a.nseg0 == 0 && a.nseg >= kDeepMinSeg;
 }
 
+// Overlapped chunks (ivf_search_lag_kernel): on request, where the plain lane walk runs.
+bool search_lag(const SearchLaunch& a) {
+    return a.lag != 0 && a.vec == 4 && !a.f32 && !a.a1i && a.nseg0 == 0;
+}
+
 SearchShape search_shape_of(const SearchLaunch& a) {
     const int64_t cap64 = a.first > a.step ? a.first : a.step;
     if (a.first < 1 || a.step < 1) throw std::invalid_argument("search: threshold schedule must be >= 1");
@@ -1198,7 +1556,10 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     SearchShape sh{};
     sh.cap = static_cast<int>(cap64);
     sh.smem = search_smem(a, sh.cap);
-    if (a.f32 && a.vec == 4 && a.full)
+    if (search_lag(a)) {
+        sh.smem = search_smem_lag(a, sh.cap);
+        sh.kern = a.full ? ivf_search_lag_kernel<true> : ivf_search_lag_kernel<false>;
+    } else if (a.f32 && a.vec == 4 && a.full)
         sh.kern = a.a1i ? ivf_search_kernel<4, true, true, true> : ivf_search_kernel<4, true, false, true>;
     else if (search_deep(a))
         sh.kern = a.a1i ? (a.full ? ivf_search_kernel<4, true, true, false, true> : ivf_search_kernel<4, false, true, false, true>)

@@ -620,6 +620,44 @@ def test_ivf_deep_tail_steps_bitexact(eng, orc, case, warps, monkeypatch):
                     assert_same_results(res, orc, lay, qt, qr, K, nprobe, mode, 2.1, dd, first, step)
 
 
+@pytest.mark.parametrize("case", [(2500, 960, 12, 16, 32, 32),   # config 3's plan: 30 full segments
+                                  (2500, 300, 12, 16, 32, 32),   # ragged last segment
+                                  (3000, 128, 16, 20, 32, 32),   # config 2's plan: 4 segments
+                                  (2000, 512, 8, 12, 64, 16)])   # 16-float segments, d1 = 64
+@pytest.mark.parametrize("warps", [0, 4])
+def test_ivf_overlapped_chunks_bitexact(eng, orc, case, warps):
+    """opts.lag = 1: lanes that find a chunk's stream exhausted start on the next chunk;
+    chunk c >= 2 is tested against the thresholds after chunk c - 2, chunk 1 against chunk
+    0's, with the merges in chunk order.  The oracle replays that schedule (lag = 2): ids,
+    distances, dims and candidate counts are bit-exact, at schedules from one candidate per
+    chunk to one chunk per query, and the plan reports the overlap."""
+    n, d, blobs, k, d1, dd = case
+    raw, t, qr, qt, P = make_fixture(orc, n, d, blobs, 12, 800 + d)
+    lay = oracle_index(orc, raw, t, P, k, 801, d1=d1)
+    idx = gpu_index(eng, lay, P)
+    cfg = eng.DcoConfig(2.1, dd)
+    K = 10
+    for mode in ("ad-split", "ad", "pd-split"):
+        for first, step in ((1, 1), (K, 64), (K, 7), (K, 5000), (3, 50), (K, 0)):
+            for nprobe in (2, k):
+                opts = eng.search_opts(first=first, step=step, tile=-1, warps_per_cta=warps, walk=1, lag=1)
+                plan = eng.search_plan(idx, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg, opts=opts)
+                assert plan["lag"] == 1 and plan["first"] == first
+                res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg, opts=opts)
+                for qi in range(qt.shape[0]):
+                    ids, dists, stats = orc.ivf_query(lay, qt[qi], qr[qi], K, nprobe, mode, 2.1, dd,
+                                                      plan["first"], plan["step"], lag=2)
+                    c = int(res.counts[qi])
+                    assert c == len(ids), (mode, first, step, nprobe, qi)
+                    np.testing.assert_array_equal(res.ids[qi, :c], ids, err_msg=f"{mode} {first}/{step} np={nprobe} q={qi}")
+                    np.testing.assert_array_equal(res.dists[qi, :c], dists)
+                    assert int(res.dims[qi]) == int(stats[0]), (mode, first, step, nprobe, qi)
+                    assert int(res.candidates[qi]) == int(stats[2])
+    # where the plan cannot overlap (the FD walk pre-walks its untested prefix) lag is ignored
+    plan = eng.search_plan(idx, K, 2, eng.IvfMode.kFd, cfg, opts=eng.search_opts(lag=1))
+    assert plan["lag"] == 0
+
+
 def test_ivf_long_lists_default_path_bitexact(eng, orc):
     """The default path at config 5's shape of work: 6 250-row lists (the interleaved A1
     copy and its dense prefix phase) and 100 000 candidates per query (the certified fp32
