@@ -436,7 +436,7 @@ def measure(S, cfg, nprobe, args, D, log, steps):
         "dims_fraction": float(dims.mean()) / (float(cand.mean()) * d),
         "clocks": clk, "ids": ids,
         "threshold_refresh": {"first": plan["first"], "step": plan["step"]},
-        "warps_per_cta": plan["warps_per_cta"], "walk": plan["walk"], "dense_prefix": plan["dense"],
+        "warps_per_cta": plan["warps_per_cta"], "walk": plan["walk"], "dense_prefix": plan["dense"], "overlapped_chunks": bool(plan["lag"]),
     }
 
 
@@ -541,7 +541,7 @@ def run_search(args, D):
         "stages_ms": M["stages_ms"], "dims_per_query": M["dims_per_query"],
         "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
         "threshold_refresh": M["threshold_refresh"], "warps_per_cta": M["warps_per_cta"],
-        "walk": M["walk"], "dense_prefix": M["dense_prefix"],
+        "walk": M["walk"], "dense_prefix": M["dense_prefix"], "overlapped_chunks": M["overlapped_chunks"],
         "query_rotation": "raw queries rotated on the device each step: 3xTF32 tcgen05 (rotate_mode 2)",
         "setup": S["info"],
     }
@@ -862,7 +862,7 @@ def main():
     ap.add_argument("--walk", type=int, default=0,
                     help="lane walk: 0 engine default, 1 exact fp64, 2 certified fp32 + exact re-walk")
     ap.add_argument("--lag", type=int, default=0,
-                    help="1: overlapped chunks (opts.lag; exact walk without the dense phase)")
+                    help="overlapped chunks (opts.lag): 0 engine default, 1 on, -1 off")
     ap.add_argument("--no-dense", action="store_true",
                     help="A/B: the lane walk gathers A1 too (no dense prefix phase)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -317,11 +317,14 @@ typedef struct {
                               fp64 re-walk of every undecided or possibly positive candidate (results
                               identical to the exact walk; 32-float segments); 0 (default)
                               picks 2 when a query streams >= 32 000 candidates on average, else 1 */
-    int32_t lag;           /* 1: overlapped chunks (exact walk on 16-byte lines without the dense phase):
-                              lanes that find a chunk's stream exhausted start on the next chunk, and
-                              every chunk c >= 2 is tested against the thresholds after chunk c - 2
-                              (chunk 1 against chunk 0's), a deterministic schedule the oracle replays;
-                              0 (default): every chunk sees the thresholds after the one before it */
+    int32_t lag;           /* overlapped chunks (exact walk on 16-byte lines, no dense phase, no untested
+                              prefix): lanes that find a chunk's stream exhausted start on the next
+                              chunk, and every chunk c >= 2 is tested against the thresholds after
+                              chunk c - 2 (chunk 1 against chunk 0's), a deterministic schedule the
+                              oracle replays.  1: wherever the plan takes it; -1: never (every chunk
+                              sees the thresholds after the one before it); 0 (default): when the engine
+                              also picks the schedule (step 0, no probe_lo / r0) and walks are >= 8
+                              segments.  ads_ivf_search_plan reports the choice. */
 } ads_search_opts;
 void ads_search_opts_default(ads_search_opts *o);
 

@@ -1409,10 +1409,15 @@ void plan_scan(ads_ivf* x, int32_t K, int32_t nprobe, int32_t mode, double eps0,
     // at 8 warps: 768 -1.2 %, 1024 best; refreshing less often costs dims: +2 % at 1280
     // with 10 warps, profiles/r02/ab_step1), 128 per warp for the dense + fp32 walk, whose compact
     // chunk state keeps 9 CTAs per SM at 512 (config 5: +10 %; 768 +0.5 % at 8 CTAs)
-    require(o.lag == 0 || o.lag == 1, "search: lag must be 0 or 1");
-    // overlapped chunks: where the plain exact lane walk runs; two chunk states in shared
-    // memory, so half the refresh step
-    a.lag = (o.lag == 1 && a.vec == 4 && !a.f32 && !a.a1i && a.nseg0 == 0) ? 1 : 0;
+    require(o.lag >= -1 && o.lag <= 1, "search: lag must be -1, 0 or 1");
+    // overlapped chunks (ivf_search_lag_kernel): where the plain exact lane walk runs; two
+    // chunk states in shared memory, so half the refresh step.  lag 0 takes them when the
+    // engine also picks the schedule (step 0, no probe range / initial radius) and walks are
+    // long (>= 8 segments; config 3: 61.4 -> 57.2 ms, profiles/r02/ab_tail/ab_lag_planes.log);
+    // a caller that pins first / step gets exactly that schedule unless it sets lag = 1.
+    const bool lag_ok = a.vec == 4 && !a.f32 && !a.a1i && a.nseg0 == 0;
+    const bool lag_auto = o.lag == 0 && o.step <= 0 && o.probe_lo == 0 && o.r0 == nullptr && a.nseg >= 8;
+    a.lag = (lag_ok && (o.lag == 1 || lag_auto)) ? 1 : 0;
     a.first = o.first;
     const int64_t per_warp = (a.a1i && a.f32) ? 128 : (D > 256 ? 128 : 64);
     a.step = o.step > 0 ? o.step : per_warp * o.warps_per_cta / (a.lag ? 2 : 1);

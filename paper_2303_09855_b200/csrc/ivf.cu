@@ -231,6 +231,11 @@ __device__ void warp_offer(double* topd, int32_t* topi, int* cnt, int K, double 
     __syncwarp();
 }
 
+#ifndef ADS_QUERY_PLANES
+#define ADS_QUERY_PLANES 1
+#endif
+constexpr bool kQueryPlanes = ADS_QUERY_PLANES != 0;  // scan_engine.cuh, stage_query_planes
+
 // Live candidates per warp at or below which a step goes deep (0: off).
 #ifndef ADS_DEEP_TAIL
 #define ADS_DEEP_TAIL 16
@@ -493,6 +498,11 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
     static_assert(!DEEP || (VEC == 4 && !F32), "deep tail steps: 16-byte lines, exact walk");
     static_assert(!F32 || (VEC == 4 && FULL), "the fp32 walk runs on full 32-float lines");
     using acc_t = typename std::conditional<F32, float, double>::type;
+    // the staged query as bank-conflict-free planes (scan_engine.cuh) where every lane read is
+    // a full segment of the exact walk and no dense phase reads it as doubles
+    // (long plans only, i.e. the DEEP instances: on config 2's 4 segments, whose rows never
+    // collide, the extra unpacking measured -6 %)
+    constexpr bool QP = kQueryPlanes && DEEP && FULL && !DENSE;
     extern __shared__ __align__(128) unsigned char smem_raw[];  // gather rows: 128-byte aligned (swizzle)
     __shared__ SearchShared sh;
     const int nwarps = blockDim.x >> 5;
@@ -592,6 +602,7 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
         if (sh.stop) break;
         const int qi = sh.q;
         if constexpr (F32) stage_query_f32(qsegf, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        else if constexpr (QP) stage_query_planes(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
         else stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
         for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) {
             thr[i] = __dmul_rn(tfac[i], sh.r_sq);
@@ -851,7 +862,8 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                             const unsigned row0 = static_cast<unsigned>(__popc(livem & ((1u << lane) - 1u))) << ks;
                             for (int m = 0; m < (1 << ks); ++m) {
                                 const Seg sg = segs[seg];
-                                s = accumulate_row<FULL>(wbuf, row0 + m, qseg + seg * kQPitch, sg.len, s);
+                                if constexpr (QP) s = accumulate_planes(wbuf, row0 + m, qseg, a.nseg, seg, s);
+                                else s = accumulate_row<FULL>(wbuf, row0 + m, qseg + seg * kQPitch, sg.len, s);
                                 if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
                                     my_dims += static_cast<unsigned long long>(sg.col + sg.len);
                                     cand = -1;
@@ -893,6 +905,7 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                 __syncwarp();
                 if (cand >= 0) {
                     if constexpr (F32) s = accumulate_line_f32(wbuf, qsegf + seg * kQPitchF, s);
+                    else if constexpr (QP) s = accumulate_planes(wbuf, lane, qseg, a.nseg, seg, s);
                     else s = accumulate_line<VEC, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
                     if constexpr (F32) {
                         // decide only what the band proves; the rest is re-walked exactly
@@ -1075,8 +1088,10 @@ struct LagShared {
     double r[2], r_sq[2];
 };
 
-template <bool FULL>
+template <bool FULL, bool PLANES>
 __global__ void __maxnreg__(64) ivf_search_lag_kernel(SearchLaunch a, int chunk_cap) {
+    static_assert(!PLANES || FULL, "query planes hold full 32-float segments");
+    constexpr bool QP = PLANES;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ SearchShared sh;
     __shared__ LagShared lg;
@@ -1126,7 +1141,8 @@ __global__ void __maxnreg__(64) ivf_search_lag_kernel(SearchLaunch a, int chunk_
         __syncthreads();
         if (sh.stop) break;
         const int qi = sh.q;
-        stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        if constexpr (QP) stage_query_planes(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
+        else stage_query(qseg, segs, a.nseg, a.Q + static_cast<int64_t>(qi) * a.D);
         for (int i = threadIdx.x; i < a.ntest; i += blockDim.x) {
             const double t = __dmul_rn(tfac[i], sh.r_sq);
             thr2[i] = t;
@@ -1273,7 +1289,8 @@ __global__ void __maxnreg__(64) ivf_search_lag_kernel(SearchLaunch a, int chunk_
                         const double* thr = thr2 + par * nt;
                         for (int m = 0; m < (1 << ks); ++m) {
                             const Seg sg = segs[seg];
-                            s = accumulate_row<FULL>(wbuf, row0 + m, qseg + seg * kQPitch, sg.len, s);
+                            if constexpr (QP) s = accumulate_planes(wbuf, row0 + m, qseg, a.nseg, seg, s);
+                            else s = accumulate_row<FULL>(wbuf, row0 + m, qseg + seg * kQPitch, sg.len, s);
                             if (sg.test >= 0 && s > thr[sg.test]) {  // reject (dco.hpp:141)
                                 my_dims += static_cast<unsigned long long>(sg.col + sg.len);
                                 cand = -1;
@@ -1306,7 +1323,8 @@ __global__ void __maxnreg__(64) ivf_search_lag_kernel(SearchLaunch a, int chunk_
                 cp_async_wait_group<0>();
                 __syncwarp();
                 if (cand >= 0) {
-                    s = accumulate_line<4, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
+                    if constexpr (QP) s = accumulate_planes(wbuf, lane, qseg, a.nseg, seg, s);
+                    else s = accumulate_line<4, FULL>(wbuf, qseg + seg * kQPitch, sg.len, s);
                     if (sg.test >= 0 && s > thr2[par * nt + sg.test]) {  // reject (dco.hpp:141)
                         my_dims += static_cast<unsigned long long>(sg.col + sg.len);
                         cand = -1;
@@ -1558,7 +1576,9 @@ SearchShape search_shape_of(const SearchLaunch& a) {
     sh.smem = search_smem(a, sh.cap);
     if (search_lag(a)) {
         sh.smem = search_smem_lag(a, sh.cap);
-        sh.kern = a.full ? ivf_search_lag_kernel<true> : ivf_search_lag_kernel<false>;
+        sh.kern = a.full ? ((kQueryPlanes && a.nseg >= kDeepMinSeg) ? ivf_search_lag_kernel<true, true>
+                                                                     : ivf_search_lag_kernel<true, false>)
+                         : ivf_search_lag_kernel<false, false>;
     } else if (a.f32 && a.vec == 4 && a.full)
         sh.kern = a.a1i ? ivf_search_kernel<4, true, true, true> : ivf_search_kernel<4, true, false, true>;
     else if (search_deep(a))

@@ -231,6 +231,62 @@ __device__ __forceinline__ float accumulate_line_f32(const float* wbuf, const fl
     return s;
 }
 
+// Query planes (exact walk on full 32-float segments).  Lanes of a warp sit at different
+// segments, so the staged query is read at up to 32 different rows per instruction: as
+// double2 rows (stage_query) those reads collide in the shared-memory banks and the data
+// pipe becomes the scan's limiter (ncu on config 3: 85 % of its wavefront peak, 6.6
+// wavefronts per query read, 100 of a step's 148).  The planes split (double)q into its
+// high words, one 33-word row per segment -- bank (seg + k) mod 32, so 32 lanes at up to 32
+// different segments read coordinate k in ONE wavefront -- and the low words, which for a
+// converted float hold only mantissa bits 0..2 in bits 29..31 (also for denormals, inf, NaN):
+// 3 bits per coordinate, ten coordinates per word, four words per segment (one 16-byte read
+// per step).  q = hiloint2double(hi, (word << (29 - 3p)) & 0xE0000000) is (double)q exactly.
+constexpr int kQHiPitch = 33;  // words per segment row of the high-word plane
+__device__ __forceinline__ const uint32_t* q_lo_plane(const double* qseg, int nseg) {
+    return reinterpret_cast<const uint32_t*>(qseg) + ((nseg * kQHiPitch + 3) & ~3);
+}
+__device__ __forceinline__ void stage_query_planes(double* qseg, const Seg* segs, int nseg, const float* q) {
+    uint32_t* hi = reinterpret_cast<uint32_t*>(qseg);
+    uint32_t* lo = const_cast<uint32_t*>(q_lo_plane(qseg, nseg));
+    for (int i = threadIdx.x; i < nseg * 32; i += blockDim.x) {
+        const int sgi = i >> 5, k = i & 31;
+        hi[sgi * kQHiPitch + k] = static_cast<uint32_t>(__double2hiint(static_cast<double>(q[segs[sgi].col + k])));
+    }
+    for (int i = threadIdx.x; i < nseg * 4; i += blockDim.x) {
+        const int sgi = i >> 2, w = i & 3;
+        uint32_t pack = 0;
+        for (int p = 0; p < 10; ++p) {
+            const int k = w * 10 + p;
+            if (k < 32) {
+                const uint32_t l = static_cast<uint32_t>(__double2loint(static_cast<double>(q[segs[sgi].col + k])));
+                pack |= (l >> 29) << (3 * p);
+            }
+        }
+        lo[sgi * 4 + w] = pack;
+    }
+}
+// The lane's gathered full segment in buffer row `row` against segment `seg` of the planes.
+__device__ __forceinline__ double accumulate_planes(const float* wbuf, unsigned row, const double* qseg, int nseg,
+                                                    int seg, double s) {
+    const unsigned rk = row_key_at(wbuf, row);
+    const uint32_t* qh = reinterpret_cast<const uint32_t*>(qseg) + seg * kQHiPitch;
+    const uint4 lw = *reinterpret_cast<const uint4*>(q_lo_plane(qseg, nseg) + seg * 4);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float4 v = lds128(rk ^ (static_cast<unsigned>(c) << 4));
+        const float ve[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int k = c * 4 + e, w = k / 10, p = k % 10;
+            const uint32_t word = w == 0 ? lw.x : (w == 1 ? lw.y : (w == 2 ? lw.z : lw.w));
+            const uint32_t l = (word << (29 - 3 * p)) & 0xE0000000u;
+            const double q = __hiloint2double(static_cast<int>(qh[k]), static_cast<int>(l));
+            s = sq_diff_acc(s, ve[e], q);
+        }
+    }
+    return s;
+}
+
 constexpr int kQPitchF = 36;  // floats per segment slot of the fp32-staged query
 
 __device__ __forceinline__ void stage_query_f32(float* qseg, const Seg* segs, int nseg, const float* q) {

@@ -34,9 +34,10 @@ def test_full_size_vs_oracle(eng, orc, cfgid, nq):
     K, nprobe = cfg.K, cfg.nprobe
     for mode in ("ad-split", "fd"):
         res = eng.ivf_query_batch(idx, qt, q, K, nprobe, eng.IvfMode(MODE_ID[mode]))
-        step = eng.search_plan(idx, K, nprobe, eng.IvfMode(MODE_ID[mode]))["step"]
+        plan = eng.search_plan(idx, K, nprobe, eng.IvfMode(MODE_ID[mode]))
+        step, lag = plan["step"], (2 if plan["lag"] else 0)  # overlapped chunks == the oracle's lag 2
         for i in range(q.shape[0]):
-            ids, dists, stats = orc.ivf_query(lay, qt[i], q[i], K, nprobe, mode, 2.1, 32, K, step)
+            ids, dists, stats = orc.ivf_query(lay, qt[i], q[i], K, nprobe, mode, 2.1, 32, K, step, lag=lag)
             c = int(res.counts[i])
             assert c == len(ids)
             np.testing.assert_array_equal(res.ids[i, :c], ids, err_msg=f"{mode} q={i}")

@@ -642,11 +642,13 @@ def test_ivf_overlapped_chunks_bitexact(eng, orc, case, warps):
             for nprobe in (2, k):
                 opts = eng.search_opts(first=first, step=step, tile=-1, warps_per_cta=warps, walk=1, lag=1)
                 plan = eng.search_plan(idx, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg, opts=opts)
-                assert plan["lag"] == 1 and plan["first"] == first
+                # plans with an untested prefix (d1 spanning several segments) keep the
+                # pre-walk and the plain schedule; the plan says which one runs
+                assert plan["first"] == first and (plan["lag"] == 1 or d1 > dd)
                 res = eng.ivf_query_batch(idx, qt, qr, K, nprobe, eng.IvfMode(MODE_ID[mode]), cfg, opts=opts)
                 for qi in range(qt.shape[0]):
                     ids, dists, stats = orc.ivf_query(lay, qt[qi], qr[qi], K, nprobe, mode, 2.1, dd,
-                                                      plan["first"], plan["step"], lag=2)
+                                                      plan["first"], plan["step"], lag=2 if plan["lag"] else 0)
                     c = int(res.counts[qi])
                     assert c == len(ids), (mode, first, step, nprobe, qi)
                     np.testing.assert_array_equal(res.ids[qi, :c], ids, err_msg=f"{mode} {first}/{step} np={nprobe} q={qi}")
@@ -656,6 +658,13 @@ def test_ivf_overlapped_chunks_bitexact(eng, orc, case, warps):
     # where the plan cannot overlap (the FD walk pre-walks its untested prefix) lag is ignored
     plan = eng.search_plan(idx, K, 2, eng.IvfMode.kFd, cfg, opts=eng.search_opts(lag=1))
     assert plan["lag"] == 0
+    # default options: overlapped from 8 segments when the engine also picks the schedule;
+    # a pinned schedule, a probe range or lag = -1 keep the plain one
+    auto = eng.search_plan(idx, K, k, eng.IvfMode.kAdSplit, cfg)["lag"]
+    assert auto == (1 if (d1 <= dd and (d + dd - 1) // dd >= 8) else 0)
+    assert eng.search_plan(idx, K, k, eng.IvfMode.kAdSplit, cfg, opts=eng.search_opts(step=64))["lag"] == 0
+    assert eng.search_plan(idx, K, k, eng.IvfMode.kAdSplit, cfg, opts=eng.search_opts(lag=-1))["lag"] == 0
+    assert eng.search_plan(idx, K, k, eng.IvfMode.kAdSplit, cfg, opts=eng.search_opts(probe_lo=1))["lag"] == 0
 
 
 def test_ivf_long_lists_default_path_bitexact(eng, orc):

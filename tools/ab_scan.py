@@ -32,7 +32,7 @@ def main():
             args.step = int(v.split("step=")[1].split("+")[0]) if "step=" in v else 0
             args.warps = int(v.split("warps=")[1].split("+")[0]) if "warps=" in v else 0
             args.walk = 2 if "f32" in v else (1 if "exact" in v else 0)
-            args.lag = 1 if "lag" in v else 0
+            args.lag = -1 if "nolag" in v else (1 if "lag" in v else 0)
             M = bench.measure(S, cfg, cfg.nprobe, args, D, log, a.steps)
             row = {"variant": v, "rep": rep, "qps": M["value"], "scan_ms": M["stages_ms"]["scan"],
                    "frac": M["roofline"]["frac"], "sm_mhz": M["clocks"]["sm_mhz"],
