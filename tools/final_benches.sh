@@ -11,4 +11,9 @@ run cfg3 --config 3
 run transform --mode transform --steps 5 --warmup 3
 run dco --mode dco --steps 3 --warmup 3
 run theory --mode theory --steps 3 --warmup 3
-run cfg5 --config 5 --steps 3 --warmup 3
+run cfg2 --config 2
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/final/rc.txt
+# launch list of the default command's timed region (the scan's share of the step)
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" --csv \
+  --log-file gpurun_out/final/launches_cfg5.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extra \
+  > gpurun_out/final/launches.log 2>&1; echo "launches rc=$?" >> gpurun_out/final/rc.txt
