@@ -574,6 +574,7 @@ def extra_config(args, D, log, cid):
            "unit": "queries/s", "ms_per_step": M["ms_per_step"], "steps": max(3, args.steps // 2),
            "recall_at_k": M["recall_at_k"], "e2e": M["e2e"], "roofline": M["roofline"],
            "stages_ms": M["stages_ms"], "dims_fraction": M["dims_fraction"], "clocks": M["clocks"],
+           "threshold_refresh": M["threshold_refresh"], "overlapped_chunks": M["overlapped_chunks"],
            "gpu_fd": gpu_mode_line(S, cfg, cfg.nprobe, "fd")}
     # north-star subsystem 1 delta: the default rotates the query batch on the tensor cores
     # (3xTF32 tcgen05, rotate_mode 2); the same step with the exact fp64 rotation (0), whose
