@@ -251,6 +251,17 @@ constexpr int kDeepShift = ADS_DEEP_SHIFT;  // a candidate takes at most 1 << kD
 #endif
 constexpr int kDeepMinSeg = ADS_DEEP_MIN_NSEG;  // walks shorter than this have no tail to speak of
 
+// Set bits in flags[0, nw), the same value in every thread: each warp counts lane-parallel
+// (one word per lane and pass) and reduces, instead of every thread walking all the words.
+__device__ __forceinline__ int flag_count(const unsigned* flags, int nw) {
+    int c = 0;
+    for (int b = 0; b < nw; b += 32) {
+        const int i = b + static_cast<int>(lane_id());
+        c += __reduce_add_sync(kFull, i < nw ? __popc(flags[i]) : 0);
+    }
+    return c;
+}
+
 struct SearchShared {
     double r, r_sq;
     int q, stop, total, next, cnt, pnext;
@@ -961,7 +972,7 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
                 // order and arithmetic (dco.hpp:130-150; split resume at d1, ivf.cpp:389-400)
                 const int nw = (hi - lo + 31) >> 5;
                 int nv = 0;
-                for (int w = 0; w < nw; ++w) nv += __popc(vflag[w]);
+                nv = flag_count(vflag, nw);
                 for (int k = threadIdx.x; k < nv; k += blockDim.x) {
                     int w = 0, c = k;
                     for (;; ++w) {
@@ -1009,7 +1020,7 @@ __global__ void __maxnreg__(F32 ? 56 : 64) ivf_search_kernel(SearchLaunch a, int
             // many -> the whole CTA, ties or oversize -> one by one
             const int n = hi - lo;
             int npos = 0;
-            for (int w = 0; w < (n + 31) >> 5; ++w) npos += __popc(pflag[w]);
+            npos = flag_count(pflag, (n + 31) >> 5);
             int seq = -1;  // >= 0: offer pend[0, seq) sequentially (compacted batch)
             if (npos > 32 && n <= 2 * static_cast<int>(blockDim.x) && sh.cnt <= 2 * static_cast<int>(blockDim.x)) {
                 const int rc = cta_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n, wc);
@@ -1351,7 +1362,7 @@ __global__ void __maxnreg__(64) ivf_search_lag_kernel(SearchLaunch a, int chunk_
             const unsigned* pflag = pflag2 + pw * pw32;
             const int n = hi - lo;
             int npos = 0;
-            for (int k = 0; k < (n + 31) >> 5; ++k) npos += __popc(pflag[k]);
+            npos = flag_count(pflag, (n + 31) >> 5);
             int seq = -1;
             if (npos > 32 && n <= 2 * static_cast<int>(blockDim.x) && sh.cnt <= 2 * static_cast<int>(blockDim.x)) {
                 const int rc = cta_merge_chunk(topd, topi, sh, a.K, pend_d, pend_i, pflag, n, wc);
